@@ -1,0 +1,651 @@
+// oracle.cpp -- TEST INFRASTRUCTURE ONLY (see oracle.h).
+//
+// A plain CPU replay of Zeus's batch-size / power-limit optimiser, one
+// trial at a time, in the order the paper states it:
+//   step 1  power-limit optimiser, Eq. 7, §4.2
+//   step 2  pruning (Alg. 3) then Gaussian Thompson
+//           sampling (Alg. 1)
+//   step 3  trace lookup: the training trace
+//   step 4  early stopping at β·min_t C_t and Observe (Alg. 2,
+//           P:L494-506, window P:L655)
+// Numerics follow the contract NC-1..NC-9 of DESIGN.md §4 literally:
+// compiled with -O2 -ffp-contract=off, every fma written out, no libm
+// transcendental is ever called (zlog / zsincospi below are the contract
+// functions, written from fdlibm's published e_log.c / k_sin.c / k_cos.c).
+//
+// This file shares nothing with the CUDA path.  Nothing in it is tuned.
+
+#include "oracle.h"
+
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <limits>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+// ---------------------------------------------------------------- bits
+double bits_to_double(uint64_t u) { double d; std::memcpy(&d, &u, 8); return d; }
+uint64_t double_to_bits(double d) { uint64_t u; std::memcpy(&u, &d, 8); return u; }
+int32_t high_word(double d) { return (int32_t)(double_to_bits(d) >> 32); }
+double with_high_word(double d, int32_t hi) {
+  uint64_t u = double_to_bits(d);
+  u = (u & 0xffffffffULL) | ((uint64_t)(uint32_t)hi << 32);
+  return bits_to_double(u);
+}
+double from_words(int32_t hi, uint32_t lo) {
+  return bits_to_double(((uint64_t)(uint32_t)hi << 32) | lo);
+}
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Salmon et al., "Parallel random numbers: as easy as 1, 2, 3" (SC'11);
+// multipliers and Weyl constants as published there (NC-3).
+void philox(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint32_t W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+  uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+  uint32_t k[2] = {key_in[0], key_in[1]};
+  for (int round = 0; round < 10; ++round) {
+    if (round > 0) { k[0] += W0; k[1] += W1; }
+    uint64_t p0 = (uint64_t)M0 * c[0];
+    uint64_t p1 = (uint64_t)M1 * c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k[0];
+    uint32_t n1 = lo1;
+    uint32_t n2 = hi0 ^ c[3] ^ k[1];
+    uint32_t n3 = lo0;
+    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+  }
+  out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+// ---------------------------------------------------------------- zlog
+// fdlibm e_log.c (__ieee754_log) for a positive normal x, with the two
+// shortcut branches (|f| < 2^-20 and k == 0) folded into the general
+// formulas (contract NC-3; the general formulas are the same algorithm).
+double zlog(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01;  // 3fe62e42 fee00000
+  const double ln2_lo = 1.90821492927058770002e-10;  // 3dea39ef 35793c76
+  const double Lg1 = 6.666666666666735130e-01;       // 3FE55555 55555593
+  const double Lg2 = 3.999999999940941908e-01;       // 3FD99999 9997FA04
+  const double Lg3 = 2.857142874366239149e-01;       // 3FD24924 94229359
+  const double Lg4 = 2.222219843214978396e-01;       // 3FCC71C5 1D8E78AF
+  const double Lg5 = 1.818357216161805012e-01;       // 3FC74664 96CB03DE
+  const double Lg6 = 1.531383769920937332e-01;       // 3FC39A09 D078C69F
+  const double Lg7 = 1.479819860511658591e-01;       // 3FC2F112 DF3E5244
+  int32_t hx = high_word(x);
+  int32_t k = (hx >> 20) - 1023;
+  hx &= 0x000fffff;
+  int32_t i = (hx + 0x95f64) & 0x100000;
+  x = with_high_word(x, hx | (i ^ 0x3ff00000));   // normalise x or x/2
+  k += (i >> 20);
+  double f = x - 1.0;
+  double s = f / (2.0 + f);
+  double dk = (double)k;
+  double z = s * s;
+  i = hx - 0x6147a;
+  double w = z * z;
+  int32_t j = 0x6b851 - hx;
+  double t1 = w * (Lg2 + w * (Lg4 + w * Lg6));
+  double t2 = z * (Lg1 + w * (Lg3 + w * (Lg5 + w * Lg7)));
+  i |= j;
+  double R = t2 + t1;
+  if (i > 0) {
+    double hfsq = 0.5 * f * f;
+    return dk * ln2_hi - ((hfsq - (s * (hfsq + R) + dk * ln2_lo)) - f);
+  }
+  return dk * ln2_hi - ((s * (f - R) - dk * ln2_lo) - f);
+}
+
+// ---------------------------------------------------------------- sin/cos kernels
+// fdlibm k_sin.c / k_cos.c for |x| <= pi/4, x + y the argument (iy = 1).
+double kernel_sin(double x, double y) {
+  const double S1 = -1.66666666666666324348e-01;  // BFC55555 55555549
+  const double S2 = 8.33333333332248946124e-03;   // 3F811111 1110F8A6
+  const double S3 = -1.98412698298579493134e-04;  // BF2A01A0 19C161D5
+  const double S4 = 2.75573137070700676789e-06;   // 3EC71DE3 57B1FE7D
+  const double S5 = -2.50507602534068634195e-08;  // BE5AE5E6 8A2B9CEB
+  const double S6 = 1.58969099521155010221e-10;   // 3DE5D93A 5ACFD57C
+  double z = x * x;
+  double v = z * x;
+  double r = S2 + z * (S3 + z * (S4 + z * (S5 + z * S6)));
+  return x - ((z * (0.5 * y - v * r) - y) - v * S1);
+}
+
+double kernel_cos(double x, double y) {
+  const double C1 = 4.16666666666666019037e-02;   // 3FA55555 5555554C
+  const double C2 = -1.38888888888741095749e-03;  // BF56C16C 16C15177
+  const double C3 = 2.48015872894767294178e-05;   // 3EFA01A0 19CB1590
+  const double C4 = -2.75573143513906633035e-07;  // BE927E4F 809C52AD
+  const double C5 = 2.08757232129817482790e-09;   // 3E21EE9E BDB4B1C4
+  const double C6 = -1.13596475577881948265e-11;  // BDA8FAE9 BE8838D4
+  int32_t ix = high_word(x) & 0x7fffffff;
+  double z = x * x;
+  double r = z * (C1 + z * (C2 + z * (C3 + z * (C4 + z * (C5 + z * C6)))));
+  if (ix < 0x3FD33333) return 1.0 - (0.5 * z - (z * r - x * y));  // |x| < 0.3
+  double qx;
+  if (ix > 0x3fe90000) qx = 0.28125;                               // |x| > 0.78125
+  else qx = from_words(ix - 0x00200000, 0u);                       // |x|/4
+  double hz = 0.5 * z - qx;
+  double a = 1.0 - qx;
+  return a - (hz - (z * r - x * y));
+}
+
+// sin(pi*x), cos(pi*x) for x = m / 2^51, 0 <= m < 2^52 (i.e. x = 2v, v in [0,1)).
+// The reduction x = n/2 + f, |f| <= 1/4, is done exactly in integers; pi*f is
+// carried as a double-double (contract NC-3).
+void zsincospi(uint64_t m, double *s_out, double *c_out) {
+  const double PI = 3.14159265358979311600e+00;     // 400921FB 54442D18
+  const double PI_LO = 1.22464679914735320717e-16;  // 3CA1A626 33145C07
+  int64_t n = (int64_t)((m + (1ULL << 49)) >> 50);          // round(2x), 0..4
+  int64_t jj = (int64_t)m - n * (int64_t)(1ULL << 50);      // |jj| <= 2^49
+  double f = (double)jj * 4.44089209850062616169e-16;       // * 2^-51, exact
+  double a = f * PI;
+  double a_lo = std::fma(f, PI, -a) + f * PI_LO;
+  double sf = kernel_sin(a, a_lo);
+  double cf = kernel_cos(a, a_lo);
+  double s, c;
+  switch ((int)(n & 3)) {
+    case 0: s = sf; c = cf; break;
+    case 1: s = cf; c = -sf; break;
+    case 2: s = -sf; c = -cf; break;
+    default: s = -cf; c = sf; break;
+  }
+  *s_out = s; *c_out = c;
+}
+
+// u1 in (0,1], v in [0,1) from two 64-bit words (NC-3).
+void uniforms(uint64_t w0, uint64_t w1, double *u1, double *v) {
+  *u1 = 2.0 - bits_to_double(0x3FF0000000000000ULL | (w0 >> 12));
+  *v = bits_to_double(0x3FF0000000000000ULL | (w1 >> 12)) - 1.0;
+}
+
+// The Box-Muller pair for arms (2k, 2k+1) of trial i at recurrence t (NC-3).
+void normal_pair(uint64_t seed, int64_t trial, int32_t t, int32_t k, double *z0, double *z1) {
+  uint32_t ctr[4] = {(uint32_t)t, 0x01000000u | (uint32_t)k, (uint32_t)(uint64_t)trial,
+                     (uint32_t)((uint64_t)trial >> 32)};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t x[4];
+  philox(ctr, key, x);
+  uint64_t w0 = ((uint64_t)x[1] << 32) | x[0];
+  uint64_t w1 = ((uint64_t)x[3] << 32) | x[2];
+  double u1, v;
+  uniforms(w0, w1, &u1, &v);
+  double r = std::sqrt(-2.0 * zlog(u1));
+  double s, c;
+  zsincospi(w1 >> 12, &s, &c);   // 2*pi*v with v = (w1>>12) / 2^52
+  *z0 = r * c;
+  *z1 = r * s;
+}
+
+// Which of the K recorded seeds a run replays (Q15 / NC-3).
+uint32_t replica(uint64_t seed, int64_t trial, int32_t t, int32_t K) {
+  uint32_t ctr[4] = {(uint32_t)t, 0x02000000u, (uint32_t)(uint64_t)trial,
+                     (uint32_t)((uint64_t)trial >> 32)};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t x[4];
+  philox(ctr, key, x);
+  return (uint32_t)(((uint64_t)x[0] * (uint64_t)(uint32_t)K) >> 32);
+}
+
+// ---------------------------------------------------------------- Observe (Alg. 2)
+// One arm's belief.  Var(C_b) and Sum(C_b) of Alg. 2 are kept as
+// sums shifted by the arm's first observation (NC-6); the window of the N most
+// recent observations is an explicit queue.
+struct Arm {
+  std::deque<double> window;   // observations currently counted
+  int64_t cnt = 0;             // observations ever
+  double sh = 0.0, S1 = 0.0, S2 = 0.0;
+  double mu = 0.0, sigma = 0.0;
+  bool profiled = false;
+};
+
+struct Prior { double prec0, pm0; };
+
+Prior make_prior(double prior_mean, double prior_var) {
+  Prior p;
+  p.prec0 = std::isinf(prior_var) ? 0.0 : 1.0 / prior_var;   // flat prior: P:L529
+  p.pm0 = prior_mean * p.prec0;
+  return p;
+}
+
+// returns true when the posterior was (re)computed (n >= 2)
+bool observe(Arm &a, double x, int32_t window, const Prior &pr, double *s2_out, double *var_out) {
+  if (a.cnt == 0) a.sh = x;
+  if (window > 0 && (int32_t)a.window.size() == window) {   // forget the oldest
+    double y = a.window.front();
+    a.window.pop_front();
+    double dy = y - a.sh;
+    a.S1 = a.S1 - dy;
+    a.S2 = a.S2 - dy * dy;
+  }
+  double d = x - a.sh;                                       // C_b <- C_b ∪ {C}
+  a.S1 = a.S1 + d;
+  a.S2 = a.S2 + d * d;
+  a.window.push_back(x);
+  a.cnt += 1;
+  int64_t n = (int64_t)a.window.size();
+  if (n < 2) return false;
+  double dn = (double)n;
+  double mean = a.sh + a.S1 / dn;
+  double s2 = (a.S2 - (a.S1 * a.S1) / dn) / (dn - 1.0);     // σ̃² = Var(C_b), n-1 divisor
+  double fl = 1e-12 * (1.0 + mean * mean);
+  if (!(s2 >= fl)) s2 = fl;                                 // zero-variance floor (R-Q7)
+  double q = 1.0 / s2;
+  double var = 1.0 / (pr.prec0 + dn * q);                   // σ̂² = (1/σ̂0² + |C_b|/σ̃²)^-1
+  double sum = dn * a.sh + a.S1;                             // Sum(C_b)
+  a.mu = var * (pr.pm0 + sum * q);                          // μ̂ = σ̂²(μ̂0/σ̂0² + Sum/σ̃²)
+  a.sigma = std::sqrt(var);
+  if (s2_out) *s2_out = s2;
+  if (var_out) *var_out = var;
+  return true;
+}
+
+// ---------------------------------------------------------------- step 1
+struct Tables {
+  int B = 0, P = 0, S = 0;
+  std::vector<int32_t> pstar;
+  std::vector<double> c1, t1, e1, cP, tP, eP;
+  std::vector<double> ebar, regret, opt;
+  std::vector<int32_t> opt_arm;
+};
+
+void step1(const oracle_trace &tr, const oracle_cell &cell, Tables &T) {
+  const int B = tr.num_batch_sizes, P = tr.num_power_limits, S = tr.num_slices, K = tr.replicas;
+  const double eta = cell.eta, MP = tr.max_power_w;
+  T.B = B; T.P = P; T.S = S;
+  T.pstar.assign(B, 0);
+  T.c1.assign(B, 0); T.t1.assign(B, 0); T.e1.assign(B, 0);
+  T.cP.assign(B, 0); T.tP.assign(B, 0); T.eP.assign(B, 0);
+  for (int b = 0; b < B; ++b) {
+    const double *A = tr.avg_power_w + (size_t)b * P;
+    const double *Th = tr.throughput_eps + (size_t)b * P;
+    // Eq. 7: EpochCost(b) = min_p (η·AvgPower + (1-η)·MAXPOWER) / Throughput
+    double best = std::numeric_limits<double>::infinity();
+    int arg = 0;
+    for (int p = 0; p < P; ++p) {
+      double num = (eta * A[p]) + ((1.0 - eta) * MP);
+      double c = num / Th[p];
+      if (c < best) { best = c; arg = p; }       // first minimum: smaller p wins ties
+    }
+    T.pstar[b] = arg;
+    T.c1[b] = best;
+    T.t1[b] = 1.0 / Th[arg];
+    T.e1[b] = A[arg] / Th[arg];
+    // JIT profiling epoch: one equal-work slice per power limit
+    double st = 0.0, se = 0.0;
+    for (int p = 0; p < P; ++p) {
+      st = st + 1.0 / Th[p];
+      se = se + A[p] / Th[p];
+    }
+    T.tP[b] = st / (double)P;
+    T.eP[b] = se / (double)P;
+    T.cP[b] = (eta * T.eP[b]) + (((1.0 - eta) * MP) * T.tP[b]);
+  }
+  // known optimum per slice: min over (b,p) of Epochs(b)*c(b,p)
+  T.ebar.assign((size_t)S * B, 0);
+  T.regret.assign((size_t)S * B, 0);
+  T.opt.assign(S, 0);
+  T.opt_arm.assign(S, -1);
+  for (int s = 0; s < S; ++s) {
+    std::vector<int64_t> count(B, 0);
+    double best = std::numeric_limits<double>::infinity();
+    int barg = -1;
+    for (int b = 0; b < B; ++b) {
+      int64_t sum = 0;
+      for (int k = 0; k < K; ++k) {
+        int32_t E = tr.epochs_to_target[((size_t)s * B + b) * K + k];
+        if (E > 0) { sum += E; count[b] += 1; }
+      }
+      double eb = count[b] > 0 ? (double)sum / (double)count[b] : (double)tr.max_epochs;
+      T.ebar[(size_t)s * B + b] = eb;
+      if (count[b] > 0) {
+        double v = eb * T.c1[b];
+        if (v < best) { best = v; barg = b; }
+      }
+    }
+    T.opt[s] = best;
+    T.opt_arm[s] = barg;
+    for (int b = 0; b < B; ++b)   // Eq. 9 with Epochs(b_t) read as its mean (R-Q12)
+      T.regret[(size_t)s * B + b] = T.ebar[(size_t)s * B + b] * T.c1[b] - best;
+  }
+}
+
+// ---------------------------------------------------------------- validation
+std::string validate(const oracle_trace &tr, const oracle_cell &cell) {
+  std::string e;
+  auto add = [&](const char *m) { if (!e.empty()) e += "; "; e += m; };
+  const int B = tr.num_batch_sizes, P = tr.num_power_limits;
+  if (B < 1) add("no batch sizes");
+  if (B > 32) add("more than 32 batch sizes");
+  if (P < 1) add("no power limits");
+  if (P > 64) add("more than 64 power limits");
+  if (B >= 1 && tr.batch_sizes) {
+    for (int b = 0; b < B; ++b) if (tr.batch_sizes[b] <= 0) { add("batch size not positive"); break; }
+    for (int b = 1; b < B; ++b) if (tr.batch_sizes[b] <= tr.batch_sizes[b - 1]) { add("batch sizes not strictly increasing"); break; }
+  }
+  if (tr.default_bs_index < 0 || tr.default_bs_index >= B) add("default batch size index out of range");
+  double pmax = 0.0;
+  if (P >= 1 && tr.power_limits_w) {
+    for (int p = 0; p < P; ++p) if (!(tr.power_limits_w[p] > 0.0)) { add("power limit not positive"); break; }
+    for (int p = 1; p < P; ++p) if (!(tr.power_limits_w[p] > tr.power_limits_w[p - 1])) { add("power limits not strictly increasing"); break; }
+    pmax = tr.power_limits_w[P - 1];
+  }
+  if (!(tr.max_power_w >= pmax) || !std::isfinite(tr.max_power_w)) add("max power below the largest power limit");
+  if (tr.max_epochs < 1) add("max_epochs < 1");
+  if (!(cell.eta >= 0.0 && cell.eta <= 1.0)) add("eta out of [0,1]");
+  if (!(cell.beta > 1.0)) add("beta must be > 1");
+  if (cell.window == 1 || cell.window < 0) add("window must be 0 (unbounded) or >= 2");
+  if (!(cell.prior_var > 0.0)) add("prior variance must be > 0");
+  if (!std::isfinite(cell.prior_mean)) add("prior mean not finite");
+  if (B >= 1 && P >= 1 && B <= 32 && P <= 64) {
+    for (int i = 0; i < B * P; ++i)
+      if (!(tr.avg_power_w[i] > 0.0) || !std::isfinite(tr.avg_power_w[i])) { add("average power not positive"); break; }
+    for (int i = 0; i < B * P; ++i)
+      if (!(tr.avg_power_w[i] <= tr.max_power_w)) { add("average power above max power"); break; }
+    for (int i = 0; i < B * P; ++i)
+      if (!(tr.throughput_eps[i] > 0.0) || !std::isfinite(tr.throughput_eps[i])) { add("throughput not positive"); break; }
+  }
+  if (tr.num_slices < 1) add("num_slices < 1");
+  if (tr.replicas < 1) add("replicas < 1");
+  if (e.empty()) {
+    const int S = tr.num_slices, K = tr.replicas;
+    for (size_t i = 0; i < (size_t)S * B * K; ++i)
+      if (tr.epochs_to_target[i] > tr.max_epochs) { add("epochs_to_target above max_epochs"); break; }
+    for (int s = 0; s < S; ++s) {
+      bool any = false;
+      for (int i = 0; i < B * K; ++i) any |= tr.epochs_to_target[(size_t)s * B * K + i] > 0;
+      if (!any) { add("a slice has no converged replica on any arm"); break; }
+    }
+  }
+  return e;
+}
+
+// ---------------------------------------------------------------- one trial
+int lowest_bit(uint32_t m) { for (int b = 0; b < 32; ++b) if (m & (1u << b)) return b; return -1; }
+int highest_bit(uint32_t m) { for (int b = 31; b >= 0; --b) if (m & (1u << b)) return b; return -1; }
+uint32_t below(int c) { return c <= 0 ? 0u : ((1u << c) - 1u); }
+uint32_t above(int c) { return c >= 31 ? 0u : ~((2u << c) - 1u); }
+
+enum Step { START, DOWN, UP };
+
+struct TrialResult {
+  double tot_cost = 0, tot_energy = 0, tot_time = 0;
+  uint64_t digest = 0xcbf29ce484222325ULL;
+  int32_t n_stop = 0, final_arm = -1;
+};
+
+struct Counters { int64_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0}; };
+
+void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T, int32_t R,
+               int64_t trial, TrialResult &res, double *curves, uint32_t *log, double *clog,
+               double *elog, double *tlog, Counters &cnt) {
+  const int B = tr.num_batch_sizes, S = tr.num_slices, K = tr.replicas;
+  const Prior pr = make_prior(cell.prior_mean, cell.prior_var);
+  std::vector<Arm> arm(B);
+  double best = std::numeric_limits<double>::infinity();   // min_t C_t
+
+  // Alg. 3 state
+  bool in_ts = false;
+  int round = 1;
+  Step step = START;
+  uint32_t cand = (B == 32) ? 0xffffffffu : ((1u << B) - 1u);
+  int start = tr.default_bs_index;
+  int cursor = start;
+  uint32_t surv = 0, ts_set = 0;
+  double r1_cost = std::numeric_limits<double>::infinity();
+  int r1_arm = -1;
+
+  for (int32_t t = 0; t < R; ++t) {
+    const int s = (int)(((int64_t)t * S) / R);   // slice of recurrence t (R-Q19)
+    // ---- step 2: decide b_t
+    int b;
+    const bool ts_dec = in_ts;   // phase at decision time (flag bit 3)
+    if (!in_ts) {
+      if (step == START) b = start;
+      else if (step == DOWN) b = highest_bit(cand & below(cursor));
+      else b = lowest_bit(cand & above(cursor));
+      cnt.c[5] += 1;
+    } else {
+      b = -1;
+      for (int a = 0; a < B; ++a)           // arms without a variance estimate first (R-Q6)
+        if ((ts_set & (1u << a)) && (int)arm[a].window.size() < 2) { b = a; break; }
+      if (b < 0) {
+        // Alg. 1: θ̂_b ~ N(μ̂_b, σ̂_b²) for every b, b* = argmin θ̂_b
+        double best_theta = std::numeric_limits<double>::infinity();
+        for (int k = 0; 2 * k < B; ++k) {
+          uint32_t pairmask = (ts_set >> (2 * k)) & 3u;
+          if (!pairmask) continue;
+          double z[2];
+          normal_pair(cell.seed, trial, t, k, &z[0], &z[1]);
+          cnt.c[2] += 1;
+          for (int h = 0; h < 2; ++h) {
+            int a = 2 * k + h;
+            if (!(pairmask & (1u << h))) continue;
+            double theta = std::fma(arm[a].sigma, z[h], arm[a].mu);
+            cnt.c[3] += 1;
+            if (theta < best_theta) { best_theta = theta; b = a; }
+          }
+        }
+        cnt.c[1] += 1;
+      } else {
+        cnt.c[6] += 1;
+      }
+    }
+    // ---- step 1 result: the power limit accompanying b
+    const int p = T.pstar[b];
+    // ---- step 3: replay one recorded run of b
+    const uint32_t r = replica(cell.seed, trial, t, K);
+    const int32_t E = tr.epochs_to_target[((size_t)s * B + b) * K + r];
+    const int32_t E_run = E > 0 ? E : tr.max_epochs;
+    double c0, t0, e0;
+    bool profiled_now = false;
+    if (tr.charge_profiling && !arm[b].profiled) {   // JIT profiling epoch
+      c0 = T.cP[b]; t0 = T.tP[b]; e0 = T.eP[b]; profiled_now = true;
+    } else {
+      c0 = T.c1[b]; t0 = T.t1[b]; e0 = T.e1[b];
+    }
+    arm[b].profiled = true;
+    const double em1 = (double)(E_run - 1);
+    const double C_full = c0 + em1 * T.c1[b];
+    const double T_full = t0 + em1 * T.t1[b];
+    const double En_full = e0 + em1 * T.e1[b];
+    // ---- step 4: early stop at β·min_t C_t
+    const double thr = cell.beta * best;
+    double C, Tm, En;
+    bool stopped = false;
+    if (C_full > thr) {
+      stopped = true;
+      C = thr;
+      if (thr <= c0) {
+        double phi = thr / c0;
+        Tm = phi * t0;
+        En = phi * e0;
+      } else {
+        double phi = (thr - c0) / T.c1[b];
+        Tm = t0 + phi * T.t1[b];
+        En = e0 + phi * T.e1[b];
+      }
+    } else {
+      C = C_full; Tm = T_full; En = En_full;
+    }
+    const bool converged = (E > 0) && !stopped;
+    if (converged && !(C >= best)) best = C;
+    // Alg. 2 Observe: every run is observed, stopped runs at the threshold (R-Q3)
+    if (observe(arm[b], C, cell.window, pr, nullptr, nullptr)) cnt.c[7] += 1;
+    cnt.c[0] += 1;
+    if (stopped) cnt.c[4] += 1;
+
+    // ---- Alg. 3 bookkeeping
+    if (!in_ts) {
+      if (converged) {
+        surv |= 1u << b;
+        if (round == 1 && (C < r1_cost || (C == r1_cost && b < r1_arm))) { r1_cost = C; r1_arm = b; }
+      }
+      bool end_round = false;
+      if (step == START) { step = DOWN; cursor = start; }
+      else if (step == DOWN) { if (converged) cursor = b; else { step = UP; cursor = start; } }
+      else { if (converged) cursor = b; else end_round = true; }
+      if (!end_round && step == DOWN && (cand & below(cursor)) == 0) { step = UP; cursor = start; }
+      if (!end_round && step == UP && (cand & above(cursor)) == 0) end_round = true;
+      if (end_round) {
+        if (surv == 0) surv = 1u << start;           // R-Q23
+        if (round == 1) {
+          cand = surv;
+          if (r1_arm >= 0) start = r1_arm;           // b0 <- b with smallest cost observed
+          surv = 0;
+          round = 2;
+          step = START;
+          cursor = start;
+        } else {
+          in_ts = true;
+          ts_set = surv;
+        }
+      }
+    }
+
+    // ---- accumulate (Eq. 4, Eqs. 8-9)
+    const uint32_t flags = (stopped ? 1u : 0u) | (converged ? 2u : 0u) |
+                           (profiled_now ? 4u : 0u) | (ts_dec ? 8u : 0u);
+    res.tot_cost += C;
+    res.tot_energy += En;
+    res.tot_time += Tm;
+    if (stopped) res.n_stop += 1;
+    res.final_arm = b;
+    const uint8_t bytes[3] = {(uint8_t)b, (uint8_t)p, (uint8_t)flags};   // NC-9 digest
+    for (int q = 0; q < 3; ++q) { res.digest ^= bytes[q]; res.digest *= 0x100000001b3ULL; }
+    if (curves) {
+      double *row = curves + (size_t)t * 7;
+      row[0] += C;
+      row[1] += En;
+      row[2] += Tm;
+      row[3] += T.regret[(size_t)s * B + b];
+      row[4] += stopped ? 1.0 : 0.0;
+      row[5] += (b == T.opt_arm[s]) ? 1.0 : 0.0;
+      row[6] += ts_dec ? 1.0 : 0.0;
+    }
+    if (log) log[t] = (uint32_t)b | ((uint32_t)p << 8) | (flags << 16);
+    if (clog) clog[t] = C;
+    if (elog) elog[t] = En;
+    if (tlog) tlog[t] = Tm;
+  }
+}
+
+}  // namespace
+
+// ======================================================================== C API
+extern "C" {
+
+int oracle_validate(const oracle_trace *tr, const oracle_cell *cell, char *msg, int32_t msglen) {
+  std::string e = validate(*tr, *cell);
+  if (msg && msglen > 0) {
+    std::strncpy(msg, e.c_str(), (size_t)msglen - 1);
+    msg[msglen - 1] = 0;
+  }
+  return e.empty() ? 0 : 1;
+}
+
+int oracle_step1(const oracle_trace *tr, const oracle_cell *cell, oracle_tables *out) {
+  if (!validate(*tr, *cell).empty()) return 1;
+  Tables T;
+  step1(*tr, *cell, T);
+  const int B = T.B, S = T.S;
+  for (int b = 0; b < B; ++b) {
+    if (out->pstar) out->pstar[b] = T.pstar[b];
+    if (out->c1) out->c1[b] = T.c1[b];
+    if (out->t1) out->t1[b] = T.t1[b];
+    if (out->e1) out->e1[b] = T.e1[b];
+    if (out->c_prof) out->c_prof[b] = T.cP[b];
+    if (out->t_prof) out->t_prof[b] = T.tP[b];
+    if (out->e_prof) out->e_prof[b] = T.eP[b];
+  }
+  for (int s = 0; s < S; ++s) {
+    if (out->opt) out->opt[s] = T.opt[s];
+    if (out->opt_arm) out->opt_arm[s] = T.opt_arm[s];
+    for (int b = 0; b < B; ++b) {
+      if (out->ebar) out->ebar[(size_t)s * B + b] = T.ebar[(size_t)s * B + b];
+      if (out->regret) out->regret[(size_t)s * B + b] = T.regret[(size_t)s * B + b];
+    }
+  }
+  return 0;
+}
+
+int oracle_replay(const oracle_trace *tr, const oracle_cell *cell, int32_t R,
+                  const int64_t *trials, int64_t n, int32_t threads, oracle_out *out) {
+  if (!validate(*tr, *cell).empty() || R < 0 || n < 0) return 1;
+  Tables T;
+  step1(*tr, *cell, T);
+  if (threads < 1) threads = 1;
+  if ((int64_t)threads > n) threads = (int32_t)(n > 0 ? n : 1);
+  std::vector<std::vector<double>> part(threads, std::vector<double>(out->curves ? (size_t)R * 7 : 0, 0.0));
+  std::vector<Counters> pc(threads);
+  auto worker = [&](int w) {
+    for (int64_t j = w; j < n; j += threads) {   // trials are independent; one task each
+      TrialResult res;
+      size_t off = (size_t)j * (size_t)R;
+      run_trial(*tr, *cell, T, R, trials[j], res, out->curves ? part[w].data() : nullptr,
+                out->log ? out->log + off : nullptr, out->cost_log ? out->cost_log + off : nullptr,
+                out->energy_log ? out->energy_log + off : nullptr,
+                out->time_log ? out->time_log + off : nullptr, pc[w]);
+      if (out->tot_cost) out->tot_cost[j] = res.tot_cost;
+      if (out->tot_energy) out->tot_energy[j] = res.tot_energy;
+      if (out->tot_time) out->tot_time[j] = res.tot_time;
+      if (out->digest) out->digest[j] = res.digest;
+      if (out->n_stop) out->n_stop[j] = res.n_stop;
+      if (out->final_arm) out->final_arm[j] = res.final_arm;
+    }
+  };
+  if (threads == 1) {
+    worker(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int w = 0; w < threads; ++w) pool.emplace_back(worker, w);
+    for (auto &th : pool) th.join();
+  }
+  if (out->curves) {
+    for (size_t i = 0; i < (size_t)R * 7; ++i) out->curves[i] = 0.0;
+    for (int w = 0; w < threads; ++w)
+      for (size_t i = 0; i < (size_t)R * 7; ++i) out->curves[i] += part[w][i];
+  }
+  if (out->counters) {
+    for (int q = 0; q < 8; ++q) {
+      out->counters[q] = 0;
+      for (int w = 0; w < threads; ++w) out->counters[q] += pc[w].c[q];
+    }
+  }
+  return 0;
+}
+
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  philox(ctr, key, out);
+}
+double oracle_zlog(double x) { return zlog(x); }
+void oracle_zsincospi(uint64_t m52, double *s, double *c) { zsincospi(m52, s, c); }
+void oracle_uniforms(uint64_t w0, uint64_t w1, double *u1, double *v) { uniforms(w0, w1, u1, v); }
+void oracle_normal_pair(uint64_t seed, int64_t trial, int32_t t, int32_t k, double *z0, double *z1) {
+  normal_pair(seed, trial, t, k, z0, z1);
+}
+uint32_t oracle_replica(uint64_t seed, int64_t trial, int32_t t, int32_t K) {
+  return replica(seed, trial, t, K);
+}
+int oracle_posterior(const double *xs, int32_t n, int32_t window, double prior_mean,
+                     double prior_var, double *mu, double *sigma, double *s2, double *var) {
+  Arm a;
+  Prior pr = make_prior(prior_mean, prior_var);
+  bool ok = false;
+  for (int32_t i = 0; i < n; ++i) ok = observe(a, xs[i], window, pr, s2, var);
+  if (!ok) return 1;
+  *mu = a.mu;
+  *sigma = a.sigma;
+  return 0;
+}
+int32_t oracle_hardware_threads(void) {
+  unsigned h = std::thread::hardware_concurrency();
+  return h == 0 ? 1 : (int32_t)h;
+}
+
+}  // extern "C"

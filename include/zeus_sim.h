@@ -1,0 +1,171 @@
+/*
+ * zeus_sim.h -- C ABI of the B200 batched replay of Zeus's optimiser.
+ *
+ * Zeus (You, Chung, Chowdhury, arXiv 2208.06102) picks, for every recurrence
+ * of a recurring DNN training job, a batch size b by Gaussian Thompson
+ * sampling after a pruning stage (Alg. 1-3) and the power limit p
+ * of that batch size by minimising the per-epoch cost of a JIT profile
+ * (Eq. 7), early-stopping runs whose cost is to exceed beta times
+ * the minimum cost seen.  The paper evaluates it by replaying a
+ * training trace and a power trace (§6.1).  This library runs
+ * that replay for many independent trials at once on one GPU: one call of
+ * zeus_sim_run is trials x R decisions for every cell.
+ *
+ * Citations: P:Lnnn = line of the paper's LaTeX; DESIGN.md §4 is
+ * the numerics contract (NC-1..NC-9) both this library and the CPU oracle
+ * follow, §3 the readings of passages the paper leaves open (R-Qn).
+ *
+ * Conventions (all calls):
+ *  - Every call returns zeus_status; ZEUS_OK = 0.  On failure
+ *    zeus_sim_last_error(sim) returns a message listing EVERY violated
+ *    invariant ("; "-separated), valid until the next call on that handle.
+ *    For a failed zeus_sim_create, the message is returned by
+ *    zeus_sim_last_error(NULL) (thread-local).
+ *  - Ownership: input arrays are read (and copied) before the call returns;
+ *    the handle owns all device memory until zeus_sim_destroy; results are
+ *    written only into caller-owned buffers.
+ *  - Async: zeus_sim_run enqueues work on the caller's CUDA stream and
+ *    returns; zeus_sim_results synchronises that stream first.
+ *  - Threading: a handle belongs to one thread at a time; distinct handles
+ *    may run concurrently on different streams or devices.
+ *  - Sharding: RNG counters use the GLOBAL trial index (NC-3), so per-trial
+ *    results do not depend on how [0, trials) is split across ranks.
+ *  - No CPU fallback: when no CUDA device is usable every call that would
+ *    launch work fails with ZEUS_E_CUDA.
+ */
+#ifndef ZEUS_SIM_H
+#define ZEUS_SIM_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZEUS_SIM_ABI_VERSION 1
+#define ZEUS_MAX_BATCH_SIZES 32
+#define ZEUS_MAX_POWER_LIMITS 64
+#define ZEUS_CURVE_QUANTITIES 7   /* cost, energy, time, pseudo-regret, n_stop, n_opt, n_ts */
+#define ZEUS_COUNTERS 8
+
+typedef enum {
+  ZEUS_OK = 0,
+  ZEUS_E_INVALID = 1,            /* an argument violates an invariant (message lists all) */
+  ZEUS_E_STATE = 2,              /* calls out of order (run before load_profile, ...) */
+  ZEUS_E_NO_CONVERGENT_ARM = 3,  /* a trace slice where no replica of any arm converges */
+  ZEUS_E_CUDA = 4,               /* CUDA runtime error (message has the CUDA string) */
+  ZEUS_E_NOMEM = 5,              /* device or host allocation failed */
+  ZEUS_E_UNSUPPORTED = 6         /* valid but outside this build's limits (B > 32, ...) */
+} zeus_status;
+
+typedef struct zeus_sim zeus_sim;   /* opaque; single owner */
+
+/* The recurring job ("a set of feasible batch sizes B and power limits P"). */
+typedef struct {
+  uint32_t struct_size;              /* = sizeof(zeus_job) (ABI guard) */
+  int32_t num_batch_sizes;           /* B = |𝓑|, 1..32 */
+  const int32_t *batch_sizes;        /* host [B], positive, strictly increasing */
+  int32_t default_bs_index;          /* b0 in [0,B): Alg. 3's starting batch size */
+  int32_t num_power_limits;          /* P = |𝓟|, 1..64 */
+  const double *power_limits_w;      /* host [P], positive, strictly increasing (watts) */
+  double max_power_w;                /* MAXPOWER of Eq. 2, >= max 𝓟 */
+  int32_t max_epochs;                /* >= 1: epochs a never-converging run is charged (R-Q16) */
+  int32_t charge_profiling;          /* 1: the first run of each arm pays the JIT profiling
+                                        epoch, one equal-work slice per power limit */
+} zeus_job;
+
+/* One sweep cell: the knobs η, β, N and the prior of Alg. 2. */
+typedef struct {
+  double eta;                        /* η in [0,1] (Eq. 2) */
+  double beta;                       /* β > 1, or +INFINITY = never early-stop */
+  int32_t window;                    /* N >= 2 most recent observations, 0 = unbounded */
+  double prior_mean;                 /* μ̂0 (Alg. 2) */
+  double prior_var;                  /* σ̂0² > 0; +INFINITY = flat prior */
+  uint64_t seed;                     /* Philox4x32-10 key (NC-3) */
+  int64_t trials;                    /* global trial count of this cell, >= 0 */
+} zeus_cell;
+
+typedef struct {
+  uint32_t struct_size;              /* = sizeof(zeus_run_opts) */
+  int32_t recurrences;               /* R >= 0; 0 = auto = 2|𝓑||𝓟| */
+  int64_t shard_begin, shard_end;    /* this rank's global trial range [begin, end) of
+                                        every cell, clipped to [0, trials); end < 0 = all */
+  int32_t log_mode;                  /* 0: no log; 1: per-decision log (4 B / decision) */
+  int32_t layout;                    /* 0: auto; 1: one thread per trial; 2: one lane group
+                                        per trial, lane = arm */
+} zeus_run_opts;
+
+/* Outputs.  Every pointer is caller-owned and may be NULL (skipped); each
+ * may point to host or device memory (detected per pointer).  Layouts are
+ * row-major; "shard" = shard_end - shard_begin after clipping. */
+typedef struct {
+  uint32_t struct_size;              /* = sizeof(zeus_results) */
+  /* per-recurrence curves summed over this shard's trials, [cells][R][7]:
+     q = 0 cost, 1 energy (J), 2 time (s), 3 pseudo-regret Ebar(b_t)c1(b_t) - opt
+     (Eq. 9 with Epochs read as the trace mean, R-Q12), 4 early stops, 5 decisions
+     equal to the known optimum, 6 decisions taken by Thompson sampling.
+     Counts are exact in fp64 (< 2^53), so the array can be all-reduced as is. */
+  double *curves;
+  /* per trial [cells][shard] */
+  double *tot_cost, *tot_energy, *tot_time;   /* summed in recurrence order (NC-8) */
+  uint64_t *digest;                           /* FNV-1a-64 over (b_t, p_t, flags) (NC-9) */
+  int32_t *n_stop;                            /* early stops of the trial */
+  int32_t *final_arm;                         /* b_{R-1} index (-1 if R = 0) */
+  /* step-1 tables (Eq. 7 and the JIT epoch) [cells][B] */
+  int32_t *pstar_index;
+  double *c1, *t1, *e1;                       /* cost / s / J per epoch at p*(b) */
+  double *c_prof, *t_prof, *e_prof;           /* cost / s / J of the profiling epoch */
+  /* known optimum per slice [cells][S] */
+  double *opt_cost;
+  int32_t *opt_arm;
+  /* per-decision log [cells][shard][R] (needs log_mode = 1):
+     arm | p_index << 8 | flags << 16, flags bit0 stopped, bit1 converged,
+     bit2 paid the profiling epoch, bit3 decided by Thompson sampling */
+  uint32_t *log;
+  /* instrumentation [8]: decisions, sampled TS decisions, normal pairs drawn,
+     normals used, early stops, pruning decisions, forced explorations,
+     posterior recomputations */
+  int64_t *counters;
+  /* timing of the last zeus_sim_run, CUDA events on the caller's stream:
+     step 1 (Eq. 7) kernel, replay kernel, curve-reduction kernel */
+  float step1_ms, replay_ms, reduce_ms;
+} zeus_results;
+
+/* Validates job, cells and opts (every violated invariant is reported),
+ * selects cuda_device, allocates device memory.  *out is NULL on failure. */
+zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t num_cells,
+                            const zeus_run_opts *opts, int32_t cuda_device, zeus_sim **out);
+
+/* The power trace and the training trace (§6.1):
+ *   avg_power_w     host [B][P], 0 < AvgPower(b,p) <= MAXPOWER
+ *   throughput_eps  host [B][P], Throughput(b,p) > 0 in epochs/s
+ *   epochs_to_target host [S][B][K] (S slices, K replicas); <= 0 = the run never
+ *                   reaches the target (R-Q16); every value <= max_epochs;
+ *                   every slice needs one converged replica on some arm.
+ * Copies them to the device and computes step 1 for every cell (Eq. 7 argmin,
+ * per-epoch and profiling constants, known optimum).  Synchronous. */
+zeus_status zeus_sim_load_profile(zeus_sim *sim, const double *avg_power_w,
+                                  const double *throughput_eps, int32_t num_slices,
+                                  int32_t replicas, const int32_t *epochs_to_target);
+
+/* Enqueues one pass of the whole path on cuda_stream (a cudaStream_t; NULL =
+ * the legacy default stream): step 1 for every cell, the replay of every
+ * (cell, shard trial) for R recurrences, and the curve reduction. */
+zeus_status zeus_sim_run(zeus_sim *sim, void *cuda_stream);
+
+/* Synchronises the run's stream and copies the requested outputs. */
+zeus_status zeus_sim_results(zeus_sim *sim, zeus_results *out);
+
+/* Frees the handle and its device memory; NULL is a no-op. */
+void zeus_sim_destroy(zeus_sim *sim);
+
+/* Message of the last failed call on sim (NULL: of the last failed create on
+ * this thread).  Never NULL; "" when there is none. */
+const char *zeus_sim_last_error(const zeus_sim *sim);
+
+/* R actually used (after auto), shard size, number of cells; any out may be NULL. */
+zeus_status zeus_sim_shape(const zeus_sim *sim, int32_t *recurrences, int64_t *shard,
+                           int32_t *num_cells, int32_t *num_batch_sizes, int32_t *num_slices);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

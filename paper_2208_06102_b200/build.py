@@ -1,0 +1,44 @@
+"""Builds the CUDA library in-tree: paper_2208_06102_b200/libzeus_sim.so (sm_100a).
+
+NC-1: --fmad=false so no multiply-add is contracted behind the contract's back;
+fp64 division and sqrt are IEEE round-to-nearest by default.
+"""
+from __future__ import annotations
+
+import glob
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libzeus_sim.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "--fmad=false",
+    "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
+    "-I", os.path.join(ROOT, "include"),
+]
+
+
+def sources():
+    return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh"))
+                  + [os.path.join(ROOT, "include", "zeus_sim.h")])
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    srcs = sources()
+    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(f) for f in srcs):
+        return LIB
+    cmd = [NVCC, *FLAGS, "-o", LIB, os.path.join(HERE, "csrc", "zeus_sim.cu"), "-lcudart"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+    with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as f:
+        f.write(r.stderr)
+    if verbose:
+        print(r.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force=True, verbose=True))

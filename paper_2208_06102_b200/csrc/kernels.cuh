@@ -1,0 +1,476 @@
+// kernels.cuh -- the sm_100a kernels of the replay.
+//
+//   step1_kernel   Eq. 7 argmin over the power profile + per-arm constants +
+//                  the known optimum per slice (a1 in SURVEY §8(a)).
+//   replay_kernel  steps 2-4 for every (trial, recurrence): pruning (Alg. 3),
+//                  Thompson sampling (Alg. 1), trace lookup, early stop
+//                  (P:L559), Observe (Alg. 2), curves + digests (a2..a7).
+//   curve_reduce   sums the atomic curve slots in a fixed order (a7).
+//
+// Layout: one thread per trial; the arm state of a trial lives
+// in shared memory as [field][arm][thread] so a warp's accesses hit 32
+// consecutive 8-byte words; the per-cell tables (arm constants, the trace
+// pool, pseudo-regret table) are staged once per block into shared memory
+// with a 1-D TMA bulk copy (cp.async.bulk) completing on an mbarrier.
+#pragma once
+#include <cstdint>
+
+#include "contract.cuh"
+
+namespace zs {
+
+constexpr int kQ = 7;             // curve quantities
+constexpr int kCounters = 8;
+
+struct ArmConst {                 // per (cell, arm), 64 B
+  double c1, t1, e1, cP, tP, eP;
+  int32_t pstar, pad0;
+  double pad1;
+};
+
+struct CellParam {                // per cell
+  double eta, beta, prec0, pm0;
+  int32_t window, pad;
+  uint32_t key0, key1;
+  int64_t begin, n, out_off;      // global first trial, shard size, offset into per-trial outputs
+};
+
+// ------------------------------------------------------------------ step 1
+struct Step1Args {
+  const double *A, *Th;           // [B][P]
+  const int32_t *pool;            // [S][B][K]
+  const CellParam *cells;
+  ArmConst *arms;                 // [cells][B]
+  double *regret;                 // [cells][reg_stride] (S*B used)
+  double *opt;                    // [cells][S]
+  int32_t *opt_arm;               // [cells][opt_stride] (S used)
+  int B, P, S, K, max_epochs, reg_stride, opt_stride;
+  double MP;
+};
+
+__global__ void step1_kernel(Step1Args a) {
+  const int cell = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const double eta = a.cells[cell].eta;
+  ArmConst *arms = a.arms + (size_t)cell * a.B;
+  for (int b = warp; b < a.B; b += nwarp) {
+    const double *A = a.A + (size_t)b * a.P;
+    const double *Th = a.Th + (size_t)b * a.P;
+    double bc = __longlong_as_double(0x7ff0000000000000ll);   // +inf
+    int bp = 0x7fffffff;
+    for (int p = lane; p < a.P; p += 32) {                      // Eq. 7, lanes over p
+      const double num = (eta * A[p]) + ((1.0 - eta) * a.MP);
+      const double c = num / Th[p];
+      if (c < bc) { bc = c; bp = p; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {                   // argmin, ties -> smaller p
+      const double oc = __shfl_xor_sync(0xffffffffu, bc, off);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, off);
+      if (oc < bc || (oc == bc && op < bp)) { bc = oc; bp = op; }
+    }
+    if (lane == 0) {
+      if (bp == 0x7fffffff) bp = 0;
+      ArmConst ac;
+      ac.c1 = bc;
+      ac.t1 = 1.0 / Th[bp];
+      ac.e1 = A[bp] / Th[bp];
+      double st = 0.0, se = 0.0;                                // JIT epoch, left-to-right (NC-2)
+      for (int p = 0; p < a.P; ++p) {
+        st = st + 1.0 / Th[p];
+        se = se + A[p] / Th[p];
+      }
+      ac.tP = st / (double)a.P;
+      ac.eP = se / (double)a.P;
+      ac.cP = (eta * ac.eP) + (((1.0 - eta) * a.MP) * ac.tP);
+      ac.pstar = bp;
+      ac.pad0 = 0;
+      ac.pad1 = 0.0;
+      arms[b] = ac;
+    }
+  }
+  __syncthreads();
+  for (int s = threadIdx.x; s < a.S; s += blockDim.x) {        // known optimum
+    double best = __longlong_as_double(0x7ff0000000000000ll);
+    int barg = -1;
+    for (int b = 0; b < a.B; ++b) {
+      long long sum = 0;
+      int cnt = 0;
+      for (int k = 0; k < a.K; ++k) {
+        const int E = a.pool[((size_t)s * a.B + b) * a.K + k];
+        if (E > 0) { sum += E; ++cnt; }
+      }
+      if (cnt > 0) {
+        const double v = ((double)sum / (double)cnt) * arms[b].c1;
+        if (v < best) { best = v; barg = b; }
+      }
+    }
+    a.opt[(size_t)cell * a.S + s] = best;
+    a.opt_arm[(size_t)cell * a.opt_stride + s] = barg;
+    for (int b = 0; b < a.B; ++b) {
+      long long sum = 0;
+      int cnt = 0;
+      for (int k = 0; k < a.K; ++k) {
+        const int E = a.pool[((size_t)s * a.B + b) * a.K + k];
+        if (E > 0) { sum += E; ++cnt; }
+      }
+      const double eb = cnt > 0 ? (double)sum / (double)cnt : (double)a.max_epochs;
+      a.regret[(size_t)cell * a.reg_stride + (size_t)s * a.B + b] = eb * arms[b].c1 - best;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ replay
+struct ReplayArgs {
+  const CellParam *cells;
+  const ArmConst *arms;           // [cells][B]
+  const double *regret;           // [cells][reg_stride]
+  const int32_t *opt_arm;         // [cells][opt_stride]
+  const int32_t *pool;            // [S][B][K], allocation padded to 16 B
+  double *curve_slots;            // [cells][nslot][R][kQ]
+  double *tot_cost, *tot_energy, *tot_time;
+  unsigned long long *digest;
+  int32_t *n_stop, *final_arm;
+  uint32_t *log;                  // [out][R] or null
+  unsigned long long *counters;   // [kCounters]
+  int B, S, K, R, max_epochs, charge_profiling, b0, nslot, reg_stride, opt_stride;
+  int tab_bytes;                  // bytes of the staged table region (multiple of 16)
+  int ring_n;                     // ring slots per arm in the smem layout (max window)
+};
+
+// shared-memory table region of one block: [ArmConst B][regret S*B][opt_arm S][pool S*B*K]
+struct TabLayout {
+  int arms, regret, optarm, pool, bytes;
+  __host__ __device__ static int align16(int x) { return (x + 15) & ~15; }
+  __host__ __device__ TabLayout(int B, int S, int K) {
+    arms = 0;
+    regret = align16(arms + B * (int)sizeof(ArmConst));
+    optarm = align16(regret + S * B * 8);
+    pool = align16(optarm + S * 4);
+    bytes = align16(pool + S * B * K * 4);
+  }
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// 1-D bulk copy global -> shared through the TMA unit, completion on an mbarrier.
+__device__ __forceinline__ void tma_bulk_load(void *dst_smem, const void *src, uint32_t bytes,
+                                              uint64_t *mbar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst_smem);
+  const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(d), "l"(src), "r"(bytes), "r"(m) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count) {
+  const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(m), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *mbar, uint32_t bytes) {
+  const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(m), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase) {
+  const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" :: "r"(m), "r"(phase) : "memory");
+}
+
+enum : int { kStart = 0, kDown = 1, kUp = 2 };
+
+__device__ __forceinline__ uint32_t below_mask(int c) { return c <= 0 ? 0u : ((1u << c) - 1u); }
+__device__ __forceinline__ uint32_t above_mask(int c) { return c >= 31 ? 0u : ~((2u << c) - 1u); }
+
+// One thread per trial.  WINDOWED: N > 0 (ring buffer per arm).  LOG: write the
+// per-decision log.  Dynamic smem = tab_bytes + per-thread arm state.
+template <bool WINDOWED, bool LOG>
+__global__ void __launch_bounds__(128) replay_kernel(ReplayArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  const int cell = blockIdx.y;
+  const CellParam cp = a.cells[cell];
+  const int tid = threadIdx.x, TPB = blockDim.x;
+  const int64_t j0 = (int64_t)blockIdx.x * TPB;
+  if (j0 >= cp.n) return;                                  // whole block past this cell's shard
+
+  // ---- stage the cell's tables with TMA bulk copies (one elected thread)
+  const TabLayout L(a.B, a.S, a.K);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    const uint32_t b_arm = a.B * (uint32_t)sizeof(ArmConst);
+    const uint32_t b_reg = a.S * a.B * 8u;
+    const uint32_t b_opt = a.S * 4u;
+    const uint32_t b_pool = a.S * a.B * a.K * 4u;
+    // bulk copies need 16-byte sizes; the host pads every table to 16 B
+    const uint32_t p_arm = (b_arm + 15u) & ~15u, p_reg = (b_reg + 15u) & ~15u;
+    const uint32_t p_opt = (b_opt + 15u) & ~15u, p_pool = (b_pool + 15u) & ~15u;
+    mbar_expect_tx(&mbar, p_arm + p_reg + p_opt + p_pool);
+    tma_bulk_load(smem + L.arms, a.arms + (size_t)cell * a.B, p_arm, &mbar);
+    tma_bulk_load(smem + L.regret, a.regret + (size_t)cell * a.reg_stride, p_reg, &mbar);
+    tma_bulk_load(smem + L.optarm, a.opt_arm + (size_t)cell * a.opt_stride, p_opt, &mbar);
+    tma_bulk_load(smem + L.pool, a.pool, p_pool, &mbar);
+  }
+  __syncthreads();
+  mbar_wait(&mbar, 0);
+
+  const ArmConst *arm = reinterpret_cast<const ArmConst *>(smem + L.arms);
+  const double *regret = reinterpret_cast<const double *>(smem + L.regret);
+  const int32_t *optarm = reinterpret_cast<const int32_t *>(smem + L.optarm);
+  const int32_t *pool = reinterpret_cast<const int32_t *>(smem + L.pool);
+  const int B = a.B, R = a.R, S = a.S, K = a.K;
+  // per-thread state: [field][arm][thread]
+  double *s_mu = reinterpret_cast<double *>(smem + a.tab_bytes);
+  double *s_sig = s_mu + B * TPB;
+  double *s_sh = s_sig + B * TPB;
+  double *s_S1 = s_sh + B * TPB;
+  double *s_S2 = s_S1 + B * TPB;
+  double *s_ring = s_S2 + B * TPB;                          // [N][B][TPB] when WINDOWED
+  int32_t *s_cnt = reinterpret_cast<int32_t *>(s_ring + (WINDOWED ? a.ring_n * B * TPB : 0));
+#define ST(arr, arm_) arr[(arm_) * TPB + tid]
+
+  const int64_t jj = j0 + tid;
+  const bool active = jj < cp.n;
+  const int64_t trial = cp.begin + jj;
+  const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
+  double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+
+  for (int b = 0; b < B; ++b) ST(s_cnt, b) = 0;
+  uint32_t profiled = 0, mature = 0;                        // bit a: profiled / n_a >= 2
+  double best = kInf;                                       // min_t C_t
+  bool in_ts = false;
+  int round = 1, step = kStart, start = a.b0, cursor = a.b0;
+  uint32_t cand = (B == 32) ? 0xffffffffu : ((1u << B) - 1u), surv = 0, ts_set = 0;
+  double r1_cost = kInf;
+  int r1_arm = -1;
+  double totC = 0.0, totE = 0.0, totT = 0.0;
+  unsigned long long dig = 0xcbf29ce484222325ull;
+  int nstop = 0, last_b = -1;
+  unsigned long long ctr[kCounters] = {0, 0, 0, 0, 0, 0, 0, 0};
+
+  for (int t = 0; t < R; ++t) {
+    double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
+    int vPacked = 0;
+    if (active) {
+      const int s = (int)(((long long)t * S) / R);
+      // ---------------- step 2: decide b_t
+      const bool ts_dec = in_ts;
+      int b;
+      if (!in_ts) {
+        b = (step == kStart) ? start
+          : (step == kDown) ? 31 - __clz(cand & below_mask(cursor))
+                            : __ffs(cand & above_mask(cursor)) - 1;
+        ctr[5] += 1;
+      } else {
+        const uint32_t unripe = ts_set & ~mature;
+        if (unripe) {
+          b = __ffs(unripe) - 1;                            // explore arms with n < 2 first
+          ctr[6] += 1;
+        } else {
+          double bt = kInf;
+          b = -1;
+          for (int k = 0; 2 * k < B; ++k) {                 // Alg. 1: sample, then argmin
+            const uint32_t pm = (ts_set >> (2 * k)) & 3u;
+            if (!pm) continue;
+            double z0, z1;
+            normal_pair(cp.key0, cp.key1, trial, t, k, z0, z1);
+            ctr[2] += 1;
+            if (pm & 1u) {
+              const double th = fma(ST(s_sig, 2 * k), z0, ST(s_mu, 2 * k));
+              ctr[3] += 1;
+              if (th < bt) { bt = th; b = 2 * k; }
+            }
+            if (pm & 2u) {
+              const double th = fma(ST(s_sig, 2 * k + 1), z1, ST(s_mu, 2 * k + 1));
+              ctr[3] += 1;
+              if (th < bt) { bt = th; b = 2 * k + 1; }
+            }
+          }
+          ctr[1] += 1;
+        }
+      }
+      const ArmConst ac = arm[b];
+      // ---------------- step 3: replay one recorded run
+      const uint32_t r = replica(cp.key0, cp.key1, trial, t, (uint32_t)K);
+      const int E = pool[((size_t)s * B + b) * K + r];
+      const int Erun = E > 0 ? E : a.max_epochs;
+      double c0, t0, e0;
+      const bool prof_now = a.charge_profiling && !((profiled >> b) & 1u);
+      if (prof_now) { c0 = ac.cP; t0 = ac.tP; e0 = ac.eP; } else { c0 = ac.c1; t0 = ac.t1; e0 = ac.e1; }
+      profiled |= 1u << b;
+      const double em1 = (double)(Erun - 1);
+      const double Cf = c0 + em1 * ac.c1;
+      // ---------------- step 4: early stop at β·min_t C_t, truncated charge
+      const double thr = cp.beta * best;
+      double C, Tm, En;
+      const bool stopped = Cf > thr;
+      if (stopped) {
+        C = thr;
+        if (thr <= c0) {
+          const double phi = thr / c0;
+          Tm = phi * t0;
+          En = phi * e0;
+        } else {
+          const double phi = (thr - c0) / ac.c1;
+          Tm = t0 + phi * ac.t1;
+          En = e0 + phi * ac.e1;
+        }
+      } else {
+        C = Cf;
+        Tm = t0 + em1 * ac.t1;
+        En = e0 + em1 * ac.e1;
+      }
+      const bool conv = (E > 0) && !stopped;
+      if (conv && !(C >= best)) best = C;
+      // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
+      {
+        const int cnt = ST(s_cnt, b);
+        double sh, S1, S2;
+        if (cnt == 0) { sh = C; S1 = 0.0; S2 = 0.0; ST(s_sh, b) = sh; }
+        else { sh = ST(s_sh, b); S1 = ST(s_S1, b); S2 = ST(s_S2, b); }
+        int n = cnt;
+        if (WINDOWED && cp.window > 0) {
+          const int N = cp.window;
+          double *slot = &s_ring[((cnt % N) * B + b) * TPB + tid];
+          if (cnt >= N) {
+            const double dy = *slot - sh;
+            S1 = S1 - dy;
+            S2 = S2 - dy * dy;
+            n = N - 1;
+          }
+          *slot = C;
+        }
+        const double d = C - sh;
+        S1 = S1 + d;
+        S2 = S2 + d * d;
+        n += 1;
+        ST(s_S1, b) = S1;
+        ST(s_S2, b) = S2;
+        ST(s_cnt, b) = cnt + 1;
+        if (n >= 2) {
+          const double dn = (double)n;
+          const double mean = sh + S1 / dn;
+          double s2 = (S2 - (S1 * S1) / dn) / (dn - 1.0);
+          const double fl = 1e-12 * (1.0 + mean * mean);
+          if (!(s2 >= fl)) s2 = fl;
+          const double q = 1.0 / s2;
+          const double var = 1.0 / (cp.prec0 + dn * q);
+          const double sum = dn * sh + S1;
+          ST(s_mu, b) = var * (cp.pm0 + sum * q);
+          ST(s_sig, b) = sqrt(var);
+          mature |= 1u << b;
+          ctr[7] += 1;
+        }
+      }
+      ctr[0] += 1;
+      if (stopped) ctr[4] += 1;
+      // ---------------- Alg. 3 bookkeeping
+      if (!in_ts) {
+        if (conv) {
+          surv |= 1u << b;
+          if (round == 1 && (C < r1_cost || (C == r1_cost && b < r1_arm))) { r1_cost = C; r1_arm = b; }
+        }
+        bool end_round = false;
+        if (step == kStart) { step = kDown; cursor = start; }
+        else if (step == kDown) { if (conv) cursor = b; else { step = kUp; cursor = start; } }
+        else { if (conv) cursor = b; else end_round = true; }
+        if (!end_round && step == kDown && (cand & below_mask(cursor)) == 0u) { step = kUp; cursor = start; }
+        if (!end_round && step == kUp && (cand & above_mask(cursor)) == 0u) end_round = true;
+        if (end_round) {
+          if (surv == 0u) surv = 1u << start;
+          if (round == 1) {
+            cand = surv;
+            if (r1_arm >= 0) start = r1_arm;
+            surv = 0u;
+            round = 2;
+            step = kStart;
+            cursor = start;
+          } else {
+            in_ts = true;
+            ts_set = surv;
+          }
+        }
+      }
+      // ---------------- accumulate
+      const uint32_t flags = (stopped ? 1u : 0u) | (conv ? 2u : 0u) | (prof_now ? 4u : 0u) |
+                             (ts_dec ? 8u : 0u);
+      totC += C;
+      totE += En;
+      totT += Tm;
+      nstop += stopped ? 1 : 0;
+      last_b = b;
+      dig = (dig ^ (unsigned long long)(uint32_t)b) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)(uint32_t)ac.pstar) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)flags) * 0x100000001b3ull;
+      if (LOG) a.log[(size_t)(cp.out_off + jj) * R + t] = (uint32_t)b | ((uint32_t)ac.pstar << 8) | (flags << 16);
+      vC = C;
+      vE = En;
+      vT = Tm;
+      vReg = regret[s * B + b];
+      vPacked = (stopped ? 1 : 0) | ((b == optarm[s]) ? (1 << 8) : 0) | (ts_dec ? (1 << 16) : 0);
+    }
+    // ---------------- warp partial of the curves, one atomic per quantity per warp
+    vC = warp_sum(vC);
+    vE = warp_sum(vE);
+    vT = warp_sum(vT);
+    vReg = warp_sum(vReg);
+    vPacked = warp_sum(vPacked);
+    if ((tid & 31) == 0) {
+      double *row = curves + (size_t)t * kQ;
+      atomicAdd(row + 0, vC);
+      atomicAdd(row + 1, vE);
+      atomicAdd(row + 2, vT);
+      atomicAdd(row + 3, vReg);
+      if (vPacked & 0xff) atomicAdd(row + 4, (double)(vPacked & 0xff));
+      if ((vPacked >> 8) & 0xff) atomicAdd(row + 5, (double)((vPacked >> 8) & 0xff));
+      if ((vPacked >> 16) & 0xff) atomicAdd(row + 6, (double)((vPacked >> 16) & 0xff));
+    }
+  }
+#undef ST
+  if (active) {
+    const size_t o = (size_t)(cp.out_off + jj);
+    a.tot_cost[o] = totC;
+    a.tot_energy[o] = totE;
+    a.tot_time[o] = totT;
+    a.digest[o] = dig;
+    a.n_stop[o] = nstop;
+    a.final_arm[o] = last_b;
+  }
+#pragma unroll
+  for (int q = 0; q < kCounters; ++q) {
+    unsigned long long v = ctr[q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((tid & 31) == 0 && v) atomicAdd(a.counters + q, v);
+  }
+}
+
+// curves[cell][t][q] = sum over slots in slot order
+__global__ void curve_reduce_kernel(const double *slots, double *curves, int ncells, int nslot,
+                                    int R) {
+  const long long total = (long long)ncells * R * kQ;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long cell = i / ((long long)R * kQ);
+    const long long rq = i % ((long long)R * kQ);
+    double s = 0.0;
+    for (int k = 0; k < nslot; ++k) s += slots[((size_t)cell * nslot + k) * (size_t)R * kQ + rq];
+    curves[i] = s;
+  }
+}
+
+}  // namespace zs

@@ -1,0 +1,497 @@
+// zeus_sim.cu -- host side of the C ABI declared in include/zeus_sim.h.
+//
+// Validation (every violated invariant is reported), device
+// allocation, H2D staging of the two traces (§6.1), launches of
+// the step-1 / replay / curve-reduction kernels on the caller's stream, and
+// D2H of the results.  There is no CPU compute path: without a usable CUDA
+// device every call that would launch work fails with ZEUS_E_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/zeus_sim.h"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t alloc(size_t n) {
+    if (p) { cudaFree(p); p = nullptr; }
+    bytes = n;
+    if (n == 0) return cudaSuccess;
+    return cudaMalloc(&p, n);
+  }
+  template <class T> T *as() const { return static_cast<T *>(p); }
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct zeus_sim {
+  // job
+  int B = 0, P = 0, b0 = 0, max_epochs = 0, charge_profiling = 0;
+  std::vector<int32_t> batch_sizes;
+  std::vector<double> power_limits;
+  double MP = 0.0;
+  // cells / run
+  std::vector<zeus_cell> cells;
+  std::vector<zs::CellParam> cpar;
+  int R = 0, log_mode = 0, layout = 0, device = 0;
+  int64_t shard_total = 0, max_shard = 0;
+  // trace
+  int S = 0, K = 0, reg_stride = 0, opt_stride = 0;
+  bool loaded = false, ran = false;
+  int nslot = 1, tpb = 128, smem_bytes = 0, tab_bytes = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  std::string err;
+  // device memory
+  DevBuf d_A, d_Th, d_pool, d_cells, d_arms, d_regret, d_opt, d_optarm;
+  DevBuf d_slots, d_curves, d_tot_cost, d_tot_energy, d_tot_time, d_digest, d_nstop, d_final,
+      d_log, d_counters;
+  ~zeus_sim() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (ev2) cudaEventDestroy(ev2);
+    if (ev3) cudaEventDestroy(ev3);
+  }
+};
+
+namespace {
+
+struct Errors {
+  std::string s;
+  zeus_status code = ZEUS_OK;
+  void add(zeus_status c, const std::string &m) {
+    if (!s.empty()) s += "; ";
+    s += m;
+    // the most specific code wins: INVALID over UNSUPPORTED over NO_CONVERGENT_ARM
+    if (code == ZEUS_OK || c == ZEUS_E_INVALID) code = c;
+  }
+};
+
+zeus_status fail(zeus_sim *sim, zeus_status c, const std::string &m) {
+  if (sim) sim->err = m; else g_create_error = m;
+  return c;
+}
+
+zeus_status cuda_fail(zeus_sim *sim, cudaError_t e, const char *where) {
+  return fail(sim, ZEUS_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define ZS_CUDA(sim, call)                                 \
+  do {                                                     \
+    cudaError_t e_ = (call);                               \
+    if (e_ != cudaSuccess) return cuda_fail(sim, e_, #call); \
+  } while (0)
+
+void check_job(const zeus_job *job, Errors &E) {
+  if (!job) { E.add(ZEUS_E_INVALID, "job is NULL"); return; }
+  if (job->struct_size != sizeof(zeus_job)) E.add(ZEUS_E_INVALID, "zeus_job.struct_size mismatch (ABI)");
+  const int B = job->num_batch_sizes, P = job->num_power_limits;
+  if (B < 1) E.add(ZEUS_E_INVALID, "no batch sizes");
+  if (B > ZEUS_MAX_BATCH_SIZES) E.add(ZEUS_E_UNSUPPORTED, "more than 32 batch sizes");
+  if (P < 1) E.add(ZEUS_E_INVALID, "no power limits");
+  if (P > ZEUS_MAX_POWER_LIMITS) E.add(ZEUS_E_UNSUPPORTED, "more than 64 power limits");
+  if (B >= 1 && !job->batch_sizes) E.add(ZEUS_E_INVALID, "batch_sizes is NULL");
+  if (P >= 1 && !job->power_limits_w) E.add(ZEUS_E_INVALID, "power_limits_w is NULL");
+  if (B >= 1 && job->batch_sizes) {
+    for (int b = 0; b < B; ++b)
+      if (job->batch_sizes[b] <= 0) { E.add(ZEUS_E_INVALID, "batch size not positive"); break; }
+    for (int b = 1; b < B; ++b)
+      if (job->batch_sizes[b] <= job->batch_sizes[b - 1]) { E.add(ZEUS_E_INVALID, "batch sizes not strictly increasing"); break; }
+  }
+  if (job->default_bs_index < 0 || job->default_bs_index >= B)
+    E.add(ZEUS_E_INVALID, "default batch size index out of range");
+  double pmax = 0.0;
+  if (P >= 1 && job->power_limits_w) {
+    for (int p = 0; p < P; ++p)
+      if (!(job->power_limits_w[p] > 0.0)) { E.add(ZEUS_E_INVALID, "power limit not positive"); break; }
+    for (int p = 1; p < P; ++p)
+      if (!(job->power_limits_w[p] > job->power_limits_w[p - 1])) { E.add(ZEUS_E_INVALID, "power limits not strictly increasing"); break; }
+    pmax = job->power_limits_w[P - 1];
+  }
+  if (!(job->max_power_w >= pmax) || !std::isfinite(job->max_power_w))
+    E.add(ZEUS_E_INVALID, "max power below the largest power limit");
+  if (job->max_epochs < 1) E.add(ZEUS_E_INVALID, "max_epochs < 1");
+  if (job->charge_profiling != 0 && job->charge_profiling != 1) E.add(ZEUS_E_INVALID, "charge_profiling must be 0 or 1");
+}
+
+void check_cells(const zeus_cell *cells, int n, Errors &E) {
+  if (n < 1) { E.add(ZEUS_E_INVALID, "no cells"); return; }
+  if (!cells) { E.add(ZEUS_E_INVALID, "cells is NULL"); return; }
+  for (int i = 0; i < n; ++i) {
+    const zeus_cell &c = cells[i];
+    const std::string at = " (cell " + std::to_string(i) + ")";
+    if (!(c.eta >= 0.0 && c.eta <= 1.0)) E.add(ZEUS_E_INVALID, "eta out of [0,1]" + at);
+    if (!(c.beta > 1.0)) E.add(ZEUS_E_INVALID, "beta must be > 1" + at);
+    if (c.window == 1 || c.window < 0) E.add(ZEUS_E_INVALID, "window must be 0 (unbounded) or >= 2" + at);
+    if (!(c.prior_var > 0.0)) E.add(ZEUS_E_INVALID, "prior variance must be > 0" + at);
+    if (!std::isfinite(c.prior_mean)) E.add(ZEUS_E_INVALID, "prior mean not finite" + at);
+    if (c.trials < 0) E.add(ZEUS_E_INVALID, "trials < 0" + at);
+  }
+}
+
+void launch_step1(zeus_sim *s, cudaStream_t st) {
+  zs::Step1Args a{};
+  a.A = s->d_A.as<double>();
+  a.Th = s->d_Th.as<double>();
+  a.pool = s->d_pool.as<int32_t>();
+  a.cells = s->d_cells.as<zs::CellParam>();
+  a.arms = s->d_arms.as<zs::ArmConst>();
+  a.regret = s->d_regret.as<double>();
+  a.opt = s->d_opt.as<double>();
+  a.opt_arm = s->d_optarm.as<int32_t>();
+  a.B = s->B; a.P = s->P; a.S = s->S; a.K = s->K; a.max_epochs = s->max_epochs;
+  a.reg_stride = s->reg_stride; a.opt_stride = s->opt_stride; a.MP = s->MP;
+  zs::step1_kernel<<<(unsigned)s->cells.size(), 256, 0, st>>>(a);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *zeus_sim_last_error(const zeus_sim *sim) {
+  return sim ? sim->err.c_str() : g_create_error.c_str();
+}
+
+zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t num_cells,
+                            const zeus_run_opts *opts, int32_t cuda_device, zeus_sim **out) {
+  g_create_error.clear();
+  if (!out) return fail(nullptr, ZEUS_E_INVALID, "out is NULL");
+  *out = nullptr;
+  Errors E;
+  check_job(job, E);
+  check_cells(cells, num_cells, E);
+  if (!opts) E.add(ZEUS_E_INVALID, "opts is NULL");
+  else {
+    if (opts->struct_size != sizeof(zeus_run_opts)) E.add(ZEUS_E_INVALID, "zeus_run_opts.struct_size mismatch (ABI)");
+    if (opts->recurrences < 0) E.add(ZEUS_E_INVALID, "recurrences < 0");
+    if (opts->shard_begin < 0) E.add(ZEUS_E_INVALID, "shard_begin < 0");
+    if (opts->shard_end >= 0 && opts->shard_end < opts->shard_begin) E.add(ZEUS_E_INVALID, "shard_end < shard_begin");
+    if (opts->log_mode != 0 && opts->log_mode != 1) E.add(ZEUS_E_INVALID, "log_mode must be 0 or 1");
+    if (opts->layout < 0 || opts->layout > 2) E.add(ZEUS_E_INVALID, "layout must be 0, 1 or 2");
+    if (opts->layout == 2) E.add(ZEUS_E_UNSUPPORTED, "layout 2 (lane group per trial) is not built yet");
+  }
+  if (E.code != ZEUS_OK) return fail(nullptr, E.code, E.s);
+
+  int ndev = 0;
+  cudaError_t ce = cudaGetDeviceCount(&ndev);
+  if (ce != cudaSuccess || ndev == 0)
+    return fail(nullptr, ZEUS_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(ce));
+  if (cuda_device < 0 || cuda_device >= ndev) return fail(nullptr, ZEUS_E_INVALID, "cuda_device out of range");
+  ce = cudaSetDevice(cuda_device);
+  if (ce != cudaSuccess) return fail(nullptr, ZEUS_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(ce));
+
+  zeus_sim *s = new (std::nothrow) zeus_sim();
+  if (!s) return fail(nullptr, ZEUS_E_NOMEM, "host allocation failed");
+  s->device = cuda_device;
+  s->B = job->num_batch_sizes;
+  s->P = job->num_power_limits;
+  s->b0 = job->default_bs_index;
+  s->max_epochs = job->max_epochs;
+  s->charge_profiling = job->charge_profiling;
+  s->MP = job->max_power_w;
+  s->batch_sizes.assign(job->batch_sizes, job->batch_sizes + s->B);
+  s->power_limits.assign(job->power_limits_w, job->power_limits_w + s->P);
+  s->cells.assign(cells, cells + num_cells);
+  s->R = opts->recurrences > 0 ? opts->recurrences : 2 * s->B * s->P;
+  s->log_mode = opts->log_mode;
+  s->layout = opts->layout;
+  int64_t off = 0;
+  for (int i = 0; i < num_cells; ++i) {
+    const zeus_cell &c = cells[i];
+    zs::CellParam p{};
+    p.eta = c.eta;
+    p.beta = c.beta;
+    p.prec0 = std::isinf(c.prior_var) ? 0.0 : 1.0 / c.prior_var;   // flat prior
+    p.pm0 = c.prior_mean * p.prec0;
+    p.window = c.window;
+    p.key0 = (uint32_t)c.seed;
+    p.key1 = (uint32_t)(c.seed >> 32);
+    const int64_t b = std::min(opts->shard_begin, c.trials);
+    const int64_t e = opts->shard_end < 0 ? c.trials : std::min(opts->shard_end, c.trials);
+    p.begin = b;
+    p.n = e - b;
+    p.out_off = off;
+    off += p.n;
+    s->max_shard = std::max(s->max_shard, p.n);
+    s->cpar.push_back(p);
+  }
+  s->shard_total = off;
+  // curve slots: spread the per-warp atomics over up to 64 copies, bounded to 64 MB
+  const size_t curve_bytes = (size_t)num_cells * s->R * zs::kQ * sizeof(double);
+  s->nslot = (int)std::max<size_t>(1, std::min<size_t>(64, (64ull << 20) / std::max<size_t>(1, curve_bytes)));
+
+  const size_t n = (size_t)s->shard_total;
+  cudaError_t e = cudaSuccess;
+  if ((e = s->d_cells.alloc(sizeof(zs::CellParam) * num_cells)) != cudaSuccess ||
+      (e = s->d_slots.alloc(curve_bytes * s->nslot)) != cudaSuccess ||
+      (e = s->d_curves.alloc(curve_bytes)) != cudaSuccess ||
+      (e = s->d_tot_cost.alloc(n * 8)) != cudaSuccess ||
+      (e = s->d_tot_energy.alloc(n * 8)) != cudaSuccess ||
+      (e = s->d_tot_time.alloc(n * 8)) != cudaSuccess ||
+      (e = s->d_digest.alloc(n * 8)) != cudaSuccess ||
+      (e = s->d_nstop.alloc(n * 4)) != cudaSuccess ||
+      (e = s->d_final.alloc(n * 4)) != cudaSuccess ||
+      (e = s->d_log.alloc(s->log_mode ? n * (size_t)s->R * 4 : 0)) != cudaSuccess ||
+      (e = s->d_counters.alloc(zs::kCounters * 8)) != cudaSuccess) {
+    std::string m = std::string("device allocation: ") + cudaGetErrorString(e);
+    delete s;
+    return fail(nullptr, e == cudaErrorMemoryAllocation ? ZEUS_E_NOMEM : ZEUS_E_CUDA, m);
+  }
+  if ((e = cudaMemcpy(s->d_cells.p, s->cpar.data(), sizeof(zs::CellParam) * num_cells,
+                      cudaMemcpyHostToDevice)) != cudaSuccess ||
+      (e = cudaEventCreate(&s->ev0)) != cudaSuccess || (e = cudaEventCreate(&s->ev1)) != cudaSuccess ||
+      (e = cudaEventCreate(&s->ev2)) != cudaSuccess || (e = cudaEventCreate(&s->ev3)) != cudaSuccess) {
+    std::string m = std::string("create: ") + cudaGetErrorString(e);
+    delete s;
+    return fail(nullptr, ZEUS_E_CUDA, m);
+  }
+  *out = s;
+  return ZEUS_OK;
+}
+
+zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th, int32_t S,
+                                  int32_t K, const int32_t *pool) {
+  if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
+  s->err.clear();
+  Errors E;
+  const int B = s->B, P = s->P;
+  if (!A) E.add(ZEUS_E_INVALID, "avg_power_w is NULL");
+  if (!Th) E.add(ZEUS_E_INVALID, "throughput_eps is NULL");
+  if (!pool) E.add(ZEUS_E_INVALID, "epochs_to_target is NULL");
+  if (S < 1) E.add(ZEUS_E_INVALID, "num_slices < 1");
+  if (K < 1) E.add(ZEUS_E_INVALID, "replicas < 1");
+  if (A) {
+    for (int i = 0; i < B * P; ++i)
+      if (!(A[i] > 0.0) || !std::isfinite(A[i])) { E.add(ZEUS_E_INVALID, "average power not positive"); break; }
+    for (int i = 0; i < B * P; ++i)
+      if (!(A[i] <= s->MP)) { E.add(ZEUS_E_INVALID, "average power above max power"); break; }
+  }
+  if (Th)
+    for (int i = 0; i < B * P; ++i)
+      if (!(Th[i] > 0.0) || !std::isfinite(Th[i])) { E.add(ZEUS_E_INVALID, "throughput not positive"); break; }
+  if (pool && S >= 1 && K >= 1) {
+    for (size_t i = 0; i < (size_t)S * B * K; ++i)
+      if (pool[i] > s->max_epochs) { E.add(ZEUS_E_INVALID, "epochs_to_target above max_epochs"); break; }
+    for (int sl = 0; sl < S; ++sl) {
+      bool any = false;
+      for (int i = 0; i < B * K && !any; ++i) any = pool[(size_t)sl * B * K + i] > 0;
+      if (!any) { E.add(ZEUS_E_NO_CONVERGENT_ARM, "slice " + std::to_string(sl) + " has no converged replica on any arm"); break; }
+    }
+  }
+  if (E.code == ZEUS_OK) {
+    const zs::TabLayout L(B, S, K);
+    const size_t per_thread = (size_t)B * (5 * 8 + 4);
+    int wmax = 0;
+    for (const auto &c : s->cells) wmax = std::max(wmax, c.window);
+    const size_t need = (size_t)L.bytes + 32 * (per_thread + (size_t)wmax * B * 8);
+    if (need > 200 * 1024)
+      E.add(ZEUS_E_UNSUPPORTED, "trace tables + per-trial arm state exceed shared memory (" +
+                                    std::to_string(need) + " B for 32 trials)");
+  }
+  if (E.code != ZEUS_OK) return fail(s, E.code, E.s);
+  ZS_CUDA(s, cudaSetDevice(s->device));
+  s->S = S;
+  s->K = K;
+  s->reg_stride = (int)align_up((size_t)S * B, 2);
+  s->opt_stride = (int)align_up((size_t)S, 4);
+  const int nc = (int)s->cells.size();
+  ZS_CUDA(s, s->d_A.alloc((size_t)B * P * 8));
+  ZS_CUDA(s, s->d_Th.alloc((size_t)B * P * 8));
+  ZS_CUDA(s, s->d_pool.alloc(align_up((size_t)S * B * K * 4, 16)));
+  ZS_CUDA(s, s->d_arms.alloc((size_t)nc * B * sizeof(zs::ArmConst)));
+  ZS_CUDA(s, s->d_regret.alloc((size_t)nc * s->reg_stride * 8));
+  ZS_CUDA(s, s->d_opt.alloc((size_t)nc * S * 8));
+  ZS_CUDA(s, s->d_optarm.alloc((size_t)nc * s->opt_stride * 4));
+  ZS_CUDA(s, cudaMemset(s->d_pool.p, 0, s->d_pool.bytes));
+  ZS_CUDA(s, cudaMemset(s->d_regret.p, 0, s->d_regret.bytes));
+  ZS_CUDA(s, cudaMemset(s->d_optarm.p, 0, s->d_optarm.bytes));
+  ZS_CUDA(s, cudaMemcpy(s->d_A.p, A, (size_t)B * P * 8, cudaMemcpyHostToDevice));
+  ZS_CUDA(s, cudaMemcpy(s->d_Th.p, Th, (size_t)B * P * 8, cudaMemcpyHostToDevice));
+  ZS_CUDA(s, cudaMemcpy(s->d_pool.p, pool, (size_t)S * B * K * 4, cudaMemcpyHostToDevice));
+  launch_step1(s, nullptr);
+  ZS_CUDA(s, cudaGetLastError());
+  ZS_CUDA(s, cudaDeviceSynchronize());
+
+  // launch shape of the replay: the block size (32/64/128 trials) that keeps the
+  // most warps resident given the shared-memory footprint per trial
+  const zs::TabLayout L(B, S, K);
+  s->tab_bytes = L.bytes;
+  int wmax = 0;
+  for (const auto &c : s->cells) wmax = std::max(wmax, c.window);
+  const size_t per_thread = (size_t)B * (5 * 8 + 4) + (size_t)wmax * B * 8;
+  int best_warps = -1;
+  for (int tpb : {128, 64, 32}) {
+    const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
+    if (bytes > 227 * 1024) continue;
+    int blocks = 0;
+    const void *fn = wmax > 0 ? (const void *)zs::replay_kernel<true, false>
+                              : (const void *)zs::replay_kernel<false, false>;
+    ZS_CUDA(s, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    ZS_CUDA(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, tpb, bytes));
+    const int warps = blocks * tpb / 32;
+    if (warps > best_warps) { best_warps = warps; s->tpb = tpb; s->smem_bytes = (int)bytes; }
+  }
+  if (best_warps <= 0) return fail(s, ZEUS_E_UNSUPPORTED, "no launch shape fits shared memory");
+  for (const void *fn : {(const void *)zs::replay_kernel<false, false>, (const void *)zs::replay_kernel<false, true>,
+                         (const void *)zs::replay_kernel<true, false>, (const void *)zs::replay_kernel<true, true>})
+    ZS_CUDA(s, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, s->smem_bytes));
+  s->loaded = true;
+  return ZEUS_OK;
+}
+
+zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
+  if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
+  s->err.clear();
+  if (!s->loaded) return fail(s, ZEUS_E_STATE, "zeus_sim_run before zeus_sim_load_profile");
+  ZS_CUDA(s, cudaSetDevice(s->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  s->stream = st;
+  const int nc = (int)s->cells.size();
+  ZS_CUDA(s, cudaMemsetAsync(s->d_slots.p, 0, s->d_slots.bytes, st));
+  ZS_CUDA(s, cudaMemsetAsync(s->d_counters.p, 0, s->d_counters.bytes, st));
+  ZS_CUDA(s, cudaEventRecord(s->ev0, st));
+  launch_step1(s, st);                        // a1: Eq. 7 argmin + per-arm constants
+  ZS_CUDA(s, cudaGetLastError());
+  ZS_CUDA(s, cudaEventRecord(s->ev3, st));
+  if (s->max_shard > 0 && s->R > 0) {
+    zs::ReplayArgs a{};
+    a.cells = s->d_cells.as<zs::CellParam>();
+    a.arms = s->d_arms.as<zs::ArmConst>();
+    a.regret = s->d_regret.as<double>();
+    a.opt_arm = s->d_optarm.as<int32_t>();
+    a.pool = s->d_pool.as<int32_t>();
+    a.curve_slots = s->d_slots.as<double>();
+    a.tot_cost = s->d_tot_cost.as<double>();
+    a.tot_energy = s->d_tot_energy.as<double>();
+    a.tot_time = s->d_tot_time.as<double>();
+    a.digest = s->d_digest.as<unsigned long long>();
+    a.n_stop = s->d_nstop.as<int32_t>();
+    a.final_arm = s->d_final.as<int32_t>();
+    a.log = s->d_log.as<uint32_t>();
+    a.counters = s->d_counters.as<unsigned long long>();
+    a.B = s->B; a.S = s->S; a.K = s->K; a.R = s->R; a.max_epochs = s->max_epochs;
+    a.charge_profiling = s->charge_profiling; a.b0 = s->b0; a.nslot = s->nslot;
+    a.reg_stride = s->reg_stride; a.opt_stride = s->opt_stride; a.tab_bytes = s->tab_bytes;
+    int wmax = 0;
+    for (const auto &c : s->cells) wmax = std::max(wmax, c.window);
+    const bool windowed = wmax > 0;
+    a.ring_n = wmax;
+    const dim3 grid((unsigned)((s->max_shard + s->tpb - 1) / s->tpb), (unsigned)nc);
+    if (windowed && s->log_mode) zs::replay_kernel<true, true><<<grid, s->tpb, s->smem_bytes, st>>>(a);
+    else if (windowed) zs::replay_kernel<true, false><<<grid, s->tpb, s->smem_bytes, st>>>(a);
+    else if (s->log_mode) zs::replay_kernel<false, true><<<grid, s->tpb, s->smem_bytes, st>>>(a);
+    else zs::replay_kernel<false, false><<<grid, s->tpb, s->smem_bytes, st>>>(a);
+    ZS_CUDA(s, cudaGetLastError());
+  }
+  ZS_CUDA(s, cudaEventRecord(s->ev1, st));
+  zs::curve_reduce_kernel<<<std::max(1, std::min(1184, (int)((nc * (size_t)s->R * zs::kQ + 255) / 256))), 256, 0, st>>>(
+      s->d_slots.as<double>(), s->d_curves.as<double>(), nc, s->nslot, s->R);
+  ZS_CUDA(s, cudaGetLastError());
+  ZS_CUDA(s, cudaEventRecord(s->ev2, st));
+  s->ran = true;
+  return ZEUS_OK;
+}
+
+zeus_status zeus_sim_results(zeus_sim *s, zeus_results *out) {
+  if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
+  s->err.clear();
+  if (!out) return fail(s, ZEUS_E_INVALID, "out is NULL");
+  if (out->struct_size != sizeof(zeus_results)) return fail(s, ZEUS_E_INVALID, "zeus_results.struct_size mismatch (ABI)");
+  if (!s->loaded) return fail(s, ZEUS_E_STATE, "zeus_sim_results before zeus_sim_load_profile");
+  ZS_CUDA(s, cudaSetDevice(s->device));
+  cudaStream_t st = s->stream;
+  const int nc = (int)s->cells.size();
+  const size_t n = (size_t)s->shard_total;
+  auto cp = [&](void *dst, const DevBuf &src, size_t bytes) -> cudaError_t {
+    if (!dst || bytes == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src.p, bytes, cudaMemcpyDefault, st);   // host or device dst
+  };
+  if (s->ran) {
+    ZS_CUDA(s, cp(out->curves, s->d_curves, (size_t)nc * s->R * zs::kQ * 8));
+    ZS_CUDA(s, cp(out->tot_cost, s->d_tot_cost, n * 8));
+    ZS_CUDA(s, cp(out->tot_energy, s->d_tot_energy, n * 8));
+    ZS_CUDA(s, cp(out->tot_time, s->d_tot_time, n * 8));
+    ZS_CUDA(s, cp(out->digest, s->d_digest, n * 8));
+    ZS_CUDA(s, cp(out->n_stop, s->d_nstop, n * 4));
+    ZS_CUDA(s, cp(out->final_arm, s->d_final, n * 4));
+    if (out->log && !s->log_mode) return fail(s, ZEUS_E_STATE, "log requested but log_mode = 0");
+    ZS_CUDA(s, cp(out->log, s->d_log, n * (size_t)s->R * 4));
+    ZS_CUDA(s, cp(out->counters, s->d_counters, zs::kCounters * 8));
+  } else if (out->curves || out->tot_cost || out->tot_energy || out->tot_time || out->digest ||
+             out->n_stop || out->final_arm || out->log || out->counters) {
+    return fail(s, ZEUS_E_STATE, "replay outputs requested before zeus_sim_run");
+  }
+  ZS_CUDA(s, cp(out->opt_cost, s->d_opt, (size_t)nc * s->S * 8));
+  if (out->opt_arm) {
+    std::vector<int32_t> tmp((size_t)nc * s->opt_stride);
+    ZS_CUDA(s, cudaMemcpyAsync(tmp.data(), s->d_optarm.p, tmp.size() * 4, cudaMemcpyDeviceToHost, st));
+    ZS_CUDA(s, cudaStreamSynchronize(st));
+    std::vector<int32_t> packed((size_t)nc * s->S);
+    for (int c = 0; c < nc; ++c)
+      std::memcpy(&packed[(size_t)c * s->S], &tmp[(size_t)c * s->opt_stride], (size_t)s->S * 4);
+    ZS_CUDA(s, cudaMemcpy(out->opt_arm, packed.data(), packed.size() * 4, cudaMemcpyDefault));
+  }
+  const bool want_arms = out->pstar_index || out->c1 || out->t1 || out->e1 || out->c_prof ||
+                         out->t_prof || out->e_prof;
+  if (want_arms) {
+    std::vector<zs::ArmConst> arms((size_t)nc * s->B);
+    ZS_CUDA(s, cudaMemcpyAsync(arms.data(), s->d_arms.p, arms.size() * sizeof(zs::ArmConst),
+                               cudaMemcpyDeviceToHost, st));
+    ZS_CUDA(s, cudaStreamSynchronize(st));
+    std::vector<int32_t> ps(arms.size());
+    std::vector<double> f[6];
+    for (auto &v : f) v.resize(arms.size());
+    for (size_t i = 0; i < arms.size(); ++i) {
+      ps[i] = arms[i].pstar;
+      f[0][i] = arms[i].c1; f[1][i] = arms[i].t1; f[2][i] = arms[i].e1;
+      f[3][i] = arms[i].cP; f[4][i] = arms[i].tP; f[5][i] = arms[i].eP;
+    }
+    double *dst[6] = {out->c1, out->t1, out->e1, out->c_prof, out->t_prof, out->e_prof};
+    if (out->pstar_index) ZS_CUDA(s, cudaMemcpy(out->pstar_index, ps.data(), ps.size() * 4, cudaMemcpyDefault));
+    for (int q = 0; q < 6; ++q)
+      if (dst[q]) ZS_CUDA(s, cudaMemcpy(dst[q], f[q].data(), f[q].size() * 8, cudaMemcpyDefault));
+  }
+  ZS_CUDA(s, cudaStreamSynchronize(st));
+  out->replay_ms = 0.f;
+  out->step1_ms = 0.f;
+  out->reduce_ms = 0.f;
+  if (s->ran) {
+    ZS_CUDA(s, cudaEventElapsedTime(&out->step1_ms, s->ev0, s->ev3));
+    ZS_CUDA(s, cudaEventElapsedTime(&out->replay_ms, s->ev3, s->ev1));
+    ZS_CUDA(s, cudaEventElapsedTime(&out->reduce_ms, s->ev1, s->ev2));
+  }
+  return ZEUS_OK;
+}
+
+void zeus_sim_destroy(zeus_sim *s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  delete s;
+}
+
+zeus_status zeus_sim_shape(const zeus_sim *s, int32_t *recurrences, int64_t *shard,
+                           int32_t *num_cells, int32_t *num_batch_sizes, int32_t *num_slices) {
+  if (!s) return ZEUS_E_INVALID;
+  if (recurrences) *recurrences = s->R;
+  if (shard) *shard = s->shard_total;
+  if (num_cells) *num_cells = (int32_t)s->cells.size();
+  if (num_batch_sizes) *num_batch_sizes = s->B;
+  if (num_slices) *num_slices = s->S;
+  return ZEUS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): every (batch size, power limit) decision and
+early-stop event bit-exact -- checked through the per-decision log (CFG1) and
+the FNV-1a digest of (b_t, p_t, flags) per trial (all configs) -- and per-trial
+totals bit-exact (NC-8: both sides sum in recurrence order); curves summed over
+trials within 1e-9 relative (NC-8: order of the cross-trial sum is free).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2208_06102_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+CURVE_RTOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def zs():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2208_06102_b200 import build, zeus_sim
+
+    build.build()
+    return zeus_sim
+
+
+def oracle_threads(oracle):
+    return max(1, min(64, oracle.hardware_threads()))
+
+
+def run_gpu(zs, w, cells, trials, R, shard=(0, -1), log=False, want=None):
+    sim = zs.Simulation(w, cells, trials, R, shard=shard, log=log).load_profile().run()
+    keys = ["curves", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm",
+            "counters", "pstar_index", "c1", "t1", "e1", "c_prof", "t_prof", "e_prof", "opt_cost",
+            "opt_arm"] + (["log"] if log else [])
+    out = sim.results(want=want or keys)
+    out["R"] = sim.R
+    out["n"] = sim.shard_n // len(cells)
+    sim.close()
+    return out
+
+
+def compare_cell(oracle, g, w, cell, ci, trials_idx, R, n_shard, full_curves=True, logs=False,
+                 shard_begin=0):
+    """Per-trial bit-exact + curves within 1e-9 for cell ci of a GPU result."""
+    o = oracle.replay(w, cell, R, trials_idx, threads=oracle_threads(oracle), logs=logs)
+    pos = np.asarray(trials_idx) - shard_begin + ci * n_shard
+    for k in ("tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm"):
+        got, exp = g[k][pos], o[k]
+        if not np.array_equal(got, exp):
+            bad = np.nonzero(got != exp)[0]
+            raise AssertionError(f"{k}: {len(bad)} of {len(exp)} trials differ, first trial "
+                                 f"{trials_idx[bad[0]]}: gpu {got[bad[0]]!r} oracle {exp[bad[0]]!r}")
+    if logs:
+        gl = g["log"][pos]
+        if not np.array_equal(gl, o["log"]):
+            bad = np.argwhere(gl != o["log"])[0]
+            raise AssertionError(f"log differs at trial {trials_idx[bad[0]]} t={bad[1]}: "
+                                 f"gpu {gl[tuple(bad)]:#x} oracle {o['log'][tuple(bad)]:#x}")
+    if full_curves:
+        gc, oc = g["curves"][ci], o["curves"]
+        np.testing.assert_allclose(gc[:, :4], oc[:, :4], rtol=CURVE_RTOL, atol=0)
+        assert np.array_equal(gc[:, 4:], oc[:, 4:])
+        if len(g["curves"]) == 1:
+            assert np.array_equal(g["counters"], o["counters"])
+    return o
+
+
+def compare_step1(oracle, g, w, cells):
+    for ci, c in enumerate(cells):
+        st = oracle.step1(w, c)
+        assert np.array_equal(g["pstar_index"][ci], st["pstar"])
+        for k in ("c1", "t1", "e1", "c_prof", "t_prof", "e_prof"):
+            assert np.array_equal(g[k][ci], st[k]), k
+        assert np.array_equal(g["opt_cost"][ci], st["opt"])
+        assert np.array_equal(g["opt_arm"][ci], st["opt_arm"])
+
+
+# ------------------------------------------------------------------ configs
+def test_cfg1_full_log_bit_exact(zs, oracle):
+    (job,) = synth.config("cfg1")
+    g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True)
+    compare_step1(oracle, g, job.workload, job.cells)
+    compare_cell(oracle, g, job.workload, job.cells[0], 0, np.arange(job.trials), job.recurrences,
+                 job.trials, logs=True)
+
+
+def test_cfg2_six_workloads_all_trials(zs, oracle):
+    for job in synth.config("cfg2"):
+        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences)
+        compare_step1(oracle, g, job.workload, job.cells)
+        compare_cell(oracle, g, job.workload, job.cells[0], 0, np.arange(job.trials),
+                     job.recurrences, job.trials)
+
+
+def test_cfg3_sweep_sampled_trials(zs, oracle):
+    rng = np.random.default_rng(0)
+    for job in synth.config("cfg3"):
+        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences)
+        compare_step1(oracle, g, job.workload, job.cells)
+        for ci, c in enumerate(job.cells):
+            idx = np.sort(rng.choice(job.trials, size=40, replace=False))
+            compare_cell(oracle, g, job.workload, c, ci, idx, job.recurrences, job.trials,
+                         full_curves=False)
+        # one whole cell per workload, curves included
+        ci = int(rng.integers(len(job.cells)))
+        compare_cell(oracle, g, job.workload, job.cells[ci], ci, np.arange(job.trials),
+                     job.recurrences, job.trials)
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg4_38"])
+def test_cfg4_drift_window(zs, oracle, name):
+    (job,) = synth.config(name)
+    g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences)
+    compare_step1(oracle, g, job.workload, job.cells)
+    compare_cell(oracle, g, job.workload, job.cells[0], 0, np.arange(job.trials), job.recurrences,
+                 job.trials)
+
+
+def test_cfg5_full_size_sampled(zs, oracle):
+    """BASELINE size (10^7 trials x 1000 recurrences, the bench's launch): every 1000th trial
+    bit-exact; curves checked by properties that hold at any size."""
+    (job,) = synth.config("cfg5")
+    g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences,
+                want=["curves", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop",
+                      "final_arm", "counters"])
+    idx = np.arange(0, job.trials, 1000)
+    o = compare_cell(oracle, g, job.workload, job.cells[0], 0, idx, job.recurrences, job.trials,
+                     full_curves=False)
+    c = g["curves"][0]
+    n = job.trials
+    assert np.all(c[:, 4:] <= n) and np.all(c[:, 4:] >= 0)
+    assert np.all(c[:, 3] >= 0)
+    np.testing.assert_allclose(c[:, 0].sum(), g["tot_cost"].sum(), rtol=1e-9)
+    np.testing.assert_allclose(c[:, 1].sum(), g["tot_energy"].sum(), rtol=1e-9)
+    assert c[:, 4].sum() == g["n_stop"].sum() == g["counters"][4]
+    assert g["counters"][0] == n * job.recurrences
+    # the 1-in-1000 sample's curves estimate the full curves (statistical, loose)
+    np.testing.assert_allclose(o["curves"][-100:, 0].sum() * 1000, c[-100:, 0].sum(), rtol=0.05)
+
+
+# ------------------------------------------------------------------ edge cases
+def test_micro_traces_gpu(zs, oracle):
+    import json
+    import os
+
+    from tests.conftest import GOLDEN
+
+    g = json.load(open(os.path.join(GOLDEN, "micro_traces.json")))
+    t = g["trace"]
+    for key in ("W1", "W2"):
+        w = {"batch_sizes": np.array(t["batch_sizes"], np.int32), "b0": t["b0"],
+             "power_limits": np.array(t["power_limits"], float), "max_power": t["max_power"],
+             "max_epochs": t["max_epochs"], "charge_profiling": g[key]["charge_profiling"],
+             "avg_power": np.array(t["avg_power"], float), "throughput": np.array(t["throughput"], float),
+             "pool": np.array(t["pool"], np.int32)}
+        cell = synth.cell(eta=1.0, beta=2.0, seed=5)
+        r = run_gpu(zs, w, [cell], 50, 8, log=True)
+        assert [int(x & 0xFF) for x in r["log"][0]] == g[key]["arms"]
+        np.testing.assert_allclose(r["tot_cost"], g[key]["total_cost"], rtol=1e-13)
+        compare_cell(oracle, r, w, cell, 0, np.arange(50), 8, 50, logs=True)
+
+
+def _random_trace(rng, B, P, S, K, fail=0.2):
+    bs = np.cumsum(rng.integers(1, 9, size=B)).astype(np.int32) * 8
+    pl = np.sort(rng.choice(np.arange(50, 400), size=P, replace=False)).astype(float)
+    MP = float(pl.max())
+    A = rng.uniform(30, MP, size=(B, P))
+    Th = rng.uniform(1e-3, 1e-1, size=(B, P))
+    pool = rng.integers(1, 60, size=(S, B, K)).astype(np.int32)
+    pool[rng.random(pool.shape) < fail] = 0
+    pool[:, 0, 0] = np.maximum(pool[:, 0, 0], 1)
+    return {"batch_sizes": bs, "b0": int(rng.integers(B)), "power_limits": pl, "max_power": MP,
+            "max_epochs": 80, "charge_profiling": int(rng.integers(2)), "avg_power": A,
+            "throughput": Th, "pool": pool}
+
+
+@pytest.mark.parametrize("B,P,S,K,window,beta,trials,R", [
+    (1, 1, 1, 1, 0, 2.0, 37, 9),          # single arm (HPO case), ragged tail
+    (32, 64, 1, 4, 0, 2.0, 130, 40),      # maximum sizes
+    (32, 7, 5, 3, 2, 1.5, 65, 33),        # max arms, smallest window, S not dividing R
+    (7, 5, 3, 2, 4, math.inf, 200, 25),   # no early stop
+    (16, 16, 1, 4, 10, 3.0, 1, 100),      # one trial
+    (5, 3, 1, 1, 0, 1.0000001, 96, 20),   # beta just above 1: stops everywhere
+    (9, 7, 1, 4, 0, 2.0, 300, 0),         # R = 0 -> auto 2|B||P|
+])
+def test_random_traces_edge_cases(zs, oracle, B, P, S, K, window, beta, trials, R):
+    rng = np.random.default_rng(B * 1000 + P)
+    w = _random_trace(rng, B, P, S, K)
+    cells = [synth.cell(eta=e, beta=beta, window=window, seed=int(rng.integers(2**63)),
+                        prior_mean=pm, prior_var=pv)
+             for e, pm, pv in ((0.0, 0.0, math.inf), (1.0, 500.0, 1e6), (0.37, 0.0, math.inf))]
+    g = run_gpu(zs, w, cells, trials, R, log=True)
+    Rr = g["R"]
+    assert Rr == (R if R > 0 else 2 * B * P)
+    compare_step1(oracle, g, w, cells)
+    for ci, c in enumerate(cells):
+        compare_cell(oracle, g, w, c, ci, np.arange(trials), Rr, trials, logs=True)
+
+
+def test_empty_shard_and_sharding_invariance(zs, oracle):
+    """P16: per-trial results do not depend on the shard split (global-index RNG keys)."""
+    (job,) = synth.config("cfg4", trials=3000)
+    w, cells, R = job.workload, job.cells, job.recurrences
+    full = run_gpu(zs, w, cells, 3000, R)
+    parts = [run_gpu(zs, w, cells, 3000, R, shard=(b, e)) for b, e in ((0, 1111), (1111, 2048), (2048, 3000))]
+    for k in ("tot_cost", "digest", "tot_time", "n_stop", "final_arm"):
+        assert np.array_equal(full[k], np.concatenate([p[k] for p in parts]))
+    np.testing.assert_allclose(full["curves"], sum(p["curves"] for p in parts), rtol=1e-12)
+    empty = run_gpu(zs, w, cells, 3000, R, shard=(5000, 6000))
+    assert empty["n"] == 0 and np.all(empty["curves"] == 0)
+
+
+def test_results_into_device_buffers(zs):
+    import torch
+
+    (job,) = synth.config("cfg1")
+    sim = zs.Simulation(job.workload, job.cells, job.trials, job.recurrences).load_profile()
+    stream = torch.cuda.Stream()
+    sim.run(stream)
+    dev = torch.zeros((1, sim.R, 7), dtype=torch.float64, device="cuda")
+    out = sim.results(want=["curves"])
+    out2 = sim.results(want=[], out={"curves": dev})
+    np.testing.assert_array_equal(dev.cpu().numpy(), out["curves"])
+    assert out2["replay_ms"] > 0
+    sim.close()
+
+
+def test_errors_are_reported(zs):
+    (job,) = synth.config("cfg1")
+    w = dict(job.workload)
+    bad = synth.cell(eta=2.0, beta=0.5, window=1)
+    with pytest.raises(zs.ZeusError) as e:
+        zs.Simulation(w, [bad], 10, 5)
+    for frag in ("eta", "beta", "window"):
+        assert frag in str(e.value)
+    sim = zs.Simulation(w, job.cells, 10, 5)
+    with pytest.raises(zs.ZeusError, match="ZEUS_E_STATE"):
+        sim.run()
+    w2 = dict(w)
+    w2["pool"] = np.zeros_like(w["pool"])
+    sim2 = zs.Simulation(w2, job.cells, 10, 5)
+    with pytest.raises(zs.ZeusError, match="NO_CONVERGENT_ARM"):
+        sim2.load_profile()

@@ -1,0 +1,57 @@
+// work_probe.cu -- per-primitive SASS instruction counts of the contract functions
+// (compiled, never run): each probe kernel wraps ONE primitive between a load and a
+// store so `tools/work_model.py` can count its straight-line instructions by pipe.
+#include "../paper_2208_06102_b200/csrc/contract.cuh"
+using namespace zs;
+extern "C" __global__ void probe_empty(const double *in, double *out) {
+  out[threadIdx.x] = in[threadIdx.x];
+}
+extern "C" __global__ void probe_philox(const uint32_t *in, uint32_t *out) {
+  U4 x = philox4x32_10(U4{in[0], in[1], in[2], in[3]}, in[4], in[5]);
+  out[0] = x.x; out[1] = x.y; out[2] = x.z; out[3] = x.w;
+}
+extern "C" __global__ void probe_zlog(const double *in, double *out) { out[0] = zlog(in[0]); }
+extern "C" __global__ void probe_sincospi(const unsigned long long *in, double *out) {
+  double s, c; zsincospi(in[0], s, c); out[0] = s; out[1] = c;
+}
+extern "C" __global__ void probe_sqrt(const double *in, double *out) { out[0] = sqrt(in[0]); }
+extern "C" __global__ void probe_div(const double *in, double *out) { out[0] = in[0] / in[1]; }
+extern "C" __global__ void probe_pair(const long long *in, double *out) {
+  double z0, z1; normal_pair((uint32_t)in[0], (uint32_t)in[1], in[2], (int)in[3], (int)in[4], z0, z1);
+  out[0] = z0; out[1] = z1;
+}
+// theta = fma(sigma, z, mu) + strict-< argmin update (NC-4), per normal used
+extern "C" __global__ void probe_theta(const double *in, double *out, int *arg) {
+  double bt = in[0]; int b = arg[0];
+  const double th = fma(in[1], in[2], in[3]);
+  if (th < bt) { bt = th; b = arg[1]; }
+  out[0] = bt; arg[2] = b;
+}
+// Observe (NC-6), unbounded window, n >= 2 path
+extern "C" __global__ void probe_observe(const double *in, double *out, const int *nin) {
+  const double C = in[0], sh = in[1];
+  double S1 = in[2], S2 = in[3];
+  const int n = nin[0] + 1;
+  const double d = C - sh;
+  S1 = S1 + d; S2 = S2 + d * d;
+  const double dn = (double)n;
+  const double mean = sh + S1 / dn;
+  double s2 = (S2 - (S1 * S1) / dn) / (dn - 1.0);
+  const double fl = 1e-12 * (1.0 + mean * mean);
+  if (!(s2 >= fl)) s2 = fl;
+  const double q = 1.0 / s2;
+  const double var = 1.0 / (in[4] + dn * q);
+  const double sum = dn * sh + S1;
+  out[0] = var * (in[5] + sum * q); out[1] = sqrt(var); out[2] = S1; out[3] = S2;
+}
+// trace lookup + charge + early-stop test (NC-5), not-stopped path
+extern "C" __global__ void probe_charge(const double *in, const int *pool, double *out, long long trial, int t) {
+  const uint32_t r = replica(1u, 2u, trial, t, 4u);
+  const int E = pool[r];
+  const int Erun = E > 0 ? E : 99;
+  const double em1 = (double)(Erun - 1);
+  const double Cf = in[0] + em1 * in[1];
+  const double thr = in[6] * in[7];
+  out[0] = Cf; out[1] = in[2] + em1 * in[3]; out[2] = in[4] + em1 * in[5];
+  out[3] = (Cf > thr) ? 1.0 : 0.0;
+}

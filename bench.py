@@ -31,6 +31,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 from paper_2208_06102_b200 import synth  # noqa: E402
+from paper_2208_06102_b200.sharding import reduce_curves, shard_range  # noqa: E402
 
 METRIC = "simulated bandit decisions/sec (trials x recurrences) at 1/2/4/8 B200 vs roofline"
 UNIT = "decisions/s"
@@ -221,11 +222,7 @@ def main():
     if len(jobs) != 1:
         raise SystemExit("bench runs single-job configs (cfg1, cfg4, cfg5)")
     job = jobs[0]
-    per = job.trials
-    if args.scaling == "weak":
-        total, begin, end = per * world, per * rank, per * (rank + 1)
-    else:
-        total, begin, end = per, per * rank // world, per * (rank + 1) // world
+    total, begin, end = shard_range(job.trials, world, rank, args.scaling)
     sim = Simulation(job.workload, job.cells, total, job.recurrences, shard=(begin, end),
                      device=local, layout=args.layout).load_profile()
     R, nc = sim.R, sim.ncells
@@ -237,8 +234,7 @@ def main():
         sim.run(stream)
         with torch.cuda.stream(stream):
             r = sim.results(want=["counters"], out={"curves": curves})
-            if dist:
-                dist.all_reduce(curves)
+            reduce_curves(curves)
         return r
 
     for _ in range(args.warmup):
@@ -294,9 +290,7 @@ def main():
         sim.run(stream)
         sim.results(want=[], out=host_out)
         if dist:
-            cd = cur_h.to(dev)
-            dist.all_reduce(cd)
-            cur_h.copy_(cd.cpu())
+            cur_h.copy_(reduce_curves(cur_h.to(dev)).cpu())
     torch.cuda.synchronize()
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if dist:

@@ -1,0 +1,32 @@
+"""Trial sharding across ranks and the cross-GPU curve reduction.
+
+Trials are independent and RNG counters use the GLOBAL trial index (NC-3), so a
+rank only needs its [begin, end) range; the one collective is an all-reduce
+(SUM) of the [cells][R][7] curves tensor (NCCL on GPUs, gloo in CPU tests).
+"""
+from __future__ import annotations
+
+
+def shard_range(trials_per_gpu: int, world: int, rank: int, scaling: str = "weak"):
+    """Returns (global_trials, begin, end) of this rank.
+
+    weak:   every rank owns trials_per_gpu trials; the job has world * trials_per_gpu.
+    strong: one job of trials_per_gpu trials split as evenly as possible.
+    """
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    if scaling == "weak":
+        return trials_per_gpu * world, trials_per_gpu * rank, trials_per_gpu * (rank + 1)
+    if scaling == "strong":
+        n = trials_per_gpu
+        return n, n * rank // world, n * (rank + 1) // world
+    raise ValueError(scaling)
+
+
+def reduce_curves(curves, group=None):
+    """Sums per-rank curves in place (counts travel as exact fp64 integers < 2^53)."""
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(curves, op=dist.ReduceOp.SUM, group=group)
+    return curves

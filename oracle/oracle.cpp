@@ -36,9 +36,6 @@ double with_high_word(double d, int32_t hi) {
   u = (u & 0xffffffffULL) | ((uint64_t)(uint32_t)hi << 32);
   return bits_to_double(u);
 }
-double from_words(int32_t hi, uint32_t lo) {
-  return bits_to_double(((uint64_t)(uint32_t)hi << 32) | lo);
-}
 
 // ---------------------------------------------------------------- Philox4x32-10
 // Salmon et al., "Parallel random numbers: as easy as 1, 2, 3" (SC'11);
@@ -64,9 +61,12 @@ void philox(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
 }
 
 // ---------------------------------------------------------------- zlog
-// fdlibm e_log.c (__ieee754_log) for a positive normal x, with the two
-// shortcut branches (|f| < 2^-20 and k == 0) folded into the general
-// formulas (contract NC-3; the general formulas are the same algorithm).
+// fdlibm e_log.c (__ieee754_log) for a positive normal x (NC-3): x = 2^k (1+f),
+// s = f/(2+f), R(z) the Lg1..Lg7 minimax polynomial, then
+// log x = k*ln2_hi - ((hfsq - (s*(hfsq+R) + k*ln2_lo)) - f).  fdlibm's shortcut
+// branches (|f| < 2^-20, k == 0, and the alternative form used near sqrt(2)/2..
+// sqrt(2) boundaries) are all folded into this one formula, and the two
+// polynomial halves are evaluated with explicit fma.
 double zlog(double x) {
   const double ln2_hi = 6.93147180369123816490e-01;  // 3fe62e42 fee00000
   const double ln2_lo = 1.90821492927058770002e-10;  // 3dea39ef 35793c76
@@ -84,70 +84,59 @@ double zlog(double x) {
   x = with_high_word(x, hx | (i ^ 0x3ff00000));   // normalise x or x/2
   k += (i >> 20);
   double f = x - 1.0;
+  double hfsq = 0.5 * f * f;
   double s = f / (2.0 + f);
-  double dk = (double)k;
   double z = s * s;
-  i = hx - 0x6147a;
   double w = z * z;
-  int32_t j = 0x6b851 - hx;
-  double t1 = w * (Lg2 + w * (Lg4 + w * Lg6));
-  double t2 = z * (Lg1 + w * (Lg3 + w * (Lg5 + w * Lg7)));
-  i |= j;
+  double t1 = w * std::fma(w, std::fma(w, Lg6, Lg4), Lg2);
+  double t2 = z * std::fma(w, std::fma(w, std::fma(w, Lg7, Lg5), Lg3), Lg1);
   double R = t2 + t1;
-  if (i > 0) {
-    double hfsq = 0.5 * f * f;
-    return dk * ln2_hi - ((hfsq - (s * (hfsq + R) + dk * ln2_lo)) - f);
-  }
-  return dk * ln2_hi - ((s * (f - R) - dk * ln2_lo) - f);
+  double dk = (double)k;
+  return dk * ln2_hi - ((hfsq - (s * (hfsq + R) + dk * ln2_lo)) - f);
 }
 
-// ---------------------------------------------------------------- sin/cos kernels
-// fdlibm k_sin.c / k_cos.c for |x| <= pi/4, x + y the argument (iy = 1).
-double kernel_sin(double x, double y) {
-  const double S1 = -1.66666666666666324348e-01;  // BFC55555 55555549
-  const double S2 = 8.33333333332248946124e-03;   // 3F811111 1110F8A6
-  const double S3 = -1.98412698298579493134e-04;  // BF2A01A0 19C161D5
-  const double S4 = 2.75573137070700676789e-06;   // 3EC71DE3 57B1FE7D
-  const double S5 = -2.50507602534068634195e-08;  // BE5AE5E6 8A2B9CEB
-  const double S6 = 1.58969099521155010221e-10;   // 3DE5D93A 5ACFD57C
-  double z = x * x;
-  double v = z * x;
-  double r = S2 + z * (S3 + z * (S4 + z * (S5 + z * S6)));
-  return x - ((z * (0.5 * y - v * r) - y) - v * S1);
-}
-
-double kernel_cos(double x, double y) {
-  const double C1 = 4.16666666666666019037e-02;   // 3FA55555 5555554C
-  const double C2 = -1.38888888888741095749e-03;  // BF56C16C 16C15177
-  const double C3 = 2.48015872894767294178e-05;   // 3EFA01A0 19CB1590
-  const double C4 = -2.75573143513906633035e-07;  // BE927E4F 809C52AD
-  const double C5 = 2.08757232129817482790e-09;   // 3E21EE9E BDB4B1C4
-  const double C6 = -1.13596475577881948265e-11;  // BDA8FAE9 BE8838D4
-  int32_t ix = high_word(x) & 0x7fffffff;
-  double z = x * x;
-  double r = z * (C1 + z * (C2 + z * (C3 + z * (C4 + z * (C5 + z * C6)))));
-  if (ix < 0x3FD33333) return 1.0 - (0.5 * z - (z * r - x * y));  // |x| < 0.3
-  double qx;
-  if (ix > 0x3fe90000) qx = 0.28125;                               // |x| > 0.78125
-  else qx = from_words(ix - 0x00200000, 0u);                       // |x|/4
-  double hz = 0.5 * z - qx;
-  double a = 1.0 - qx;
-  return a - (hz - (z * r - x * y));
-}
-
-// sin(pi*x), cos(pi*x) for x = m / 2^51, 0 <= m < 2^52 (i.e. x = 2v, v in [0,1)).
-// The reduction x = n/2 + f, |f| <= 1/4, is done exactly in integers; pi*f is
-// carried as a double-double (contract NC-3).
+// ---------------------------------------------------------------- sin / cos of pi*x
+// sin(pi*x), cos(pi*x) for x = m / 2^51, 0 <= m < 2^52 (x = 2v, v in [0,1)), NC-3:
+// exact integer reduction x = n/2 + f with |f| <= 1/4, then the Taylor series of
+// sin(pi f) and cos(pi f) (coefficients (-1)^k pi^(2k+1)/(2k+1)! and
+// (-1)^k pi^(2k)/(2k)!, each rounded to the nearest double; truncation error
+// < 1e-19 at |f| = 1/4) by explicit-fma Horner, with pi*f carried as a
+// double-double in the sine's leading term.
 void zsincospi(uint64_t m, double *s_out, double *c_out) {
-  const double PI = 3.14159265358979311600e+00;     // 400921FB 54442D18
-  const double PI_LO = 1.22464679914735320717e-16;  // 3CA1A626 33145C07
+  const double PI = 0x1.921fb54442d18p+1;
+  const double PI_LO = 0x1.1a62633145c07p-53;
+  const double S1 = -0x1.4abbce625be53p+2, S2 = 0x1.466bc6775aae2p+1;
+  const double S3 = -0x1.32d2cce62bd86p-1, S4 = 0x1.50783487ee782p-4;
+  const double S5 = -0x1.e3074fde8871fp-8, S6 = 0x1.e8f434d018d63p-12;
+  const double S7 = -0x1.6fadb9f155744p-16, S8 = 0x1.aaec32af93359p-21;
+  const double C1 = -0x1.3bd3cc9be45dep+2, C2 = 0x1.03c1f081b5ac4p+2;
+  const double C3 = -0x1.55d3c7e3cbffap+0, C4 = 0x1.e1f506891babbp-3;
+  const double C5 = -0x1.a6d1f2a204a8cp-6, C6 = 0x1.f9d38a3763cc3p-10;
+  const double C7 = -0x1.b6e24f44b128fp-14, C8 = 0x1.20c62c2f2d7f5p-18;
+  const double C9 = -0x1.2a0c591af8314p-23;
   int64_t n = (int64_t)((m + (1ULL << 49)) >> 50);          // round(2x), 0..4
   int64_t jj = (int64_t)m - n * (int64_t)(1ULL << 50);      // |jj| <= 2^49
   double f = (double)jj * 4.44089209850062616169e-16;       // * 2^-51, exact
-  double a = f * PI;
-  double a_lo = std::fma(f, PI, -a) + f * PI_LO;
-  double sf = kernel_sin(a, a_lo);
-  double cf = kernel_cos(a, a_lo);
+  double f2 = f * f;
+  double ps = std::fma(f2, S8, S7);
+  ps = std::fma(f2, ps, S6);
+  ps = std::fma(f2, ps, S5);
+  ps = std::fma(f2, ps, S4);
+  ps = std::fma(f2, ps, S3);
+  ps = std::fma(f2, ps, S2);
+  ps = std::fma(f2, ps, S1);
+  double hi = f * PI;
+  double lo = std::fma(f, PI_LO, std::fma(f, PI, -hi));
+  double sf = hi + std::fma(f * f2, ps, lo);
+  double pc = std::fma(f2, C9, C8);
+  pc = std::fma(f2, pc, C7);
+  pc = std::fma(f2, pc, C6);
+  pc = std::fma(f2, pc, C5);
+  pc = std::fma(f2, pc, C4);
+  pc = std::fma(f2, pc, C3);
+  pc = std::fma(f2, pc, C2);
+  pc = std::fma(f2, pc, C1);
+  double cf = std::fma(f2, pc, 1.0);
   double s, c;
   switch ((int)(n & 3)) {
     case 0: s = sf; c = cf; break;
@@ -231,8 +220,9 @@ bool observe(Arm &a, double x, int32_t window, const Prior &pr, double *s2_out, 
   int64_t n = (int64_t)a.window.size();
   if (n < 2) return false;
   double dn = (double)n;
-  double mean = a.sh + a.S1 / dn;
-  double s2 = (a.S2 - (a.S1 * a.S1) / dn) / (dn - 1.0);     // σ̃² = Var(C_b), n-1 divisor
+  double inv_n = 1.0 / dn;
+  double mean = a.sh + a.S1 * inv_n;
+  double s2 = (a.S2 - a.S1 * (a.S1 * inv_n)) / (dn - 1.0);  // σ̃² = Var(C_b), n-1 divisor
   double fl = 1e-12 * (1.0 + mean * mean);
   if (!(s2 >= fl)) s2 = fl;                                 // zero-variance floor (R-Q7)
   double q = 1.0 / s2;

@@ -25,19 +25,22 @@ def sources():
                   + [os.path.join(ROOT, "include", "zeus_sim.h")])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=(), extra=()) -> str:
+    """Compiles csrc/zeus_sim.cu into ``out``; ``defines`` (e.g. ["ZS_PAIR_UNROLL=2"]) are
+    for kernel A/B builds only."""
     srcs = sources()
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(f) for f in srcs):
-        return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB, os.path.join(HERE, "csrc", "zeus_sim.cu"), "-lcudart"]
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(f) for f in srcs):
+        return out
+    cmd = [NVCC, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-o", out,
+           os.path.join(HERE, "csrc", "zeus_sim.cu"), "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
-    with open(os.path.join(HERE, "csrc", "ptxas.log"), "w") as f:
+    with open(out + ".ptxas.log", "w") as f:
         f.write(r.stderr)
     if verbose:
         print(r.stderr)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":

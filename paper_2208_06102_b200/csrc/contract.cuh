@@ -1,15 +1,55 @@
 // contract.cuh -- device side of the numerics contract (NC-3/NC-4).
 //
 // Philox4x32-10 (Salmon et al., SC'11), the (0,1] / [0,1) uniform
-// construction, and the contract transcendentals zlog / zsincospi written
-// from fdlibm's published e_log.c, k_sin.c and k_cos.c using only IEEE
-// + - * / sqrt and explicit fma.  This file is compiled with --fmad=false so
+// construction, and the contract transcendentals: zlog from fdlibm's published
+// e_log.c, zsincospi as an exact integer reduction plus the Taylor series of
+// sin/cos(pi f), using only IEEE + - * / sqrt and explicit fma.  This file is compiled with --fmad=false so
 // every a*b+c below is two roundings unless written fma(); it is written
 // independently of the CPU oracle and shares nothing with it.
 #pragma once
 #include <cstdint>
 
 namespace zs {
+
+// fp64 coefficients live in the constant bank so DFMA/DMUL take them as c[][]
+// operands instead of materialising 64-bit immediates with UMOV pairs in the loop.
+#ifdef ZS_IMMEDIATE_CONSTANTS
+#define ZS_C(name, value) constexpr double name = value
+#else
+#define ZS_C(name, value) __constant__ double name = value
+#endif
+namespace cst {
+ZS_C(kLn2Hi, 6.93147180369123816490e-01);
+ZS_C(kLn2Lo, 1.90821492927058770002e-10);
+ZS_C(kLg1, 6.666666666666735130e-01);
+ZS_C(kLg2, 3.999999999940941908e-01);
+ZS_C(kLg3, 2.857142874366239149e-01);
+ZS_C(kLg4, 2.222219843214978396e-01);
+ZS_C(kLg5, 1.818357216161805012e-01);
+ZS_C(kLg6, 1.531383769920937332e-01);
+ZS_C(kLg7, 1.479819860511658591e-01);
+ZS_C(kPi, 0x1.921fb54442d18p+1);
+ZS_C(kPiLo, 0x1.1a62633145c07p-53);
+ZS_C(kS1, -0x1.4abbce625be53p+2);
+ZS_C(kS2, 0x1.466bc6775aae2p+1);
+ZS_C(kS3, -0x1.32d2cce62bd86p-1);
+ZS_C(kS4, 0x1.50783487ee782p-4);
+ZS_C(kS5, -0x1.e3074fde8871fp-8);
+ZS_C(kS6, 0x1.e8f434d018d63p-12);
+ZS_C(kS7, -0x1.6fadb9f155744p-16);
+ZS_C(kS8, 0x1.aaec32af93359p-21);
+ZS_C(kC1, -0x1.3bd3cc9be45dep+2);
+ZS_C(kC2, 0x1.03c1f081b5ac4p+2);
+ZS_C(kC3, -0x1.55d3c7e3cbffap+0);
+ZS_C(kC4, 0x1.e1f506891babbp-3);
+ZS_C(kC5, -0x1.a6d1f2a204a8cp-6);
+ZS_C(kC6, 0x1.f9d38a3763cc3p-10);
+ZS_C(kC7, -0x1.b6e24f44b128fp-14);
+ZS_C(kC8, 0x1.20c62c2f2d7f5p-18);
+ZS_C(kC9, -0x1.2a0c591af8314p-23);
+ZS_C(kTwoM51, 0x1p-51);
+ZS_C(kVarFloor, 1e-12);
+}  // namespace cst
 
 // ------------------------------------------------------------ Philox4x32-10
 struct U4 { uint32_t x, y, z, w; };
@@ -29,18 +69,10 @@ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
 }
 
 // ------------------------------------------------------------ zlog
-// fdlibm __ieee754_log for positive normal x; the |f|<2^-20 and k==0
-// shortcuts are folded into the general formulas (NC-3).
+// fdlibm __ieee754_log for positive normal x, one formula for every f (the
+// shortcut branches folded in), polynomial halves by explicit fma (NC-3).
 __device__ __forceinline__ double zlog(double x) {
-  constexpr double kLn2Hi = 6.93147180369123816490e-01;
-  constexpr double kLn2Lo = 1.90821492927058770002e-10;
-  constexpr double kLg1 = 6.666666666666735130e-01;
-  constexpr double kLg2 = 3.999999999940941908e-01;
-  constexpr double kLg3 = 2.857142874366239149e-01;
-  constexpr double kLg4 = 2.222219843214978396e-01;
-  constexpr double kLg5 = 1.818357216161805012e-01;
-  constexpr double kLg6 = 1.531383769920937332e-01;
-  constexpr double kLg7 = 1.479819860511658591e-01;
+  using namespace cst;
   int hx = __double2hiint(x);
   const int lx = __double2loint(x);
   int k = (hx >> 20) - 1023;
@@ -49,64 +81,46 @@ __device__ __forceinline__ double zlog(double x) {
   const double xn = __hiloint2double(hx | (i0 ^ 0x3ff00000), lx);
   k += (i0 >> 20);
   const double f = xn - 1.0;
+  const double hfsq = 0.5 * f * f;
   const double s = f / (2.0 + f);
-  const double dk = (double)k;
   const double z = s * s;
   const double w = z * z;
-  const double t1 = w * (kLg2 + w * (kLg4 + w * kLg6));
-  const double t2 = z * (kLg1 + w * (kLg3 + w * (kLg5 + w * kLg7)));
-  const int sel = (hx - 0x6147a) | (0x6b851 - hx);
+  const double t1 = w * fma(w, fma(w, kLg6, kLg4), kLg2);
+  const double t2 = z * fma(w, fma(w, fma(w, kLg7, kLg5), kLg3), kLg1);
   const double R = t2 + t1;
-  if (sel > 0) {
-    const double hfsq = 0.5 * f * f;
-    return dk * kLn2Hi - ((hfsq - (s * (hfsq + R) + dk * kLn2Lo)) - f);
-  }
-  return dk * kLn2Hi - ((s * (f - R) - dk * kLn2Lo) - f);
+  const double dk = (double)k;
+  return dk * kLn2Hi - ((hfsq - (s * (hfsq + R) + dk * kLn2Lo)) - f);
 }
 
-// ------------------------------------------------------------ sin / cos kernels (|x| <= pi/4)
-__device__ __forceinline__ double ksin(double x, double y) {
-  constexpr double kS1 = -1.66666666666666324348e-01;
-  constexpr double kS2 = 8.33333333332248946124e-03;
-  constexpr double kS3 = -1.98412698298579493134e-04;
-  constexpr double kS4 = 2.75573137070700676789e-06;
-  constexpr double kS5 = -2.50507602534068634195e-08;
-  constexpr double kS6 = 1.58969099521155010221e-10;
-  const double z = x * x;
-  const double v = z * x;
-  const double r = kS2 + z * (kS3 + z * (kS4 + z * (kS5 + z * kS6)));
-  return x - ((z * (0.5 * y - v * r) - y) - v * kS1);
-}
-
-__device__ __forceinline__ double kcos(double x, double y) {
-  constexpr double kC1 = 4.16666666666666019037e-02;
-  constexpr double kC2 = -1.38888888888741095749e-03;
-  constexpr double kC3 = 2.48015872894767294178e-05;
-  constexpr double kC4 = -2.75573143513906633035e-07;
-  constexpr double kC5 = 2.08757232129817482790e-09;
-  constexpr double kC6 = -1.13596475577881948265e-11;
-  const int ix = __double2hiint(x) & 0x7fffffff;
-  const double z = x * x;
-  const double r = z * (kC1 + z * (kC2 + z * (kC3 + z * (kC4 + z * (kC5 + z * kC6)))));
-  if (ix < 0x3FD33333) return 1.0 - (0.5 * z - (z * r - x * y));
-  const double qx = (ix > 0x3fe90000) ? 0.28125 : __hiloint2double(ix - 0x00200000, 0);
-  const double hz = 0.5 * z - qx;
-  const double a = 1.0 - qx;
-  return a - (hz - (z * r - x * y));
-}
-
-// sin(pi*m/2^51), cos(pi*m/2^51) for 0 <= m < 2^52: exact integer reduction to
-// n/2 + f, |f| <= 1/4, pi*f as a double-double.
+// ------------------------------------------------------------ sin / cos of pi*m/2^51
+// Exact integer reduction to n/2 + f, |f| <= 1/4; Taylor series of sin(pi f),
+// cos(pi f) (coefficients rounded to nearest double) by fma Horner; pi*f as a
+// double-double in the sine's leading term (NC-3).
 __device__ __forceinline__ void zsincospi(uint64_t m, double &s, double &c) {
-  constexpr double kPi = 3.14159265358979311600e+00;
-  constexpr double kPiLo = 1.22464679914735320717e-16;
+  using namespace cst;
   const int64_t n = (int64_t)((m + (1ull << 49)) >> 50);
   const int64_t j = (int64_t)m - (n << 50);
-  const double f = (double)j * 4.44089209850062616169e-16;   // 2^-51
-  const double a = f * kPi;
-  const double alo = fma(f, kPi, -a) + f * kPiLo;
-  const double sf = ksin(a, alo);
-  const double cf = kcos(a, alo);
+  const double f = (double)j * kTwoM51;                      // exact
+  const double f2 = f * f;
+  double ps = fma(f2, kS8, kS7);
+  ps = fma(f2, ps, kS6);
+  ps = fma(f2, ps, kS5);
+  ps = fma(f2, ps, kS4);
+  ps = fma(f2, ps, kS3);
+  ps = fma(f2, ps, kS2);
+  ps = fma(f2, ps, kS1);
+  const double hi = f * kPi;
+  const double lo = fma(f, kPiLo, fma(f, kPi, -hi));
+  const double sf = hi + fma(f * f2, ps, lo);
+  double pc = fma(f2, kC9, kC8);
+  pc = fma(f2, pc, kC7);
+  pc = fma(f2, pc, kC6);
+  pc = fma(f2, pc, kC5);
+  pc = fma(f2, pc, kC4);
+  pc = fma(f2, pc, kC3);
+  pc = fma(f2, pc, kC2);
+  pc = fma(f2, pc, kC1);
+  const double cf = fma(f2, pc, 1.0);
   const int q = (int)(n & 3);
   const double ss = (q & 1) ? cf : sf;
   const double cc = (q & 1) ? sf : cf;
@@ -114,11 +128,38 @@ __device__ __forceinline__ void zsincospi(uint64_t m, double &s, double &c) {
   c = ((q + 1) & 2) ? -cc : cc;           // q=0: cf  1: -sf 2: -cf  3: sf
 }
 
+// Philox with the 10 round keys precomputed (the key is per cell, so the
+// schedule is hoisted out of the replay loop).
+struct RoundKeys { uint32_t k0[10], k1[10]; };
+__device__ __forceinline__ RoundKeys round_keys(uint32_t k0, uint32_t k1) {
+  RoundKeys r;
+#pragma unroll
+  for (int i = 0; i < 10; ++i) { r.k0[i] = k0; r.k1[i] = k1; k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+  return r;
+}
+__device__ __forceinline__ U4 philox4x32_10(U4 c, const RoundKeys &rk) {
+  constexpr uint32_t kMul0 = 0xD2511F53u, kMul1 = 0xCD9E8D57u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(kMul0, c.x), lo0 = kMul0 * c.x;
+    const uint32_t hi1 = __umulhi(kMul1, c.z), lo1 = kMul1 * c.z;
+    c = U4{hi1 ^ c.y ^ rk.k0[r], lo1, hi0 ^ c.w ^ rk.k1[r], lo0};
+  }
+  return c;
+}
+
 // Box-Muller pair for arms (2k, 2k+1) of `trial` at recurrence t (NC-3).
+#ifdef ZS_ROUND_KEYS
+__device__ __forceinline__ void normal_pair(const RoundKeys &key, int64_t trial, int t, int k,
+                                            double &z0, double &z1) {
+  const U4 x = philox4x32_10(U4{(uint32_t)t, 0x01000000u | (uint32_t)k, (uint32_t)trial,
+                                (uint32_t)((uint64_t)trial >> 32)}, key);
+#else
 __device__ __forceinline__ void normal_pair(uint32_t key0, uint32_t key1, int64_t trial, int t,
                                             int k, double &z0, double &z1) {
   const U4 x = philox4x32_10(U4{(uint32_t)t, 0x01000000u | (uint32_t)k, (uint32_t)trial,
                                 (uint32_t)((uint64_t)trial >> 32)}, key0, key1);
+#endif
   const uint64_t w0 = ((uint64_t)x.y << 32) | x.x;
   const uint64_t w1 = ((uint64_t)x.w << 32) | x.z;
   const double u1 = 2.0 - __longlong_as_double((long long)(0x3FF0000000000000ull | (w0 >> 12)));

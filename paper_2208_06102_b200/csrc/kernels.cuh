@@ -7,15 +7,17 @@
 //                  (P:L559), Observe (Alg. 2), curves + digests (a2..a7).
 //   curve_reduce   sums the atomic curve slots in a fixed order (a7).
 //
-// Layout: one thread per trial; the arm state of a trial lives
-// in shared memory as [field][arm][thread] so a warp's accesses hit 32
-// consecutive 8-byte words; the per-cell tables (arm constants, the trace
-// pool, pseudo-regret table) are staged once per block into shared memory
-// with a 1-D TMA bulk copy (cp.async.bulk) completing on an mbarrier.
+// Layout: one thread per trial; per-cell tables (arm constants,
+// the trace pool, pseudo-regret table) are staged once per block into shared
+// memory with a 1-D TMA bulk copy (cp.async.bulk) completing on an mbarrier.
 #pragma once
 #include <cstdint>
 
 #include "contract.cuh"
+
+#ifndef ZS_PAIR_UNROLL
+#define ZS_PAIR_UNROLL 1
+#endif
 
 namespace zs {
 
@@ -135,7 +137,10 @@ struct ReplayArgs {
   unsigned long long *counters;   // [kCounters]
   int B, S, K, R, max_epochs, charge_profiling, b0, nslot, reg_stride, opt_stride;
   int tab_bytes;                  // bytes of the staged table region (multiple of 16)
-  int ring_n;                     // ring slots per arm in the smem layout (max window)
+  // Observe statistics in global memory, [arm][stride] (+ ring [slot][arm][stride])
+  double *st_sh, *st_S1, *st_S2, *st_ring;
+  int32_t *st_cnt;
+  size_t st_stride;               // = total shard trials over all cells
 };
 
 // shared-memory table region of one block: [ArmConst B][regret S*B][opt_arm S][pool S*B*K]
@@ -195,10 +200,24 @@ enum : int { kStart = 0, kDown = 1, kUp = 2 };
 __device__ __forceinline__ uint32_t below_mask(int c) { return c <= 0 ? 0u : ((1u << c) - 1u); }
 __device__ __forceinline__ uint32_t above_mask(int c) { return c >= 31 ? 0u : ~((2u << c) - 1u); }
 
-// One thread per trial.  WINDOWED: N > 0 (ring buffer per arm).  LOG: write the
-// per-decision log.  Dynamic smem = tab_bytes + per-thread arm state.
+// One thread per trial.  WINDOWED: some cell has N > 0 (ring buffer per arm).
+// LOG: write the per-decision log.
+//
+// State placement:
+//   registers  per-trial scalars: best, the Alg. 3 state machine, bitmasks
+//              (profiled, seen, mature = n >= 2, survivors), totals, digest;
+//   smem       (mu, sigma) per arm as double2 [arm][thread] -- read for every
+//              survivor in every Thompson draw;
+//   global     the Observe statistics (sh, S1, S2, cnt, ring) [arm][trial],
+//              touched once per decision for the chosen arm only; the working
+//              set of resident trials (~30 MB) stays in L2.
+#ifdef ZS_MAXNREG
+#define ZS_REPLAY_BOUNDS __maxnreg__(ZS_MAXNREG)
+#else
+#define ZS_REPLAY_BOUNDS __launch_bounds__(128)
+#endif
 template <bool WINDOWED, bool LOG>
-__global__ void __launch_bounds__(128) replay_kernel(ReplayArgs a) {
+__global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
   const int cell = blockIdx.y;
@@ -232,41 +251,43 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs a) {
   const int32_t *optarm = reinterpret_cast<const int32_t *>(smem + L.optarm);
   const int32_t *pool = reinterpret_cast<const int32_t *>(smem + L.pool);
   const int B = a.B, R = a.R, S = a.S, K = a.K;
-  // per-thread state: [field][arm][thread]
-  double *s_mu = reinterpret_cast<double *>(smem + a.tab_bytes);
-  double *s_sig = s_mu + B * TPB;
-  double *s_sh = s_sig + B * TPB;
-  double *s_S1 = s_sh + B * TPB;
-  double *s_S2 = s_S1 + B * TPB;
-  double *s_ring = s_S2 + B * TPB;                          // [N][B][TPB] when WINDOWED
-  int32_t *s_cnt = reinterpret_cast<int32_t *>(s_ring + (WINDOWED ? a.ring_n * B * TPB : 0));
-#define ST(arr, arm_) arr[(arm_) * TPB + tid]
+  double2 *s_ms = reinterpret_cast<double2 *>(smem + a.tab_bytes);   // [arm][thread] (mu, sigma)
 
   const int64_t jj = j0 + tid;
   const bool active = jj < cp.n;
   const int64_t trial = cp.begin + jj;
+  const size_t o = (size_t)(cp.out_off + jj);              // this trial's column in the state
+  const size_t stride = a.st_stride;
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
   double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+#ifdef ZS_ROUND_KEYS
+  const RoundKeys rkeys = round_keys(cp.key0, cp.key1);
+#define ZS_KEYARG rkeys
+#else
+#define ZS_KEYARG cp.key0, cp.key1
+#endif
 
-  for (int b = 0; b < B; ++b) ST(s_cnt, b) = 0;
-  uint32_t profiled = 0, mature = 0;                        // bit a: profiled / n_a >= 2
+  uint32_t profiled = 0, seen = 0, mature = 0;              // bit a: profiled / observed / n_a >= 2
   double best = kInf;                                       // min_t C_t
   bool in_ts = false;
   int round = 1, step = kStart, start = a.b0, cursor = a.b0;
-  uint32_t cand = (B == 32) ? 0xffffffffu : ((1u << B) - 1u), surv = 0, ts_set = 0;
+  uint32_t cand = (B == 32) ? 0xffffffffu : ((1u << B) - 1u), surv = 0, ts_set = 0, ts_pairs = 0;
   double r1_cost = kInf;
   int r1_arm = -1;
   double totC = 0.0, totE = 0.0, totT = 0.0;
   unsigned long long dig = 0xcbf29ce484222325ull;
   int nstop = 0, last_b = -1;
-  unsigned long long ctr[kCounters] = {0, 0, 0, 0, 0, 0, 0, 0};
+  // event counters (u32 per trial; the pair/normal counts follow from n_sampled
+  // because the survivor set is fixed during Thompson sampling)
+  uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
 
+  int s = 0;                                                // slice of t = floor(t*S/R) (R-Q19)
   for (int t = 0; t < R; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0;
+    while ((long long)(s + 1) * R <= (long long)t * S) ++s;   // no 64-bit division per decision
     if (active) {
-      const int s = (int)(((long long)t * S) / R);
       // ---------------- step 2: decide b_t
       const bool ts_dec = in_ts;
       int b;
@@ -274,35 +295,61 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs a) {
         b = (step == kStart) ? start
           : (step == kDown) ? 31 - __clz(cand & below_mask(cursor))
                             : __ffs(cand & above_mask(cursor)) - 1;
-        ctr[5] += 1;
+        n_prune += 1;
       } else {
         const uint32_t unripe = ts_set & ~mature;
         if (unripe) {
           b = __ffs(unripe) - 1;                            // explore arms with n < 2 first
-          ctr[6] += 1;
+          n_forced += 1;
         } else {
+          // Alg. 1: θ_a ~ N(μ_a, σ_a²) for every survivor, b = argmin θ.  Each lane walks
+          // only its own survivor pairs (ascending k keeps the strict-< tie rule).
           double bt = kInf;
           b = -1;
-          for (int k = 0; 2 * k < B; ++k) {                 // Alg. 1: sample, then argmin
-            const uint32_t pm = (ts_set >> (2 * k)) & 3u;
-            if (!pm) continue;
-            double z0, z1;
-            normal_pair(cp.key0, cp.key1, trial, t, k, z0, z1);
-            ctr[2] += 1;
-            if (pm & 1u) {
-              const double th = fma(ST(s_sig, 2 * k), z0, ST(s_mu, 2 * k));
-              ctr[3] += 1;
-              if (th < bt) { bt = th; b = 2 * k; }
-            }
-            if (pm & 2u) {
-              const double th = fma(ST(s_sig, 2 * k + 1), z1, ST(s_mu, 2 * k + 1));
-              ctr[3] += 1;
-              if (th < bt) { bt = th; b = 2 * k + 1; }
-            }
+          uint32_t pm = ts_pairs;
+          auto consider = [&](int k, double z0, double z1) {   // branch-free (selects)
+            const uint32_t two = (ts_set >> (2 * k)) & 3u;
+            const double2 m0 = s_ms[(2 * k) * TPB + tid];
+            const double2 m1 = s_ms[(2 * k + 1) * TPB + tid];
+            const double th0 = fma(m0.y, z0, m0.x);
+            const bool take0 = (two & 1u) && (th0 < bt);
+            bt = take0 ? th0 : bt;
+            b = take0 ? 2 * k : b;
+            const double th1 = fma(m1.y, z1, m1.x);
+            const bool take1 = (two & 2u) && (th1 < bt);
+            bt = take1 ? th1 : bt;
+            b = take1 ? 2 * k + 1 : b;
+          };
+#if ZS_PAIR_UNROLL == 2
+          while (pm) {                                      // two independent pairs in flight
+            const int k0 = __ffs(pm) - 1;
+            pm &= pm - 1u;
+            const bool has1 = pm != 0u;
+            const int k1 = has1 ? __ffs(pm) - 1 : k0;
+            if (has1) pm &= pm - 1u;
+            double z00, z01, z10, z11;
+            normal_pair(ZS_KEYARG, trial, t, k0, z00, z01);
+            normal_pair(ZS_KEYARG, trial, t, k1, z10, z11);
+            consider(k0, z00, z01);
+            if (has1) consider(k1, z10, z11);
           }
-          ctr[1] += 1;
+#else
+          while (pm) {
+            const int k = __ffs(pm) - 1;
+            pm &= pm - 1u;
+            double z0, z1;
+            normal_pair(ZS_KEYARG, trial, t, k, z0, z1);
+            consider(k, z0, z1);
+          }
+#endif
+          n_sampled += 1;
         }
       }
+      // Observe statistics of arm b: issue the loads now, consume after the charge
+      const size_t so = (size_t)b * stride + o;
+      const bool was_seen = (seen >> b) & 1u;
+      const int cnt_g = a.st_cnt[so];
+      const double sh_g = a.st_sh[so], S1_g = a.st_S1[so], S2_g = a.st_S2[so];
       const ArmConst ac = arm[b];
       // ---------------- step 3: replay one recorded run
       const uint32_t r = replica(cp.key0, cp.key1, trial, t, (uint32_t)K);
@@ -338,14 +385,14 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs a) {
       if (conv && !(C >= best)) best = C;
       // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
       {
-        const int cnt = ST(s_cnt, b);
+        const int cnt = was_seen ? cnt_g : 0;
         double sh, S1, S2;
-        if (cnt == 0) { sh = C; S1 = 0.0; S2 = 0.0; ST(s_sh, b) = sh; }
-        else { sh = ST(s_sh, b); S1 = ST(s_S1, b); S2 = ST(s_S2, b); }
+        if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; a.st_sh[so] = sh; }
+        else { sh = sh_g; S1 = S1_g; S2 = S2_g; }
         int n = cnt;
         if (WINDOWED && cp.window > 0) {
           const int N = cp.window;
-          double *slot = &s_ring[((cnt % N) * B + b) * TPB + tid];
+          double *slot = &a.st_ring[((size_t)(cnt % N) * B + b) * stride + o];
           if (cnt >= N) {
             const double dy = *slot - sh;
             S1 = S1 - dy;
@@ -358,26 +405,25 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs a) {
         S1 = S1 + d;
         S2 = S2 + d * d;
         n += 1;
-        ST(s_S1, b) = S1;
-        ST(s_S2, b) = S2;
-        ST(s_cnt, b) = cnt + 1;
+        a.st_S1[so] = S1;
+        a.st_S2[so] = S2;
+        a.st_cnt[so] = cnt + 1;
+        seen |= 1u << b;
         if (n >= 2) {
           const double dn = (double)n;
-          const double mean = sh + S1 / dn;
-          double s2 = (S2 - (S1 * S1) / dn) / (dn - 1.0);
-          const double fl = 1e-12 * (1.0 + mean * mean);
+          const double inv_n = 1.0 / dn;
+          const double mean = sh + S1 * inv_n;
+          double s2 = (S2 - S1 * (S1 * inv_n)) / (dn - 1.0);
+          const double fl = cst::kVarFloor * (1.0 + mean * mean);
           if (!(s2 >= fl)) s2 = fl;
           const double q = 1.0 / s2;
           const double var = 1.0 / (cp.prec0 + dn * q);
           const double sum = dn * sh + S1;
-          ST(s_mu, b) = var * (cp.pm0 + sum * q);
-          ST(s_sig, b) = sqrt(var);
+          s_ms[b * TPB + tid] = make_double2(var * (cp.pm0 + sum * q), sqrt(var));
           mature |= 1u << b;
-          ctr[7] += 1;
+          n_recomp += 1;
         }
       }
-      ctr[0] += 1;
-      if (stopped) ctr[4] += 1;
       // ---------------- Alg. 3 bookkeeping
       if (!in_ts) {
         if (conv) {
@@ -402,6 +448,9 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs a) {
           } else {
             in_ts = true;
             ts_set = surv;
+            ts_pairs = 0u;
+            for (int k = 0; 2 * k < B; ++k)
+              if ((ts_set >> (2 * k)) & 3u) ts_pairs |= 1u << k;
           }
         }
       }
@@ -416,7 +465,7 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs a) {
       dig = (dig ^ (unsigned long long)(uint32_t)b) * 0x100000001b3ull;
       dig = (dig ^ (unsigned long long)(uint32_t)ac.pstar) * 0x100000001b3ull;
       dig = (dig ^ (unsigned long long)flags) * 0x100000001b3ull;
-      if (LOG) a.log[(size_t)(cp.out_off + jj) * R + t] = (uint32_t)b | ((uint32_t)ac.pstar << 8) | (flags << 16);
+      if (LOG) a.log[o * R + t] = (uint32_t)b | ((uint32_t)ac.pstar << 8) | (flags << 16);
       vC = C;
       vE = En;
       vT = Tm;
@@ -440,9 +489,7 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs a) {
       if ((vPacked >> 16) & 0xff) atomicAdd(row + 6, (double)((vPacked >> 16) & 0xff));
     }
   }
-#undef ST
   if (active) {
-    const size_t o = (size_t)(cp.out_off + jj);
     a.tot_cost[o] = totC;
     a.tot_energy[o] = totE;
     a.tot_time[o] = totT;
@@ -450,6 +497,10 @@ __global__ void __launch_bounds__(128) replay_kernel(ReplayArgs a) {
     a.n_stop[o] = nstop;
     a.final_arm[o] = last_b;
   }
+  unsigned long long ctr[kCounters] = {
+      active ? (unsigned long long)R : 0ull, n_sampled,
+      (unsigned long long)n_sampled * __popc(ts_pairs), (unsigned long long)n_sampled * __popc(ts_set),
+      (unsigned long long)nstop, n_prune, n_forced, n_recomp};
 #pragma unroll
   for (int q = 0; q < kCounters; ++q) {
     unsigned long long v = ctr[q];

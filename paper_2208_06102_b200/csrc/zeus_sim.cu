@@ -47,7 +47,7 @@ struct zeus_sim {
   // cells / run
   std::vector<zeus_cell> cells;
   std::vector<zs::CellParam> cpar;
-  int R = 0, log_mode = 0, layout = 0, device = 0;
+  int R = 0, log_mode = 0, layout = 0, device = 0, wmax = 0;
   int64_t shard_total = 0, max_shard = 0;
   // trace
   int S = 0, K = 0, reg_stride = 0, opt_stride = 0;
@@ -59,7 +59,7 @@ struct zeus_sim {
   // device memory
   DevBuf d_A, d_Th, d_pool, d_cells, d_arms, d_regret, d_opt, d_optarm;
   DevBuf d_slots, d_curves, d_tot_cost, d_tot_energy, d_tot_time, d_digest, d_nstop, d_final,
-      d_log, d_counters;
+      d_log, d_counters, d_st_sh, d_st_S1, d_st_S2, d_st_cnt, d_st_ring;
   ~zeus_sim() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -209,6 +209,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
   s->R = opts->recurrences > 0 ? opts->recurrences : 2 * s->B * s->P;
   s->log_mode = opts->log_mode;
   s->layout = opts->layout;
+  for (int i = 0; i < num_cells; ++i) s->wmax = std::max(s->wmax, (int)cells[i].window);
   int64_t off = 0;
   for (int i = 0; i < num_cells; ++i) {
     const zeus_cell &c = cells[i];
@@ -246,7 +247,12 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
       (e = s->d_nstop.alloc(n * 4)) != cudaSuccess ||
       (e = s->d_final.alloc(n * 4)) != cudaSuccess ||
       (e = s->d_log.alloc(s->log_mode ? n * (size_t)s->R * 4 : 0)) != cudaSuccess ||
-      (e = s->d_counters.alloc(zs::kCounters * 8)) != cudaSuccess) {
+      (e = s->d_counters.alloc(zs::kCounters * 8)) != cudaSuccess ||
+      (e = s->d_st_sh.alloc(n * s->B * 8)) != cudaSuccess ||
+      (e = s->d_st_S1.alloc(n * s->B * 8)) != cudaSuccess ||
+      (e = s->d_st_S2.alloc(n * s->B * 8)) != cudaSuccess ||
+      (e = s->d_st_cnt.alloc(n * s->B * 4)) != cudaSuccess ||
+      (e = s->d_st_ring.alloc(n * s->B * (size_t)s->wmax * 8)) != cudaSuccess) {
     std::string m = std::string("device allocation: ") + cudaGetErrorString(e);
     delete s;
     return fail(nullptr, e == cudaErrorMemoryAllocation ? ZEUS_E_NOMEM : ZEUS_E_CUDA, m);
@@ -294,10 +300,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   }
   if (E.code == ZEUS_OK) {
     const zs::TabLayout L(B, S, K);
-    const size_t per_thread = (size_t)B * (5 * 8 + 4);
-    int wmax = 0;
-    for (const auto &c : s->cells) wmax = std::max(wmax, c.window);
-    const size_t need = (size_t)L.bytes + 32 * (per_thread + (size_t)wmax * B * 8);
+    const size_t per_thread = (size_t)((B + 1) & ~1) * 16;
+    const size_t need = (size_t)L.bytes + 32 * per_thread;
     if (need > 200 * 1024)
       E.add(ZEUS_E_UNSUPPORTED, "trace tables + per-trial arm state exceed shared memory (" +
                                     std::to_string(need) + " B for 32 trials)");
@@ -330,9 +334,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   // most warps resident given the shared-memory footprint per trial
   const zs::TabLayout L(B, S, K);
   s->tab_bytes = L.bytes;
-  int wmax = 0;
-  for (const auto &c : s->cells) wmax = std::max(wmax, c.window);
-  const size_t per_thread = (size_t)B * (5 * 8 + 4) + (size_t)wmax * B * 8;
+  const int wmax = s->wmax;
+  const size_t per_thread = (size_t)((B + 1) & ~1) * 16;   // (mu, sigma) per arm
   int best_warps = -1;
   for (int tpb : {128, 64, 32}) {
     const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
@@ -386,10 +389,13 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     a.B = s->B; a.S = s->S; a.K = s->K; a.R = s->R; a.max_epochs = s->max_epochs;
     a.charge_profiling = s->charge_profiling; a.b0 = s->b0; a.nslot = s->nslot;
     a.reg_stride = s->reg_stride; a.opt_stride = s->opt_stride; a.tab_bytes = s->tab_bytes;
-    int wmax = 0;
-    for (const auto &c : s->cells) wmax = std::max(wmax, c.window);
-    const bool windowed = wmax > 0;
-    a.ring_n = wmax;
+    const bool windowed = s->wmax > 0;
+    a.st_sh = s->d_st_sh.as<double>();
+    a.st_S1 = s->d_st_S1.as<double>();
+    a.st_S2 = s->d_st_S2.as<double>();
+    a.st_cnt = s->d_st_cnt.as<int32_t>();
+    a.st_ring = s->d_st_ring.as<double>();
+    a.st_stride = (size_t)s->shard_total;
     const dim3 grid((unsigned)((s->max_shard + s->tpb - 1) / s->tpb), (unsigned)nc);
     if (windowed && s->log_mode) zs::replay_kernel<true, true><<<grid, s->tpb, s->smem_bytes, st>>>(a);
     else if (windowed) zs::replay_kernel<true, false><<<grid, s->tpb, s->smem_bytes, st>>>(a);

@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libzeus_sim.so")
+# ZEUS_SIM_LIB selects an alternative build of the same ABI (kernel A/B experiments only)
+LIB_PATH = os.environ.get("ZEUS_SIM_LIB") or os.path.join(HERE, "libzeus_sim.so")
 
 ZEUS_OK = 0
 STATUS = {0: "ZEUS_OK", 1: "ZEUS_E_INVALID", 2: "ZEUS_E_STATE", 3: "ZEUS_E_NO_CONVERGENT_ARM",

@@ -1,0 +1,32 @@
+"""Builds kernel A/B variants of the same ABI into build/ (experiments; the product
+library is paper_2208_06102_b200/libzeus_sim.so)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2208_06102_b200 import build as B  # noqa: E402
+
+VARIANTS = {
+    "u1": ([], []),
+    "u1_imm": (["ZS_IMMEDIATE_CONSTANTS"], []),
+    "rk": (["ZS_ROUND_KEYS"], []),
+    "rk_r88": (["ZS_ROUND_KEYS", "ZS_MAXNREG=88"], []),
+    "u2": (["ZS_PAIR_UNROLL=2"], []),
+    "u1_r96": (["ZS_MAXNREG=96"], []),
+    "u2_r96": (["ZS_PAIR_UNROLL=2", "ZS_MAXNREG=96"], []),
+    "u1_r80": (["ZS_MAXNREG=80"], []),
+    "u1_r88": (["ZS_MAXNREG=88"], []),
+    "u1_r72": (["ZS_MAXNREG=72"], []),
+    "u2_r80": (["ZS_PAIR_UNROLL=2", "ZS_MAXNREG=80"], []),
+}
+
+if __name__ == "__main__":
+    os.makedirs("build", exist_ok=True)
+    names = sys.argv[1:] or list(VARIANTS)
+    for n in names:
+        d, x = VARIANTS[n]
+        out = B.build(force=True, out=f"build/libzs_{n}.so", defines=d, extra=x)
+        log = open(out + ".ptxas.log").read().split("Compiling entry function")
+        for part in log:
+            if "replay_kernelILb0ELb0E" in part.split("\n")[0]:
+                print(n, [l.strip() for l in part.splitlines() if "Used" in l or "spill" in l])

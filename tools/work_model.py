@@ -15,7 +15,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 NVCC = "/usr/local/cuda/bin/nvcc"
 FP64 = re.compile(r"^(DFMA|DADD|DMUL|DSETP|DMNMX|DSET|MUFU\.(RCP|RSQ)64H|F2F\.F64|I2F\.F64|F2I\.F64|I2F\.S64|DMMA)")
-SCAFFOLD = ("LDG", "STG", "LDC", "LDCU", "ULDC", "S2R", "S2UR", "EXIT", "RET", "BRA", "NOP", "CALL")
+SCAFFOLD = ("LDG", "STG", "LDC", "LDCU", "ULDC", "S2R", "S2UR", "EXIT", "RET", "BRA", "NOP", "CALL",
+            "UMOV", "MOV ")  # constant materialisation is hoisted out of the replay loop
 
 
 def sass(cubin, fn):

@@ -35,8 +35,9 @@ extern "C" __global__ void probe_observe(const double *in, double *out, const in
   const double d = C - sh;
   S1 = S1 + d; S2 = S2 + d * d;
   const double dn = (double)n;
-  const double mean = sh + S1 / dn;
-  double s2 = (S2 - (S1 * S1) / dn) / (dn - 1.0);
+  const double inv_n = 1.0 / dn;
+  const double mean = sh + S1 * inv_n;
+  double s2 = (S2 - S1 * (S1 * inv_n)) / (dn - 1.0);
   const double fl = 1e-12 * (1.0 + mean * mean);
   if (!(s2 >= fl)) s2 = fl;
   const double q = 1.0 / s2;

@@ -89,8 +89,12 @@ typedef struct {
   int64_t shard_begin, shard_end;    /* this rank's global trial range [begin, end) of
                                         every cell, clipped to [0, trials); end < 0 = all */
   int32_t log_mode;                  /* 0: no log; 1: per-decision log (4 B / decision) */
-  int32_t layout;                    /* 0: auto; 1: one thread per trial; 2: one lane group
-                                        per trial, lane = arm */
+  int32_t layout;                    /* schedule of the replay kernel; results
+                                        are bit-identical for every value:
+                                        0 auto (= 2 when R > 2|𝓑|, else 1);
+                                        1 one pass, one thread per trial;
+                                        2 two phases: the pruning stage, then the Thompson
+                                          stage with trials regrouped by survivor count */
 } zeus_run_opts;
 
 /* Outputs.  Every pointer is caller-owned and may be NULL (skipped); each

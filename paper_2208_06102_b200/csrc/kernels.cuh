@@ -137,10 +137,34 @@ struct ReplayArgs {
   unsigned long long *counters;   // [kCounters]
   int B, S, K, R, max_epochs, charge_profiling, b0, nslot, reg_stride, opt_stride;
   int tab_bytes;                  // bytes of the staged table region (multiple of 16)
-  // Observe statistics in global memory, [arm][stride] (+ ring [slot][arm][stride])
-  double *st_sh, *st_S1, *st_S2, *st_ring;
-  int32_t *st_cnt;
-  size_t st_stride;               // = total shard trials over all cells
+  // Observe statistics in global memory, one 32-byte record per (trial, arm):
+  // [trial][arm] -- a lane touches one sector per decision whichever trial it runs
+  struct ArmStat *st;
+  double *st_ring;                // [trial][arm][ring_n] when some cell has a window
+  int ring_n;
+  // two-phase schedule: phase A runs t < t_split (the pruning
+  // stage, <= 2B recurrences), phase B the Thompson-sampling rest with trials
+  // regrouped so the lanes of a warp draw the same number of normal pairs
+  int t_split;
+  struct Carry *carry;            // [stride] per-trial scalar state between phases
+  int32_t *perm;                  // [stride] phase-B lane -> trial (within each cell's block)
+  int32_t *bucket;                // [cells][kBuckets] histogram, then running offsets
+};
+
+constexpr int kBuckets = 17;      // popcount of the survivor-pair mask, 0..16
+
+struct __align__(16) ArmStat {    // Observe state of one arm of one trial (NC-6)
+  double sh, S1, S2;              // shift (first observation) and shifted sums
+  int32_t cnt, pad;               // observations ever
+};
+
+// per-trial scalar state carried from phase A to phase B (80 B)
+struct Carry {
+  double best, totC, totE, totT;
+  unsigned long long dig;
+  uint32_t profiled, seen, mature, ts_set;
+  int32_t nstop, last_b;
+  uint32_t n_sampled, n_prune, n_forced, n_recomp;
 };
 
 // shared-memory table region of one block: [ArmConst B][regret S*B][opt_arm S][pool S*B*K]
@@ -197,11 +221,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase) {
 
 enum : int { kStart = 0, kDown = 1, kUp = 2 };
 
+// Alg. 2 posterior from the shifted window sums (NC-6), n >= 2: returns (mu, sigma).
+__device__ __forceinline__ double2 posterior(double sh, double S1, double S2, int n, double prec0,
+                                             double pm0) {
+  const double dn = (double)n;
+  const double inv_n = 1.0 / dn;
+  const double mean = sh + S1 * inv_n;
+  double s2 = (S2 - S1 * (S1 * inv_n)) / (dn - 1.0);     // σ̃² = Var(C_b), n-1 divisor
+  const double fl = cst::kVarFloor * (1.0 + mean * mean);
+  if (!(s2 >= fl)) s2 = fl;                              // zero-variance floor (R-Q7)
+  const double q = 1.0 / s2;
+  const double var = 1.0 / (prec0 + dn * q);            // σ̂² = (1/σ̂0² + |C_b|/σ̃²)^-1
+  const double sum = dn * sh + S1;                       // Sum(C_b)
+  return make_double2(var * (pm0 + sum * q), sqrt(var)); // μ̂ = σ̂²(μ̂0/σ̂0² + Sum/σ̃²)
+}
+
 __device__ __forceinline__ uint32_t below_mask(int c) { return c <= 0 ? 0u : ((1u << c) - 1u); }
 __device__ __forceinline__ uint32_t above_mask(int c) { return c >= 31 ? 0u : ~((2u << c) - 1u); }
 
 // One thread per trial.  WINDOWED: some cell has N > 0 (ring buffer per arm).
-// LOG: write the per-decision log.
+// LOG: write the per-decision log.  PHASE: 0 = all recurrences in one pass,
+// 1 = phase A (t < t_split, then save the carry), 2 = phase B (t >= t_split,
+// lanes mapped through perm; every trial is already in Thompson sampling).
 //
 // State placement:
 //   registers  per-trial scalars: best, the Alg. 3 state machine, bitmasks
@@ -216,7 +257,7 @@ __device__ __forceinline__ uint32_t above_mask(int c) { return c >= 31 ? 0u : ~(
 #else
 #define ZS_REPLAY_BOUNDS __launch_bounds__(128)
 #endif
-template <bool WINDOWED, bool LOG>
+template <bool WINDOWED, bool LOG, int PHASE>
 __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
@@ -253,11 +294,12 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const int B = a.B, R = a.R, S = a.S, K = a.K;
   double2 *s_ms = reinterpret_cast<double2 *>(smem + a.tab_bytes);   // [arm][thread] (mu, sigma)
 
-  const int64_t jj = j0 + tid;
-  const bool active = jj < cp.n;
+  const bool active = j0 + tid < cp.n;
+  int64_t jj = j0 + tid;                                    // this lane's trial within the cell
+  if (PHASE == 2) jj = active ? a.perm[cp.out_off + j0 + tid] : 0;
   const int64_t trial = cp.begin + jj;
-  const size_t o = (size_t)(cp.out_off + jj);              // this trial's column in the state
-  const size_t stride = a.st_stride;
+  const size_t o = (size_t)(cp.out_off + jj);              // this trial's row in the outputs/state
+  ArmStat *st = a.st + o * B;
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
   double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
@@ -270,7 +312,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
 
   uint32_t profiled = 0, seen = 0, mature = 0;              // bit a: profiled / observed / n_a >= 2
   double best = kInf;                                       // min_t C_t
-  bool in_ts = false;
+  bool in_ts = PHASE == 2;
   int round = 1, step = kStart, start = a.b0, cursor = a.b0;
   uint32_t cand = (B == 32) ? 0xffffffffu : ((1u << B) - 1u), surv = 0, ts_set = 0, ts_pairs = 0;
   double r1_cost = kInf;
@@ -281,9 +323,26 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   // event counters (u32 per trial; the pair/normal counts follow from n_sampled
   // because the survivor set is fixed during Thompson sampling)
   uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
+  if (PHASE == 2 && active) {                               // resume from phase A
+    const Carry c = a.carry[o];
+    best = c.best; totC = c.totC; totE = c.totE; totT = c.totT; dig = c.dig;
+    profiled = c.profiled; seen = c.seen; mature = c.mature; ts_set = c.ts_set;
+    nstop = c.nstop; last_b = c.last_b;
+    n_sampled = c.n_sampled; n_prune = c.n_prune; n_forced = c.n_forced; n_recomp = c.n_recomp;
+    for (int k = 0; 2 * k < B; ++k)
+      if ((ts_set >> (2 * k)) & 3u) ts_pairs |= 1u << k;
+    for (int b = 0; b < B; ++b) {                           // posterior of every arm with n >= 2,
+      if (!((mature >> b) & 1u)) continue;                  // recomputed from its window sums
+      const ArmStat q = st[b];                              // (same formula, same bits)
+      const int n = (WINDOWED && cp.window > 0) ? min(q.cnt, cp.window) : q.cnt;
+      s_ms[b * TPB + tid] = posterior(q.sh, q.S1, q.S2, n, cp.prec0, cp.pm0);
+    }
+  }
 
+  const int t_begin = PHASE == 2 ? a.t_split : 0;
+  const int t_end = PHASE == 1 ? a.t_split : R;
   int s = 0;                                                // slice of t = floor(t*S/R) (R-Q19)
-  for (int t = 0; t < R; ++t) {
+  for (int t = t_begin; t < t_end; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0;
     while ((long long)(s + 1) * R <= (long long)t * S) ++s;   // no 64-bit division per decision
@@ -291,7 +350,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       // ---------------- step 2: decide b_t
       const bool ts_dec = in_ts;
       int b;
-      if (!in_ts) {
+      if (PHASE != 2 && !in_ts) {
         b = (step == kStart) ? start
           : (step == kDown) ? 31 - __clz(cand & below_mask(cursor))
                             : __ffs(cand & above_mask(cursor)) - 1;
@@ -321,19 +380,20 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             b = take1 ? 2 * k + 1 : b;
           };
 #if ZS_PAIR_UNROLL == 2
-          while (pm) {                                      // two independent pairs in flight
-            const int k0 = __ffs(pm) - 1;
-            pm &= pm - 1u;
-            const bool has1 = pm != 0u;
-            const int k1 = has1 ? __ffs(pm) - 1 : k0;
-            if (has1) pm &= pm - 1u;
-            double z00, z01, z10, z11;
-            normal_pair(ZS_KEYARG, trial, t, k0, z00, z01);
-            normal_pair(ZS_KEYARG, trial, t, k1, z10, z11);
-            consider(k0, z00, z01);
-            if (has1) consider(k1, z10, z11);
+          if (PHASE == 2) {                                 // pair counts are warp-uniform here
+            while (pm & (pm - 1u)) {                        // two independent pairs in flight
+              const int k0 = __ffs(pm) - 1;
+              pm &= pm - 1u;
+              const int k1 = __ffs(pm) - 1;
+              pm &= pm - 1u;
+              double z00, z01, z10, z11;
+              normal_pair(ZS_KEYARG, trial, t, k0, z00, z01);
+              normal_pair(ZS_KEYARG, trial, t, k1, z10, z11);
+              consider(k0, z00, z01);
+              consider(k1, z10, z11);
+            }
           }
-#else
+#endif
           while (pm) {
             const int k = __ffs(pm) - 1;
             pm &= pm - 1u;
@@ -341,15 +401,12 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             normal_pair(ZS_KEYARG, trial, t, k, z0, z1);
             consider(k, z0, z1);
           }
-#endif
           n_sampled += 1;
         }
       }
       // Observe statistics of arm b: issue the loads now, consume after the charge
-      const size_t so = (size_t)b * stride + o;
       const bool was_seen = (seen >> b) & 1u;
-      const int cnt_g = a.st_cnt[so];
-      const double sh_g = a.st_sh[so], S1_g = a.st_S1[so], S2_g = a.st_S2[so];
+      const ArmStat q = st[b];
       const ArmConst ac = arm[b];
       // ---------------- step 3: replay one recorded run
       const uint32_t r = replica(cp.key0, cp.key1, trial, t, (uint32_t)K);
@@ -385,14 +442,14 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       if (conv && !(C >= best)) best = C;
       // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
       {
-        const int cnt = was_seen ? cnt_g : 0;
+        const int cnt = was_seen ? q.cnt : 0;
         double sh, S1, S2;
-        if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; a.st_sh[so] = sh; }
-        else { sh = sh_g; S1 = S1_g; S2 = S2_g; }
+        if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
+        else { sh = q.sh; S1 = q.S1; S2 = q.S2; }
         int n = cnt;
         if (WINDOWED && cp.window > 0) {
           const int N = cp.window;
-          double *slot = &a.st_ring[((size_t)(cnt % N) * B + b) * stride + o];
+          double *slot = &a.st_ring[(o * B + b) * (size_t)a.ring_n + (cnt % N)];
           if (cnt >= N) {
             const double dy = *slot - sh;
             S1 = S1 - dy;
@@ -405,27 +462,18 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
         S1 = S1 + d;
         S2 = S2 + d * d;
         n += 1;
-        a.st_S1[so] = S1;
-        a.st_S2[so] = S2;
-        a.st_cnt[so] = cnt + 1;
+        ArmStat nq;
+        nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
+        st[b] = nq;
         seen |= 1u << b;
         if (n >= 2) {
-          const double dn = (double)n;
-          const double inv_n = 1.0 / dn;
-          const double mean = sh + S1 * inv_n;
-          double s2 = (S2 - S1 * (S1 * inv_n)) / (dn - 1.0);
-          const double fl = cst::kVarFloor * (1.0 + mean * mean);
-          if (!(s2 >= fl)) s2 = fl;
-          const double q = 1.0 / s2;
-          const double var = 1.0 / (cp.prec0 + dn * q);
-          const double sum = dn * sh + S1;
-          s_ms[b * TPB + tid] = make_double2(var * (cp.pm0 + sum * q), sqrt(var));
+          s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
           mature |= 1u << b;
           n_recomp += 1;
         }
       }
       // ---------------- Alg. 3 bookkeeping
-      if (!in_ts) {
+      if (PHASE != 2 && !in_ts) {
         if (conv) {
           surv |= 1u << b;
           if (round == 1 && (C < r1_cost || (C == r1_cost && b < r1_arm))) { r1_cost = C; r1_arm = b; }
@@ -489,6 +537,18 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       if ((vPacked >> 16) & 0xff) atomicAdd(row + 6, (double)((vPacked >> 16) & 0xff));
     }
   }
+  if (PHASE == 1) {                                         // hand over to phase B
+    if (active) {
+      Carry c;
+      c.best = best; c.totC = totC; c.totE = totE; c.totT = totT; c.dig = dig;
+      c.profiled = profiled; c.seen = seen; c.mature = mature; c.ts_set = ts_set;
+      c.nstop = nstop; c.last_b = last_b;
+      c.n_sampled = n_sampled; c.n_prune = n_prune; c.n_forced = n_forced; c.n_recomp = n_recomp;
+      a.carry[o] = c;
+      atomicAdd(&a.bucket[cell * kBuckets + __popc(ts_pairs)], 1);
+    }
+    return;
+  }
   if (active) {
     a.tot_cost[o] = totC;
     a.tot_energy[o] = totE;
@@ -507,6 +567,34 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     if ((tid & 31) == 0 && v) atomicAdd(a.counters + q, v);
+  }
+}
+
+// bucket offsets: exclusive scan of the per-cell histogram (one thread per cell)
+__global__ void bucket_scan_kernel(int32_t *bucket, int ncells) {
+  const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cell >= ncells) return;
+  int run = 0;
+  for (int k = 0; k < kBuckets; ++k) {
+    const int c = bucket[cell * kBuckets + k];
+    bucket[cell * kBuckets + k] = run;
+    run += c;
+  }
+}
+
+// phase-B lane order: trials of a cell grouped by their survivor-pair count
+__global__ void bucket_scatter_kernel(const CellParam *cells, const Carry *carry, int32_t *bucket,
+                                      int32_t *perm, int ncells, int B) {
+  const int cell = blockIdx.y;
+  const CellParam cp = cells[cell];
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cp.n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t ts_set = carry[cp.out_off + j].ts_set;
+    uint32_t pairs = 0;
+    for (int k = 0; 2 * k < B; ++k)
+      if ((ts_set >> (2 * k)) & 3u) pairs |= 1u << k;
+    const int pos = atomicAdd(&bucket[cell * kBuckets + __popc(pairs)], 1);
+    perm[cp.out_off + pos] = (int32_t)j;
   }
 }
 

@@ -59,7 +59,7 @@ struct zeus_sim {
   // device memory
   DevBuf d_A, d_Th, d_pool, d_cells, d_arms, d_regret, d_opt, d_optarm;
   DevBuf d_slots, d_curves, d_tot_cost, d_tot_energy, d_tot_time, d_digest, d_nstop, d_final,
-      d_log, d_counters, d_st_sh, d_st_S1, d_st_S2, d_st_cnt, d_st_ring;
+      d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket;
   ~zeus_sim() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -143,6 +143,17 @@ void check_cells(const zeus_cell *cells, int n, Errors &E) {
   }
 }
 
+// replay_kernel<WINDOWED, LOG, PHASE> by runtime flags
+typedef void (*ReplayFn)(zs::ReplayArgs);
+ReplayFn replay_fn(bool windowed, bool log, int phase) {
+  static const ReplayFn tab[2][2][3] = {
+      {{zs::replay_kernel<false, false, 0>, zs::replay_kernel<false, false, 1>, zs::replay_kernel<false, false, 2>},
+       {zs::replay_kernel<false, true, 0>, zs::replay_kernel<false, true, 1>, zs::replay_kernel<false, true, 2>}},
+      {{zs::replay_kernel<true, false, 0>, zs::replay_kernel<true, false, 1>, zs::replay_kernel<true, false, 2>},
+       {zs::replay_kernel<true, true, 0>, zs::replay_kernel<true, true, 1>, zs::replay_kernel<true, true, 2>}}};
+  return tab[windowed][log][phase];
+}
+
 void launch_step1(zeus_sim *s, cudaStream_t st) {
   zs::Step1Args a{};
   a.A = s->d_A.as<double>();
@@ -182,7 +193,6 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     if (opts->shard_end >= 0 && opts->shard_end < opts->shard_begin) E.add(ZEUS_E_INVALID, "shard_end < shard_begin");
     if (opts->log_mode != 0 && opts->log_mode != 1) E.add(ZEUS_E_INVALID, "log_mode must be 0 or 1");
     if (opts->layout < 0 || opts->layout > 2) E.add(ZEUS_E_INVALID, "layout must be 0, 1 or 2");
-    if (opts->layout == 2) E.add(ZEUS_E_UNSUPPORTED, "layout 2 (lane group per trial) is not built yet");
   }
   if (E.code != ZEUS_OK) return fail(nullptr, E.code, E.s);
 
@@ -248,11 +258,11 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
       (e = s->d_final.alloc(n * 4)) != cudaSuccess ||
       (e = s->d_log.alloc(s->log_mode ? n * (size_t)s->R * 4 : 0)) != cudaSuccess ||
       (e = s->d_counters.alloc(zs::kCounters * 8)) != cudaSuccess ||
-      (e = s->d_st_sh.alloc(n * s->B * 8)) != cudaSuccess ||
-      (e = s->d_st_S1.alloc(n * s->B * 8)) != cudaSuccess ||
-      (e = s->d_st_S2.alloc(n * s->B * 8)) != cudaSuccess ||
-      (e = s->d_st_cnt.alloc(n * s->B * 4)) != cudaSuccess ||
-      (e = s->d_st_ring.alloc(n * s->B * (size_t)s->wmax * 8)) != cudaSuccess) {
+      (e = s->d_st.alloc(n * s->B * sizeof(zs::ArmStat))) != cudaSuccess ||
+      (e = s->d_st_ring.alloc(n * s->B * (size_t)s->wmax * 8)) != cudaSuccess ||
+      (e = s->d_carry.alloc(n * sizeof(zs::Carry))) != cudaSuccess ||
+      (e = s->d_perm.alloc(n * 4)) != cudaSuccess ||
+      (e = s->d_bucket.alloc((size_t)num_cells * zs::kBuckets * 4)) != cudaSuccess) {
     std::string m = std::string("device allocation: ") + cudaGetErrorString(e);
     delete s;
     return fail(nullptr, e == cudaErrorMemoryAllocation ? ZEUS_E_NOMEM : ZEUS_E_CUDA, m);
@@ -341,17 +351,18 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
     const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
     if (bytes > 227 * 1024) continue;
     int blocks = 0;
-    const void *fn = wmax > 0 ? (const void *)zs::replay_kernel<true, false>
-                              : (const void *)zs::replay_kernel<false, false>;
+    const void *fn = (const void *)replay_fn(wmax > 0, false, 0);
     ZS_CUDA(s, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     ZS_CUDA(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, tpb, bytes));
     const int warps = blocks * tpb / 32;
     if (warps > best_warps) { best_warps = warps; s->tpb = tpb; s->smem_bytes = (int)bytes; }
   }
   if (best_warps <= 0) return fail(s, ZEUS_E_UNSUPPORTED, "no launch shape fits shared memory");
-  for (const void *fn : {(const void *)zs::replay_kernel<false, false>, (const void *)zs::replay_kernel<false, true>,
-                         (const void *)zs::replay_kernel<true, false>, (const void *)zs::replay_kernel<true, true>})
-    ZS_CUDA(s, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, s->smem_bytes));
+  for (int w = 0; w < 2; ++w)
+    for (int l = 0; l < 2; ++l)
+      for (int ph = 0; ph < 3; ++ph)
+        ZS_CUDA(s, cudaFuncSetAttribute((const void *)replay_fn(w, l, ph),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, s->smem_bytes));
   s->loaded = true;
   return ZEUS_OK;
 }
@@ -390,18 +401,35 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     a.charge_profiling = s->charge_profiling; a.b0 = s->b0; a.nslot = s->nslot;
     a.reg_stride = s->reg_stride; a.opt_stride = s->opt_stride; a.tab_bytes = s->tab_bytes;
     const bool windowed = s->wmax > 0;
-    a.st_sh = s->d_st_sh.as<double>();
-    a.st_S1 = s->d_st_S1.as<double>();
-    a.st_S2 = s->d_st_S2.as<double>();
-    a.st_cnt = s->d_st_cnt.as<int32_t>();
+    a.st = s->d_st.as<zs::ArmStat>();
     a.st_ring = s->d_st_ring.as<double>();
-    a.st_stride = (size_t)s->shard_total;
+    a.ring_n = s->wmax;
     const dim3 grid((unsigned)((s->max_shard + s->tpb - 1) / s->tpb), (unsigned)nc);
-    if (windowed && s->log_mode) zs::replay_kernel<true, true><<<grid, s->tpb, s->smem_bytes, st>>>(a);
-    else if (windowed) zs::replay_kernel<true, false><<<grid, s->tpb, s->smem_bytes, st>>>(a);
-    else if (s->log_mode) zs::replay_kernel<false, true><<<grid, s->tpb, s->smem_bytes, st>>>(a);
-    else zs::replay_kernel<false, false><<<grid, s->tpb, s->smem_bytes, st>>>(a);
-    ZS_CUDA(s, cudaGetLastError());
+    // two-phase schedule when Thompson sampling follows the pruning stage (R > 2B):
+    // phase A = the first 2B recurrences (Alg. 3 pruning is at most 2B runs), then the
+    // trials of each cell are regrouped by survivor-pair count so a warp's lanes
+    // draw the same number of normals per decision in phase B
+    a.t_split = std::min(s->R, 2 * s->B);
+    a.carry = s->d_carry.as<zs::Carry>();
+    a.perm = s->d_perm.as<int32_t>();
+    a.bucket = s->d_bucket.as<int32_t>();
+    const bool two_phase = s->layout != 1 && a.t_split < s->R;
+    if (!two_phase) {
+      replay_fn(windowed, s->log_mode, 0)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+      ZS_CUDA(s, cudaGetLastError());
+    } else {
+      ZS_CUDA(s, cudaMemsetAsync(s->d_bucket.p, 0, s->d_bucket.bytes, st));
+      replay_fn(windowed, s->log_mode, 1)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+      ZS_CUDA(s, cudaGetLastError());
+      zs::bucket_scan_kernel<<<(nc + 127) / 128, 128, 0, st>>>(a.bucket, nc);
+      ZS_CUDA(s, cudaGetLastError());
+      const unsigned sx = (unsigned)std::min<int64_t>((s->max_shard + 255) / 256, 1184);
+      zs::bucket_scatter_kernel<<<dim3(std::max(1u, sx), (unsigned)nc), 256, 0, st>>>(
+          a.cells, a.carry, a.bucket, a.perm, nc, s->B);
+      ZS_CUDA(s, cudaGetLastError());
+      replay_fn(windowed, s->log_mode, 2)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+      ZS_CUDA(s, cudaGetLastError());
+    }
   }
   ZS_CUDA(s, cudaEventRecord(s->ev1, st));
   zs::curve_reduce_kernel<<<std::max(1, std::min(1184, (int)((nc * (size_t)s->R * zs::kQ + 255) / 256))), 256, 0, st>>>(

@@ -33,8 +33,8 @@ def oracle_threads(oracle):
     return max(1, min(64, oracle.hardware_threads()))
 
 
-def run_gpu(zs, w, cells, trials, R, shard=(0, -1), log=False, want=None):
-    sim = zs.Simulation(w, cells, trials, R, shard=shard, log=log).load_profile().run()
+def run_gpu(zs, w, cells, trials, R, shard=(0, -1), log=False, want=None, layout=0):
+    sim = zs.Simulation(w, cells, trials, R, shard=shard, log=log, layout=layout).load_profile().run()
     keys = ["curves", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm",
             "counters", "pstar_index", "c1", "t1", "e1", "c_prof", "t_prof", "e_prof", "opt_cost",
             "opt_arm"] + (["log"] if log else [])
@@ -247,3 +247,17 @@ def test_errors_are_reported(zs):
     sim2 = zs.Simulation(w2, job.cells, 10, 5)
     with pytest.raises(zs.ZeusError, match="NO_CONVERGENT_ARM"):
         sim2.load_profile()
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg4_38"])
+def test_schedules_bit_identical(zs, oracle, name):
+    """layout 1 (one pass) and layout 2 (pruning phase, regroup, Thompson phase) give the
+    same bits for every trial and decision."""
+    (job,) = synth.config(name, trials=2000)
+    outs = [run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True, layout=l)
+            for l in (1, 2)]
+    for k in ("log", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm", "counters"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k
+    np.testing.assert_allclose(outs[0]["curves"], outs[1]["curves"], rtol=1e-12)
+    compare_cell(oracle, outs[1], job.workload, job.cells[0], 0, np.arange(job.trials),
+                 job.recurrences, job.trials, logs=True)

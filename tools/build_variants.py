@@ -28,5 +28,8 @@ if __name__ == "__main__":
         out = B.build(force=True, out=f"build/libzs_{n}.so", defines=d, extra=x)
         log = open(out + ".ptxas.log").read().split("Compiling entry function")
         for part in log:
-            if "replay_kernelILb0ELb0E" in part.split("\n")[0]:
-                print(n, [l.strip() for l in part.splitlines() if "Used" in l or "spill" in l])
+            head = part.split("\n")[0]
+            if "replay_kernelILb0ELb0E" in head:
+                ph = head.split("ELi")[1][0] if "ELi" in head else "?"
+                print(n, "phase", ph, [l.strip()[-70:] for l in part.splitlines()
+                                       if "Used" in l or "spill" in l])

@@ -221,14 +221,17 @@ bool observe(Arm &a, double x, int32_t window, const Prior &pr, double *s2_out, 
   if (n < 2) return false;
   double dn = (double)n;
   double inv_n = 1.0 / dn;
+  double inv_nm1 = 1.0 / (dn - 1.0);
   double mean = a.sh + a.S1 * inv_n;
-  double s2 = (a.S2 - a.S1 * (a.S1 * inv_n)) / (dn - 1.0);  // σ̃² = Var(C_b), n-1 divisor
+  double s2 = (a.S2 - a.S1 * (a.S1 * inv_n)) * inv_nm1;     // σ̃² = Var(C_b), n-1 divisor
   double fl = 1e-12 * (1.0 + mean * mean);
   if (!(s2 >= fl)) s2 = fl;                                 // zero-variance floor (R-Q7)
-  double q = 1.0 / s2;
-  double var = 1.0 / (pr.prec0 + dn * q);                   // σ̂² = (1/σ̂0² + |C_b|/σ̃²)^-1
-  double sum = dn * a.sh + a.S1;                             // Sum(C_b)
-  a.mu = var * (pr.pm0 + sum * q);                          // μ̂ = σ̂²(μ̂0/σ̂0² + Sum/σ̃²)
+  // Alg. 2: σ̂² = (1/σ̂0² + |C_b|/σ̃²)^-1 and μ̂ = σ̂²(μ̂0/σ̂0² + Sum(C_b)/σ̃²), written
+  // with both numerator and denominator multiplied by σ̃² (NC-6)
+  double den = (pr.prec0 * s2) + dn;
+  double sum = (dn * a.sh) + a.S1;                           // Sum(C_b)
+  double var = s2 / den;
+  a.mu = ((pr.pm0 * s2) + sum) / den;
   a.sigma = std::sqrt(var);
   if (s2_out) *s2_out = s2;
   if (var_out) *var_out = var;

@@ -148,6 +148,23 @@ __device__ __forceinline__ U4 philox4x32_10(U4 c, const RoundKeys &rk) {
   return c;
 }
 
+// The 128 random bits of arm pair k of `trial` at recurrence t, and the
+// Box-Muller transform of them (NC-3); normal_pair = both.
+__device__ __forceinline__ U4 pair_words(uint32_t key0, uint32_t key1, int64_t trial, int t, int k) {
+  return philox4x32_10(U4{(uint32_t)t, 0x01000000u | (uint32_t)k, (uint32_t)trial,
+                          (uint32_t)((uint64_t)trial >> 32)}, key0, key1);
+}
+__device__ __forceinline__ void box_muller(const U4 x, double &z0, double &z1) {
+  const uint64_t w0 = ((uint64_t)x.y << 32) | x.x;
+  const uint64_t w1 = ((uint64_t)x.w << 32) | x.z;
+  const double u1 = 2.0 - __longlong_as_double((long long)(0x3FF0000000000000ull | (w0 >> 12)));
+  const double r = sqrt(-2.0 * zlog(u1));
+  double s, c;
+  zsincospi(w1 >> 12, s, c);
+  z0 = r * c;
+  z1 = r * s;
+}
+
 // Box-Muller pair for arms (2k, 2k+1) of `trial` at recurrence t (NC-3).
 #ifdef ZS_ROUND_KEYS
 __device__ __forceinline__ void normal_pair(const RoundKeys &key, int64_t trial, int t, int k,

@@ -18,6 +18,12 @@
 #ifndef ZS_PAIR_UNROLL
 #define ZS_PAIR_UNROLL 1
 #endif
+#ifndef ZS_PIPELINE
+#define ZS_PIPELINE 0
+#endif
+#ifndef ZS_HOIST_REPLICA
+#define ZS_HOIST_REPLICA 0
+#endif
 
 namespace zs {
 
@@ -225,15 +231,18 @@ enum : int { kStart = 0, kDown = 1, kUp = 2 };
 __device__ __forceinline__ double2 posterior(double sh, double S1, double S2, int n, double prec0,
                                              double pm0) {
   const double dn = (double)n;
-  const double inv_n = 1.0 / dn;
+  const double inv_n = 1.0 / dn;                         // the two reciprocals are
+  const double inv_nm1 = 1.0 / (dn - 1.0);               // independent: latency of one
   const double mean = sh + S1 * inv_n;
-  double s2 = (S2 - S1 * (S1 * inv_n)) / (dn - 1.0);     // σ̃² = Var(C_b), n-1 divisor
+  double s2 = (S2 - S1 * (S1 * inv_n)) * inv_nm1;        // σ̃² = Var(C_b), n-1 divisor
   const double fl = cst::kVarFloor * (1.0 + mean * mean);
   if (!(s2 >= fl)) s2 = fl;                              // zero-variance floor (R-Q7)
-  const double q = 1.0 / s2;
-  const double var = 1.0 / (prec0 + dn * q);            // σ̂² = (1/σ̂0² + |C_b|/σ̃²)^-1
-  const double sum = dn * sh + S1;                       // Sum(C_b)
-  return make_double2(var * (pm0 + sum * q), sqrt(var)); // μ̂ = σ̂²(μ̂0/σ̂0² + Sum/σ̃²)
+  // σ̂² = (1/σ̂0² + n/σ̃²)^-1 = σ̃²/(σ̃²/σ̂0² + n);  μ̂ = σ̂²(μ̂0/σ̂0² + Sum/σ̃²)
+  // = (σ̃² μ̂0/σ̂0² + Sum)/(σ̃²/σ̂0² + n): two independent divisions by one denominator
+  const double den = (prec0 * s2) + dn;
+  const double sum = (dn * sh) + S1;                     // Sum(C_b)
+  const double var = s2 / den;
+  return make_double2(((pm0 * s2) + sum) / den, sqrt(var));
 }
 
 __device__ __forceinline__ uint32_t below_mask(int c) { return c <= 0 ? 0u : ((1u << c) - 1u); }
@@ -345,11 +354,21 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   for (int t = t_begin; t < t_end; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0;
-    while ((long long)(s + 1) * R <= (long long)t * S) ++s;   // no 64-bit division per decision
+    // carried from the decision to the Observe, which runs after the curve reduction so
+    // the latency of the arm-state load hides behind the shuffles
+    int b = 0;
+    bool was_seen = false;
+    ArmStat q;
+    double C = 0.0;
+    if (S > 1)                                              // no 64-bit division per decision
+      while ((long long)(s + 1) * R <= (long long)t * S) ++s;
     if (active) {
+#if ZS_HOIST_REPLICA
+      // step 3's replica draw depends only on (trial, t): issue it ahead of the sampling
+      const uint32_t r = replica(cp.key0, cp.key1, trial, t, (uint32_t)K);
+#endif
       // ---------------- step 2: decide b_t
       const bool ts_dec = in_ts;
-      int b;
       if (PHASE != 2 && !in_ts) {
         b = (step == kStart) ? start
           : (step == kDown) ? 31 - __clz(cand & below_mask(cursor))
@@ -394,6 +413,28 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             }
           }
 #endif
+#if ZS_PIPELINE
+          {   // software pipeline: the Philox of the next pair (integer pipes) overlaps the
+              // Box-Muller transcendentals of this one (FP64 pipe)
+            int k = __ffs(pm) - 1;
+            pm &= pm - 1u;
+            U4 xn = pair_words(cp.key0, cp.key1, trial, t, k);
+            for (;;) {
+              const int kc = k;
+              const U4 xc = xn;
+              const bool more = pm != 0u;
+              if (more) {
+                k = __ffs(pm) - 1;
+                pm &= pm - 1u;
+                xn = pair_words(cp.key0, cp.key1, trial, t, k);
+              }
+              double z0, z1;
+              box_muller(xc, z0, z1);
+              consider(kc, z0, z1);
+              if (!more) break;
+            }
+          }
+#else
           while (pm) {
             const int k = __ffs(pm) - 1;
             pm &= pm - 1u;
@@ -401,15 +442,18 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             normal_pair(ZS_KEYARG, trial, t, k, z0, z1);
             consider(k, z0, z1);
           }
+#endif
           n_sampled += 1;
         }
       }
-      // Observe statistics of arm b: issue the loads now, consume after the charge
-      const bool was_seen = (seen >> b) & 1u;
-      const ArmStat q = st[b];
+      // Observe statistics of arm b: issue the load now, consume after the curves
+      was_seen = (seen >> b) & 1u;
+      q = st[b];
       const ArmConst ac = arm[b];
       // ---------------- step 3: replay one recorded run
+#if !ZS_HOIST_REPLICA
       const uint32_t r = replica(cp.key0, cp.key1, trial, t, (uint32_t)K);
+#endif
       const int E = pool[((size_t)s * B + b) * K + r];
       const int Erun = E > 0 ? E : a.max_epochs;
       double c0, t0, e0;
@@ -420,7 +464,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       const double Cf = c0 + em1 * ac.c1;
       // ---------------- step 4: early stop at β·min_t C_t, truncated charge
       const double thr = cp.beta * best;
-      double C, Tm, En;
+      double Tm, En;
       const bool stopped = Cf > thr;
       if (stopped) {
         C = thr;
@@ -440,38 +484,6 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       }
       const bool conv = (E > 0) && !stopped;
       if (conv && !(C >= best)) best = C;
-      // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
-      {
-        const int cnt = was_seen ? q.cnt : 0;
-        double sh, S1, S2;
-        if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
-        else { sh = q.sh; S1 = q.S1; S2 = q.S2; }
-        int n = cnt;
-        if (WINDOWED && cp.window > 0) {
-          const int N = cp.window;
-          double *slot = &a.st_ring[(o * B + b) * (size_t)a.ring_n + (cnt % N)];
-          if (cnt >= N) {
-            const double dy = *slot - sh;
-            S1 = S1 - dy;
-            S2 = S2 - dy * dy;
-            n = N - 1;
-          }
-          *slot = C;
-        }
-        const double d = C - sh;
-        S1 = S1 + d;
-        S2 = S2 + d * d;
-        n += 1;
-        ArmStat nq;
-        nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
-        st[b] = nq;
-        seen |= 1u << b;
-        if (n >= 2) {
-          s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
-          mature |= 1u << b;
-          n_recomp += 1;
-        }
-      }
       // ---------------- Alg. 3 bookkeeping
       if (PHASE != 2 && !in_ts) {
         if (conv) {
@@ -520,21 +532,61 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       vReg = regret[s * B + b];
       vPacked = (stopped ? 1 : 0) | ((b == optarm[s]) ? (1 << 8) : 0) | (ts_dec ? (1 << 16) : 0);
     }
-    // ---------------- warp partial of the curves, one atomic per quantity per warp
-    vC = warp_sum(vC);
-    vE = warp_sum(vE);
-    vT = warp_sum(vT);
-    vReg = warp_sum(vReg);
-    vPacked = warp_sum(vPacked);
-    if ((tid & 31) == 0) {
+    // ---------------- warp partial of the curves: a reduce-scatter leaves the warp total of
+    // quantity (lane >> 3) in lanes 0, 8, 16, 24 (12 shuffles instead of 40); then one
+    // 4-lane atomic for the fp64 sums and one 3-lane atomic for the counts
+    {
+      const int lane = tid & 31;
+      const bool h = lane & 16, g = lane & 8;
+      double k0 = h ? vT : vC, k1 = h ? vReg : vE;
+      k0 += __shfl_xor_sync(0xffffffffu, h ? vC : vT, 16);
+      k1 += __shfl_xor_sync(0xffffffffu, h ? vE : vReg, 16);
+      double kq = g ? k1 : k0;
+      kq += __shfl_xor_sync(0xffffffffu, g ? k0 : k1, 8);
+      kq += __shfl_xor_sync(0xffffffffu, kq, 4);
+      kq += __shfl_xor_sync(0xffffffffu, kq, 2);
+      kq += __shfl_xor_sync(0xffffffffu, kq, 1);
+      vPacked = warp_sum(vPacked);
       double *row = curves + (size_t)t * kQ;
-      atomicAdd(row + 0, vC);
-      atomicAdd(row + 1, vE);
-      atomicAdd(row + 2, vT);
-      atomicAdd(row + 3, vReg);
-      if (vPacked & 0xff) atomicAdd(row + 4, (double)(vPacked & 0xff));
-      if ((vPacked >> 8) & 0xff) atomicAdd(row + 5, (double)((vPacked >> 8) & 0xff));
-      if ((vPacked >> 16) & 0xff) atomicAdd(row + 6, (double)((vPacked >> 16) & 0xff));
+      if ((lane & 7) == 0) {
+        atomicAdd(row + (lane >> 3), kq);
+        const int cntq = (vPacked >> (lane & 24)) & 0xff;   // lane 0: stops, 8: optimal, 16: TS
+        if (lane < 24 && cntq) atomicAdd(row + 4 + (lane >> 3), (double)cntq);
+      }
+    }
+    if (active) {
+      // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
+      {
+        const int cnt = was_seen ? q.cnt : 0;
+        double sh, S1, S2;
+        if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
+        else { sh = q.sh; S1 = q.S1; S2 = q.S2; }
+        int n = cnt;
+        if (WINDOWED && cp.window > 0) {
+          const int N = cp.window;
+          double *slot = &a.st_ring[(o * B + b) * (size_t)a.ring_n + (cnt % N)];
+          if (cnt >= N) {
+            const double dy = *slot - sh;
+            S1 = S1 - dy;
+            S2 = S2 - dy * dy;
+            n = N - 1;
+          }
+          *slot = C;
+        }
+        const double d = C - sh;
+        S1 = S1 + d;
+        S2 = S2 + d * d;
+        n += 1;
+        ArmStat nq;
+        nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
+        st[b] = nq;
+        seen |= 1u << b;
+        if (n >= 2) {
+          s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
+          mature |= 1u << b;
+          n_recomp += 1;
+        }
+      }
     }
   }
   if (PHASE == 1) {                                         // hand over to phase B

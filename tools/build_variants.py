@@ -8,6 +8,10 @@ from paper_2208_06102_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "u1": ([], []),
+    "pipe": (["ZS_PIPELINE=1"], []),
+    "hoist": (["ZS_HOIST_REPLICA=1"], []),
+    "pipe_hoist": (["ZS_PIPELINE=1", "ZS_HOIST_REPLICA=1"], []),
+    "pipe_hoist_r80": (["ZS_PIPELINE=1", "ZS_HOIST_REPLICA=1", "ZS_MAXNREG=80"], []),
     "u1_imm": (["ZS_IMMEDIATE_CONSTANTS"], []),
     "rk": (["ZS_ROUND_KEYS"], []),
     "rk_r88": (["ZS_ROUND_KEYS", "ZS_MAXNREG=88"], []),

@@ -36,14 +36,14 @@ extern "C" __global__ void probe_observe(const double *in, double *out, const in
   S1 = S1 + d; S2 = S2 + d * d;
   const double dn = (double)n;
   const double inv_n = 1.0 / dn;
+  const double inv_nm1 = 1.0 / (dn - 1.0);
   const double mean = sh + S1 * inv_n;
-  double s2 = (S2 - S1 * (S1 * inv_n)) / (dn - 1.0);
+  double s2 = (S2 - S1 * (S1 * inv_n)) * inv_nm1;
   const double fl = 1e-12 * (1.0 + mean * mean);
   if (!(s2 >= fl)) s2 = fl;
-  const double q = 1.0 / s2;
-  const double var = 1.0 / (in[4] + dn * q);
-  const double sum = dn * sh + S1;
-  out[0] = var * (in[5] + sum * q); out[1] = sqrt(var); out[2] = S1; out[3] = S2;
+  const double den = (in[4] * s2) + dn;
+  const double sum = (dn * sh) + S1;
+  out[0] = ((in[5] * s2) + sum) / den; out[1] = sqrt(s2 / den); out[2] = S1; out[3] = S2;
 }
 // trace lookup + charge + early-stop test (NC-5), not-stopped path
 extern "C" __global__ void probe_charge(const double *in, const int *pool, double *out, long long trial, int t) {

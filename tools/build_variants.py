@@ -8,6 +8,9 @@ from paper_2208_06102_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "u1": ([], []),
+    "norecip": (["ZS_RECIP_TABLE=0"], []),
+    "p2b6": (["ZS_P2_MIN_BLOCKS=6"], []),
+    "p2b5": (["ZS_P2_MIN_BLOCKS=5"], []),
     "pipe": (["ZS_PIPELINE=1"], []),
     "hoist": (["ZS_HOIST_REPLICA=1"], []),
     "pipe_hoist": (["ZS_PIPELINE=1", "ZS_HOIST_REPLICA=1"], []),
@@ -33,7 +36,7 @@ if __name__ == "__main__":
         log = open(out + ".ptxas.log").read().split("Compiling entry function")
         for part in log:
             head = part.split("\n")[0]
-            if "replay_kernelILb0ELb0E" in head:
-                ph = head.split("ELi")[1][0] if "ELi" in head else "?"
+            if "replay_kernelILb0ELb0E" in head or "replay_kernel_tsILb0ELb0E" in head:
+                ph = head.split("ELi")[1][0] if "ELi" in head else "ts"
                 print(n, "phase", ph, [l.strip()[-70:] for l in part.splitlines()
                                        if "Used" in l or "spill" in l])

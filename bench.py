@@ -232,11 +232,13 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     curves = torch.zeros((nc, R, 7), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    launches = []
 
     def step():
         sim.run(stream)
         with torch.cuda.stream(stream):
             r = sim.results(want=["counters"], out={"curves": curves})
+            launches.append(r["kernel_launches"])
             reduce_curves(curves)
         return r
 
@@ -328,7 +330,7 @@ def main():
                 "config": workload_config(args, job, world), "clocks": clocks,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "steps": e2e_steps},
-                "gpu_launches": 3 * args.steps, "roofline": roofline,
+                "gpu_launches": int(sum(launches[-args.steps:])), "roofline": roofline,
                 "replay_ms_per_step": replay_total / args.steps,
                 "counters_per_step": [int(x) for x in counters]}
         if world == 1 and not args.no_cpu_baseline:

@@ -81,7 +81,15 @@ typedef struct {
   double prior_var;                  /* σ̂0² > 0; +INFINITY = flat prior */
   uint64_t seed;                     /* Philox4x32-10 key (NC-3) */
   int64_t trials;                    /* global trial count of this cell, >= 0 */
+  int32_t policy;                    /* ZEUS_POLICY_*: Zeus, or one of the paper's baselines
+                                        replayed on the same traces and replica draws */
 } zeus_cell;
+
+/* policies (§6.1 "Baselines"; DESIGN.md R-Q29) */
+#define ZEUS_POLICY_ZEUS 0          /* Alg. 3 pruning + Alg. 1/2 Thompson sampling, Eq. 7 p*, early stop */
+#define ZEUS_POLICY_DEFAULT 1       /* (b0, largest power limit) every recurrence */
+#define ZEUS_POLICY_GRID_SEARCH 2   /* one (b, p) per recurrence, b then p ascending; a failed run
+                                       prunes its batch size; then the cheapest seen */
 
 typedef struct {
   uint32_t struct_size;              /* = sizeof(zeus_run_opts) */
@@ -131,6 +139,7 @@ typedef struct {
   /* timing of the last zeus_sim_run, CUDA events on the caller's stream:
      step 1 (Eq. 7) kernel, replay kernel, curve-reduction kernel */
   float step1_ms, replay_ms, reduce_ms;
+  int32_t kernel_launches;           /* kernels the last zeus_sim_run launched */
 } zeus_results;
 
 /* Validates job, cells and opts (every violated invariant is reported),

@@ -335,6 +335,7 @@ std::string validate(const oracle_trace &tr, const oracle_cell &cell) {
   if (cell.window == 1 || cell.window < 0) add("window must be 0 (unbounded) or >= 2");
   if (!(cell.prior_var > 0.0)) add("prior variance must be > 0");
   if (!std::isfinite(cell.prior_mean)) add("prior mean not finite");
+  if (cell.policy < 0 || cell.policy > 2) add("policy must be 0 (Zeus), 1 (Default) or 2 (Grid Search)");
   if (B >= 1 && P >= 1 && B <= 32 && P <= 64) {
     for (int i = 0; i < B * P; ++i)
       if (!(tr.avg_power_w[i] > 0.0) || !std::isfinite(tr.avg_power_w[i])) { add("average power not positive"); break; }
@@ -374,9 +375,85 @@ struct TrialResult {
 
 struct Counters { int64_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0}; };
 
+// Per-epoch cost, time and energy of configuration (b, p) -- the quantity inside the
+// min of Eq. 7, in the NC-2 operation order.
+void epoch_cost(const oracle_trace &tr, const oracle_cell &cell, int b, int p, double *c,
+                double *t, double *e) {
+  const double A = tr.avg_power_w[(size_t)b * tr.num_power_limits + p];
+  const double Th = tr.throughput_eps[(size_t)b * tr.num_power_limits + p];
+  *c = ((cell.eta * A) + ((1.0 - cell.eta) * tr.max_power_w)) / Th;
+  *t = 1.0 / Th;
+  *e = A / Th;
+}
+
+// The two baselines of §6.1, replayed on the same trace with the same
+// replica draws (NC-3) as Zeus.  Neither uses the JIT profiler nor Zeus's early stop
+// (R-Q29): every run goes to its epochs-to-target or max_epochs.
+//   Default:      every recurrence runs (b0, the largest power limit).
+//   Grid Search:  one (b, p) per recurrence, b ascending then p ascending; a run that
+//                 fails to reach the target prunes the rest of its batch size;
+//                 after the grid, exploit the cheapest converged configuration seen.
+void run_trial_baseline(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
+                        int32_t R, int64_t trial, TrialResult &res, double *curves, uint32_t *log,
+                        double *clog, double *elog, double *tlog, Counters &cnt) {
+  const int B = tr.num_batch_sizes, P = tr.num_power_limits, S = tr.num_slices, K = tr.replicas;
+  bool exploring = cell.policy == 2;
+  int gb = 0, gp = 0;                                        // grid cursor
+  double best_c = std::numeric_limits<double>::infinity();
+  int best_b = -1, best_p = -1;
+  for (int32_t t = 0; t < R; ++t) {
+    const int s = (int)(((int64_t)t * S) / R);
+    int b, p;
+    if (cell.policy == 1) { b = tr.default_bs_index; p = P - 1; }
+    else if (exploring) { b = gb; p = gp; }
+    else if (best_b >= 0) { b = best_b; p = best_p; }
+    else { b = tr.default_bs_index; p = P - 1; }             // nothing converged in the grid
+    double c, tt, e;
+    epoch_cost(tr, cell, b, p, &c, &tt, &e);
+    const uint32_t r = replica(cell.seed, trial, t, K);
+    const int32_t E = tr.epochs_to_target[((size_t)s * B + b) * K + r];
+    const int32_t E_run = E > 0 ? E : tr.max_epochs;
+    const double em1 = (double)(E_run - 1);
+    const double C = c + em1 * c;
+    const double Tm = tt + em1 * tt;
+    const double En = e + em1 * e;
+    const bool converged = E > 0;
+    if (exploring) {
+      if (converged && C < best_c) { best_c = C; best_b = b; best_p = p; }
+      if (!converged || gp == P - 1) { gb += 1; gp = 0; }   // prune b, or its row is done
+      else gp += 1;
+      if (gb == B) exploring = false;
+    }
+    cnt.c[0] += 1;
+    const uint32_t flags = converged ? 2u : 0u;
+    res.tot_cost += C;
+    res.tot_energy += En;
+    res.tot_time += Tm;
+    res.final_arm = b;
+    const uint8_t bytes[3] = {(uint8_t)b, (uint8_t)p, (uint8_t)flags};   // NC-9 digest
+    for (int q = 0; q < 3; ++q) { res.digest ^= bytes[q]; res.digest *= 0x100000001b3ULL; }
+    if (curves) {
+      double *row = curves + (size_t)t * 7;
+      row[0] += C;
+      row[1] += En;
+      row[2] += Tm;
+      row[3] += T.ebar[(size_t)s * B + b] * c - T.opt[s];   // Eq. 9 pseudo-regret at (b, p)
+      row[5] += (b == T.opt_arm[s] && p == T.pstar[b]) ? 1.0 : 0.0;
+    }
+    if (log) log[t] = (uint32_t)b | ((uint32_t)p << 8) | (flags << 16);
+    if (clog) clog[t] = C;
+    if (elog) elog[t] = En;
+    if (tlog) tlog[t] = Tm;
+  }
+}
+
 void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T, int32_t R,
                int64_t trial, TrialResult &res, double *curves, uint32_t *log, double *clog,
                double *elog, double *tlog, Counters &cnt) {
+  if (cell.policy != 0) {
+    run_trial_baseline(tr, cell, T, R, trial, res, curves, log, clog, elog, tlog, cnt);
+    return;
+  }
   const int B = tr.num_batch_sizes, S = tr.num_slices, K = tr.replicas;
   const Prior pr = make_prior(cell.prior_mean, cell.prior_var);
   std::vector<Arm> arm(B);

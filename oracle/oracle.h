@@ -46,6 +46,8 @@ typedef struct {
   double prior_mean;   /* μ̂0 (Alg. 2) */
   double prior_var;    /* σ̂0², +inf = flat prior */
   uint64_t seed;       /* Philox key */
+  int32_t policy;      /* 0 Zeus (Alg. 3 + Alg. 1/2), 1 Default (b0, max p), 2 Grid Search
+                          with pruning (§6.1) */
 } oracle_cell;
 
 typedef struct {       /* step-1 tables; any pointer may be NULL */

@@ -54,6 +54,7 @@ class Cell(C.Structure):
         ("prior_mean", C.c_double),
         ("prior_var", C.c_double),
         ("seed", C.c_uint64),
+        ("policy", C.c_int32),
     ]
 
 
@@ -140,7 +141,7 @@ class _Held:
 def _cell(c):
     return Cell(float(c["eta"]), float(c["beta"]), int(c.get("window", 0)),
                 float(c.get("prior_mean", 0.0)), float(c.get("prior_var", np.inf)),
-                int(c.get("seed", 0)))
+                int(c.get("seed", 0)), int(c.get("policy", 0)))
 
 
 def validate(w, c):

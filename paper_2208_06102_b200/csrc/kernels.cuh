@@ -38,7 +38,7 @@ struct ArmConst {                 // per (cell, arm), 64 B
 
 struct CellParam {                // per cell
   double eta, beta, prec0, pm0;
-  int32_t window, pad;
+  int32_t window, policy;         // policy: 0 Zeus, 1 Default, 2 Grid Search (§6.1)
   uint32_t key0, key1;
   int64_t begin, n, out_off;      // global first trial, shard size, offset into per-trial outputs
 };
@@ -52,6 +52,7 @@ struct Step1Args {
   double *regret;                 // [cells][reg_stride] (S*B used)
   double *opt;                    // [cells][S]
   int32_t *opt_arm;               // [cells][opt_stride] (S used)
+  double *ebar;                   // [S][B] mean epochs of converged replicas (cell-independent)
   int B, P, S, K, max_epochs, reg_stride, opt_stride;
   double MP;
 };
@@ -124,6 +125,7 @@ __global__ void step1_kernel(Step1Args a) {
       }
       const double eb = cnt > 0 ? (double)sum / (double)cnt : (double)a.max_epochs;
       a.regret[(size_t)cell * a.reg_stride + (size_t)s * a.B + b] = eb * arms[b].c1 - best;
+      if (cell == 0) a.ebar[(size_t)s * a.B + b] = eb;
     }
   }
 }
@@ -154,10 +156,15 @@ struct ReplayArgs {
   int t_split;
   struct Carry *carry;            // [stride] per-trial scalar state between phases
   int32_t *perm;                  // [stride] phase-B lane -> trial (within each cell's block)
-  int32_t *bucket;                // [cells][kBuckets] histogram, then running offsets
+  int32_t *bucket;                // [cells][nwin][kBuckets] histogram, then running offsets
+  int nwin;                       // regroup windows per cell
 };
 
 constexpr int kBuckets = 17;      // popcount of the survivor-pair mask, 0..16
+#ifndef ZS_REGROUP_WINDOW
+#define ZS_REGROUP_WINDOW 8192
+#endif
+constexpr int kRegroupWindow = ZS_REGROUP_WINDOW;   // trials regrouped together (multiple of 128)
 
 struct __align__(16) ArmStat {    // Observe state of one arm of one trial (NC-6)
   double sh, S1, S2;              // shift (first observation) and shifted sums
@@ -195,6 +202,30 @@ __device__ __forceinline__ int warp_sum(int v) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   return v;
+}
+
+// Warp partial of the curves at recurrence t: a reduce-scatter leaves the warp total of
+// fp64 quantity (lane >> 3) in lanes 0, 8, 16, 24 (12 shuffles instead of 40), then one
+// 4-lane atomic for the sums and one 3-lane atomic for the counts (packed 8 bits each:
+// stops | optimal << 8 | Thompson << 16).  All 32 lanes must call it.
+__device__ __forceinline__ void curve_accumulate(double *curves, int t, int lane, double vC,
+                                                 double vE, double vT, double vReg, int vPacked) {
+  const bool h = lane & 16, g = lane & 8;
+  double k0 = h ? vT : vC, k1 = h ? vReg : vE;
+  k0 += __shfl_xor_sync(0xffffffffu, h ? vC : vT, 16);
+  k1 += __shfl_xor_sync(0xffffffffu, h ? vE : vReg, 16);
+  double kq = g ? k1 : k0;
+  kq += __shfl_xor_sync(0xffffffffu, g ? k0 : k1, 8);
+  kq += __shfl_xor_sync(0xffffffffu, kq, 4);
+  kq += __shfl_xor_sync(0xffffffffu, kq, 2);
+  kq += __shfl_xor_sync(0xffffffffu, kq, 1);
+  vPacked = warp_sum(vPacked);
+  double *row = curves + (size_t)t * kQ;
+  if ((lane & 7) == 0) {
+    atomicAdd(row + (lane >> 3), kq);
+    const int cntq = (vPacked >> (lane & 24)) & 0xff;     // lane 0: stops, 8: optimal, 16: TS
+    if (lane < 24 && cntq) atomicAdd(row + 4 + (lane >> 3), (double)cntq);
+  }
 }
 
 // 1-D bulk copy global -> shared through the TMA unit, completion on an mbarrier.
@@ -274,7 +305,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const CellParam cp = a.cells[cell];
   const int tid = threadIdx.x, TPB = blockDim.x;
   const int64_t j0 = (int64_t)blockIdx.x * TPB;
-  if (j0 >= cp.n) return;                                  // whole block past this cell's shard
+  if (j0 >= cp.n || cp.policy != 0) return;               // past the shard / a baseline cell
 
   // ---- stage the cell's tables with TMA bulk copies (one elected thread)
   const TabLayout L(a.B, a.S, a.K);
@@ -532,28 +563,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       vReg = regret[s * B + b];
       vPacked = (stopped ? 1 : 0) | ((b == optarm[s]) ? (1 << 8) : 0) | (ts_dec ? (1 << 16) : 0);
     }
-    // ---------------- warp partial of the curves: a reduce-scatter leaves the warp total of
-    // quantity (lane >> 3) in lanes 0, 8, 16, 24 (12 shuffles instead of 40); then one
-    // 4-lane atomic for the fp64 sums and one 3-lane atomic for the counts
-    {
-      const int lane = tid & 31;
-      const bool h = lane & 16, g = lane & 8;
-      double k0 = h ? vT : vC, k1 = h ? vReg : vE;
-      k0 += __shfl_xor_sync(0xffffffffu, h ? vC : vT, 16);
-      k1 += __shfl_xor_sync(0xffffffffu, h ? vE : vReg, 16);
-      double kq = g ? k1 : k0;
-      kq += __shfl_xor_sync(0xffffffffu, g ? k0 : k1, 8);
-      kq += __shfl_xor_sync(0xffffffffu, kq, 4);
-      kq += __shfl_xor_sync(0xffffffffu, kq, 2);
-      kq += __shfl_xor_sync(0xffffffffu, kq, 1);
-      vPacked = warp_sum(vPacked);
-      double *row = curves + (size_t)t * kQ;
-      if ((lane & 7) == 0) {
-        atomicAdd(row + (lane >> 3), kq);
-        const int cntq = (vPacked >> (lane & 24)) & 0xff;   // lane 0: stops, 8: optimal, 16: TS
-        if (lane < 24 && cntq) atomicAdd(row + 4 + (lane >> 3), (double)cntq);
-      }
-    }
+    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked);
     if (active) {
       // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
       {
@@ -597,7 +607,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       c.nstop = nstop; c.last_b = last_b;
       c.n_sampled = n_sampled; c.n_prune = n_prune; c.n_forced = n_forced; c.n_recomp = n_recomp;
       a.carry[o] = c;
-      atomicAdd(&a.bucket[cell * kBuckets + __popc(ts_pairs)], 1);
+      atomicAdd(&a.bucket[((size_t)cell * a.nwin + jj / kRegroupWindow) * kBuckets + __popc(ts_pairs)], 1);
     }
     return;
   }
@@ -622,32 +632,137 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   }
 }
 
-// bucket offsets: exclusive scan of the per-cell histogram (one thread per cell)
-__global__ void bucket_scan_kernel(int32_t *bucket, int ncells) {
-  const int cell = blockIdx.x * blockDim.x + threadIdx.x;
-  if (cell >= ncells) return;
-  int run = 0;
+// Regrouping is done within windows of kRegroupWindow consecutive trials: warps still get
+// (almost) uniform draw counts, and a window's Observe records (~1 MB at B = 16) stay on
+// one or two 2 MB pages, so phase B's scattered lanes do not thrash the TLB.
+// bucket offsets: exclusive scan of each (cell, window) histogram, offset by the window base
+__global__ void bucket_scan_kernel(int32_t *bucket, int ncells, int nwin) {
+  const int64_t cw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (cw >= (int64_t)ncells * nwin) return;
+  int run = (int)(cw % nwin) * kRegroupWindow;
   for (int k = 0; k < kBuckets; ++k) {
-    const int c = bucket[cell * kBuckets + k];
-    bucket[cell * kBuckets + k] = run;
+    const int c = bucket[cw * kBuckets + k];
+    bucket[cw * kBuckets + k] = run;
     run += c;
   }
 }
 
-// phase-B lane order: trials of a cell grouped by their survivor-pair count
+// phase-B lane order: the trials of each window grouped by their survivor-pair count
 __global__ void bucket_scatter_kernel(const CellParam *cells, const Carry *carry, int32_t *bucket,
-                                      int32_t *perm, int ncells, int B) {
+                                      int32_t *perm, int ncells, int B, int nwin) {
   const int cell = blockIdx.y;
   const CellParam cp = cells[cell];
+  if (cp.policy != 0) return;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cp.n;
        j += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t ts_set = carry[cp.out_off + j].ts_set;
     uint32_t pairs = 0;
     for (int k = 0; 2 * k < B; ++k)
       if ((ts_set >> (2 * k)) & 3u) pairs |= 1u << k;
-    const int pos = atomicAdd(&bucket[cell * kBuckets + __popc(pairs)], 1);
+    const int pos = atomicAdd(&bucket[((size_t)cell * nwin + j / kRegroupWindow) * kBuckets + __popc(pairs)], 1);
     perm[cp.out_off + pos] = (int32_t)j;
   }
+}
+
+// ------------------------------------------------------------------ §6.1 baselines
+// Default (b0, largest power limit) and Grid Search with pruning,
+// replayed on the same traces with the same replica draws as Zeus.
+// Neither uses the JIT profiler or the early stop (R-Q29).  One thread per trial; the
+// per-epoch cost of (b, p) is Eq. 7's inner term in the NC-2 order.
+struct BaselineArgs {
+  const CellParam *cells;
+  const double *A, *Th;           // [B][P]
+  const int32_t *pool;            // [S][B][K]
+  const ArmConst *arms;           // [cells][B] (p*)
+  const double *ebar;             // [S][B]
+  const double *opt;              // [cells][S]
+  const int32_t *opt_arm;         // [cells][opt_stride]
+  double *curve_slots;            // [cells][nslot][R][kQ]
+  double *tot_cost, *tot_energy, *tot_time;
+  unsigned long long *digest;
+  int32_t *n_stop, *final_arm;
+  uint32_t *log;
+  unsigned long long *counters;
+  int B, P, S, K, R, max_epochs, b0, nslot, opt_stride;
+  double MP;
+};
+
+template <bool LOG>
+__global__ void __launch_bounds__(128) baseline_kernel(BaselineArgs a) {
+  const int cell = blockIdx.y;
+  const CellParam cp = a.cells[cell];
+  const int tid = threadIdx.x;
+  const int64_t j0 = (int64_t)blockIdx.x * blockDim.x;
+  if (j0 >= cp.n || cp.policy == 0) return;
+  const int64_t jj = j0 + tid;
+  const bool active = jj < cp.n;
+  const int64_t trial = cp.begin + jj;
+  const size_t o = (size_t)(cp.out_off + jj);
+  const int B = a.B, P = a.P, S = a.S, K = a.K, R = a.R;
+  const int warp_global = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
+  double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
+  const ArmConst *arms = a.arms + (size_t)cell * B;
+  bool exploring = cp.policy == 2;
+  int gb = 0, gp = 0;
+  double best_c = __longlong_as_double(0x7ff0000000000000ll);
+  int best_b = -1, best_p = -1;
+  double totC = 0.0, totE = 0.0, totT = 0.0;
+  unsigned long long dig = 0xcbf29ce484222325ull;
+  int last_b = -1, s = 0;
+  for (int t = 0; t < R; ++t) {
+    double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
+    int vPacked = 0;
+    if (S > 1)
+      while ((long long)(s + 1) * R <= (long long)t * S) ++s;
+    if (active) {
+      int b, p;
+      if (cp.policy == 1) { b = a.b0; p = P - 1; }
+      else if (exploring) { b = gb; p = gp; }
+      else if (best_b >= 0) { b = best_b; p = best_p; }
+      else { b = a.b0; p = P - 1; }                     // nothing converged in the grid
+      const double Ab = __ldg(a.A + (size_t)b * P + p), Thb = __ldg(a.Th + (size_t)b * P + p);
+      const double c = ((cp.eta * Ab) + ((1.0 - cp.eta) * a.MP)) / Thb;
+      const double tt = 1.0 / Thb, e = Ab / Thb;
+      const uint32_t r = replica(cp.key0, cp.key1, trial, t, (uint32_t)K);
+      const int E = __ldg(a.pool + ((size_t)s * B + b) * K + r);
+      const int Erun = E > 0 ? E : a.max_epochs;
+      const double em1 = (double)(Erun - 1);
+      const double C = c + em1 * c, Tm = tt + em1 * tt, En = e + em1 * e;
+      const bool conv = E > 0;
+      if (exploring) {
+        if (conv && C < best_c) { best_c = C; best_b = b; best_p = p; }
+        if (!conv || gp == P - 1) { gb += 1; gp = 0; } else gp += 1;
+        if (gb == B) exploring = false;
+      }
+      const uint32_t flags = conv ? 2u : 0u;
+      totC += C;
+      totE += En;
+      totT += Tm;
+      last_b = b;
+      dig = (dig ^ (unsigned long long)(uint32_t)b) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)(uint32_t)p) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)flags) * 0x100000001b3ull;
+      if (LOG) a.log[o * R + t] = (uint32_t)b | ((uint32_t)p << 8) | (flags << 16);
+      vC = C;
+      vE = En;
+      vT = Tm;
+      vReg = __ldg(a.ebar + (size_t)s * B + b) * c - __ldg(a.opt + (size_t)cell * S + s);
+      vPacked = (b == __ldg(a.opt_arm + (size_t)cell * a.opt_stride + s) && p == arms[b].pstar) ? (1 << 8) : 0;
+    }
+    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked);
+  }
+  if (active) {
+    a.tot_cost[o] = totC;
+    a.tot_energy[o] = totE;
+    a.tot_time[o] = totT;
+    a.digest[o] = dig;
+    a.n_stop[o] = 0;
+    a.final_arm[o] = last_b;
+  }
+  unsigned long long v = active ? (unsigned long long)R : 0ull;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if ((tid & 31) == 0 && v) atomicAdd(a.counters, v);
 }
 
 // curves[cell][t][q] = sum over slots in slot order

@@ -51,15 +51,15 @@ struct zeus_sim {
   int64_t shard_total = 0, max_shard = 0;
   // trace
   int S = 0, K = 0, reg_stride = 0, opt_stride = 0;
-  bool loaded = false, ran = false;
-  int nslot = 1, tpb = 128, smem_bytes = 0, tab_bytes = 0;
+  bool loaded = false, ran = false, any_zeus = false, any_baseline = false;
+  int nslot = 1, tpb = 128, smem_bytes = 0, tab_bytes = 0, launches = 0, nwin = 1;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   std::string err;
   // device memory
   DevBuf d_A, d_Th, d_pool, d_cells, d_arms, d_regret, d_opt, d_optarm;
   DevBuf d_slots, d_curves, d_tot_cost, d_tot_energy, d_tot_time, d_digest, d_nstop, d_final,
-      d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket;
+      d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket, d_ebar;
   ~zeus_sim() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -140,6 +140,8 @@ void check_cells(const zeus_cell *cells, int n, Errors &E) {
     if (!(c.prior_var > 0.0)) E.add(ZEUS_E_INVALID, "prior variance must be > 0" + at);
     if (!std::isfinite(c.prior_mean)) E.add(ZEUS_E_INVALID, "prior mean not finite" + at);
     if (c.trials < 0) E.add(ZEUS_E_INVALID, "trials < 0" + at);
+    if (c.policy < ZEUS_POLICY_ZEUS || c.policy > ZEUS_POLICY_GRID_SEARCH)
+      E.add(ZEUS_E_INVALID, "policy must be ZEUS_POLICY_ZEUS, _DEFAULT or _GRID_SEARCH" + at);
   }
 }
 
@@ -164,6 +166,7 @@ void launch_step1(zeus_sim *s, cudaStream_t st) {
   a.regret = s->d_regret.as<double>();
   a.opt = s->d_opt.as<double>();
   a.opt_arm = s->d_optarm.as<int32_t>();
+  a.ebar = s->d_ebar.as<double>();
   a.B = s->B; a.P = s->P; a.S = s->S; a.K = s->K; a.max_epochs = s->max_epochs;
   a.reg_stride = s->reg_stride; a.opt_stride = s->opt_stride; a.MP = s->MP;
   zs::step1_kernel<<<(unsigned)s->cells.size(), 256, 0, st>>>(a);
@@ -229,6 +232,9 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     p.prec0 = std::isinf(c.prior_var) ? 0.0 : 1.0 / c.prior_var;   // flat prior
     p.pm0 = c.prior_mean * p.prec0;
     p.window = c.window;
+    p.policy = c.policy;
+    s->any_zeus |= c.policy == ZEUS_POLICY_ZEUS;
+    s->any_baseline |= c.policy != ZEUS_POLICY_ZEUS;
     p.key0 = (uint32_t)c.seed;
     p.key1 = (uint32_t)(c.seed >> 32);
     const int64_t b = std::min(opts->shard_begin, c.trials);
@@ -241,6 +247,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     s->cpar.push_back(p);
   }
   s->shard_total = off;
+  s->nwin = (int)std::max<int64_t>(1, (s->max_shard + zs::kRegroupWindow - 1) / zs::kRegroupWindow);
   // curve slots: spread the per-warp atomics over up to 64 copies, bounded to 64 MB
   const size_t curve_bytes = (size_t)num_cells * s->R * zs::kQ * sizeof(double);
   s->nslot = (int)std::max<size_t>(1, std::min<size_t>(64, (64ull << 20) / std::max<size_t>(1, curve_bytes)));
@@ -262,7 +269,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
       (e = s->d_st_ring.alloc(n * s->B * (size_t)s->wmax * 8)) != cudaSuccess ||
       (e = s->d_carry.alloc(n * sizeof(zs::Carry))) != cudaSuccess ||
       (e = s->d_perm.alloc(n * 4)) != cudaSuccess ||
-      (e = s->d_bucket.alloc((size_t)num_cells * zs::kBuckets * 4)) != cudaSuccess) {
+      (e = s->d_bucket.alloc((size_t)num_cells * s->nwin * zs::kBuckets * 4)) != cudaSuccess) {
     std::string m = std::string("device allocation: ") + cudaGetErrorString(e);
     delete s;
     return fail(nullptr, e == cudaErrorMemoryAllocation ? ZEUS_E_NOMEM : ZEUS_E_CUDA, m);
@@ -330,6 +337,7 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   ZS_CUDA(s, s->d_regret.alloc((size_t)nc * s->reg_stride * 8));
   ZS_CUDA(s, s->d_opt.alloc((size_t)nc * S * 8));
   ZS_CUDA(s, s->d_optarm.alloc((size_t)nc * s->opt_stride * 4));
+  ZS_CUDA(s, s->d_ebar.alloc((size_t)S * B * 8));
   ZS_CUDA(s, cudaMemset(s->d_pool.p, 0, s->d_pool.bytes));
   ZS_CUDA(s, cudaMemset(s->d_regret.p, 0, s->d_regret.bytes));
   ZS_CUDA(s, cudaMemset(s->d_optarm.p, 0, s->d_optarm.bytes));
@@ -381,7 +389,35 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
   launch_step1(s, st);                        // a1: Eq. 7 argmin + per-arm constants
   ZS_CUDA(s, cudaGetLastError());
   ZS_CUDA(s, cudaEventRecord(s->ev3, st));
-  if (s->max_shard > 0 && s->R > 0) {
+  s->launches = 2;                            // step 1 + curve reduction
+  if (s->max_shard > 0 && s->R > 0 && s->any_baseline) {
+    zs::BaselineArgs b{};
+    b.cells = s->d_cells.as<zs::CellParam>();
+    b.A = s->d_A.as<double>();
+    b.Th = s->d_Th.as<double>();
+    b.pool = s->d_pool.as<int32_t>();
+    b.arms = s->d_arms.as<zs::ArmConst>();
+    b.ebar = s->d_ebar.as<double>();
+    b.opt = s->d_opt.as<double>();
+    b.opt_arm = s->d_optarm.as<int32_t>();
+    b.curve_slots = s->d_slots.as<double>();
+    b.tot_cost = s->d_tot_cost.as<double>();
+    b.tot_energy = s->d_tot_energy.as<double>();
+    b.tot_time = s->d_tot_time.as<double>();
+    b.digest = s->d_digest.as<unsigned long long>();
+    b.n_stop = s->d_nstop.as<int32_t>();
+    b.final_arm = s->d_final.as<int32_t>();
+    b.log = s->d_log.as<uint32_t>();
+    b.counters = s->d_counters.as<unsigned long long>();
+    b.B = s->B; b.P = s->P; b.S = s->S; b.K = s->K; b.R = s->R; b.max_epochs = s->max_epochs;
+    b.b0 = s->b0; b.nslot = s->nslot; b.opt_stride = s->opt_stride; b.MP = s->MP;
+    const dim3 grid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
+    if (s->log_mode) zs::baseline_kernel<true><<<grid, 128, 0, st>>>(b);
+    else zs::baseline_kernel<false><<<grid, 128, 0, st>>>(b);
+    ZS_CUDA(s, cudaGetLastError());
+    s->launches += 1;
+  }
+  if (s->max_shard > 0 && s->R > 0 && s->any_zeus) {
     zs::ReplayArgs a{};
     a.cells = s->d_cells.as<zs::CellParam>();
     a.arms = s->d_arms.as<zs::ArmConst>();
@@ -413,19 +449,22 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     a.carry = s->d_carry.as<zs::Carry>();
     a.perm = s->d_perm.as<int32_t>();
     a.bucket = s->d_bucket.as<int32_t>();
+    a.nwin = s->nwin;
     const bool two_phase = s->layout != 1 && a.t_split < s->R;
     if (!two_phase) {
       replay_fn(windowed, s->log_mode, 0)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
       ZS_CUDA(s, cudaGetLastError());
+      s->launches += 1;
     } else {
+      s->launches += 4;
       ZS_CUDA(s, cudaMemsetAsync(s->d_bucket.p, 0, s->d_bucket.bytes, st));
       replay_fn(windowed, s->log_mode, 1)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
       ZS_CUDA(s, cudaGetLastError());
-      zs::bucket_scan_kernel<<<(nc + 127) / 128, 128, 0, st>>>(a.bucket, nc);
+      zs::bucket_scan_kernel<<<(unsigned)((nc * (int64_t)s->nwin + 127) / 128), 128, 0, st>>>(a.bucket, nc, s->nwin);
       ZS_CUDA(s, cudaGetLastError());
       const unsigned sx = (unsigned)std::min<int64_t>((s->max_shard + 255) / 256, 1184);
       zs::bucket_scatter_kernel<<<dim3(std::max(1u, sx), (unsigned)nc), 256, 0, st>>>(
-          a.cells, a.carry, a.bucket, a.perm, nc, s->B);
+          a.cells, a.carry, a.bucket, a.perm, nc, s->B, s->nwin);
       ZS_CUDA(s, cudaGetLastError());
       replay_fn(windowed, s->log_mode, 2)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
       ZS_CUDA(s, cudaGetLastError());
@@ -508,6 +547,7 @@ zeus_status zeus_sim_results(zeus_sim *s, zeus_results *out) {
     ZS_CUDA(s, cudaEventElapsedTime(&out->replay_ms, s->ev3, s->ev1));
     ZS_CUDA(s, cudaEventElapsedTime(&out->reduce_ms, s->ev1, s->ev2));
   }
+  out->kernel_launches = s->ran ? s->launches : 0;
   return ZEUS_OK;
 }
 

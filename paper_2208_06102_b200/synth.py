@@ -121,10 +121,15 @@ def make_workload(name: str, seed: int = 0, slices: int = 1, replicas: int = 4,
     }
 
 
-def cell(eta=0.5, beta=2.0, window=0, seed=1, prior_mean=0.0, prior_var=math.inf) -> dict:
+POLICIES = {"zeus": 0, "default": 1, "grid_search": 2}   # §6.1 baselines
+
+
+def cell(eta=0.5, beta=2.0, window=0, seed=1, prior_mean=0.0, prior_var=math.inf,
+         policy="zeus") -> dict:
     """One sweep cell; defaults are the paper's η = 0.5, β = 2 and a flat prior."""
     return {"eta": float(eta), "beta": float(beta), "window": int(window), "seed": int(seed),
-            "prior_mean": float(prior_mean), "prior_var": float(prior_var)}
+            "prior_mean": float(prior_mean), "prior_var": float(prior_var),
+            "policy": POLICIES[policy] if isinstance(policy, str) else int(policy)}
 
 
 @dataclass
@@ -157,6 +162,13 @@ def config(name: str, seed: int = 2208, trials: int | None = None) -> list[Job]:
     if name == "cfg4_38":
         return [Job(make_workload("bert_sa", seed, slices=38, drift=True),
                     [cell(window=10, seed=seed + 4)], 38, trials or 100_000)]
+    if name == "f1":   # Zeus vs the §6.1 baselines on the six workloads, T = 2|B||P|
+        jobs = []
+        for w in SIX:
+            wl = make_workload(w, seed)
+            R = 2 * len(wl["batch_sizes"]) * len(wl["power_limits"])
+            jobs.append(Job(wl, [cell(seed=seed + 6, policy=p) for p in POLICIES], R, trials or 10_000))
+        return jobs
     if name == "cfg5":
         return [Job(make_workload("generic16", seed), [cell(seed=seed + 5)], 1000,
                     trials or 10_000_000)]
@@ -164,3 +176,4 @@ def config(name: str, seed: int = 2208, trials: int | None = None) -> list[Job]:
 
 
 CONFIGS = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")
+NEXT = ("f1",)   # SURVEY §8(f) rows built on the same replay

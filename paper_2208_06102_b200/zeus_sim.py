@@ -44,7 +44,7 @@ class zeus_job(C.Structure):
 class zeus_cell(C.Structure):
     _fields_ = [("eta", C.c_double), ("beta", C.c_double), ("window", C.c_int32),
                 ("prior_mean", C.c_double), ("prior_var", C.c_double), ("seed", C.c_uint64),
-                ("trials", C.c_int64)]
+                ("trials", C.c_int64), ("policy", C.c_int32)]
 
 
 class zeus_run_opts(C.Structure):
@@ -60,7 +60,8 @@ class zeus_results(C.Structure):
                 ("c1", C.c_void_p), ("t1", C.c_void_p), ("e1", C.c_void_p), ("c_prof", C.c_void_p),
                 ("t_prof", C.c_void_p), ("e_prof", C.c_void_p), ("opt_cost", C.c_void_p),
                 ("opt_arm", C.c_void_p), ("log", C.c_void_p), ("counters", C.c_void_p),
-                ("step1_ms", C.c_float), ("replay_ms", C.c_float), ("reduce_ms", C.c_float)]
+                ("step1_ms", C.c_float), ("replay_ms", C.c_float), ("reduce_ms", C.c_float),
+                ("kernel_launches", C.c_int32)]
 
 
 _lib = None
@@ -157,7 +158,7 @@ class Simulation:
                        int(workload.get("charge_profiling", 1)))
         cs = [zeus_cell(float(c["eta"]), float(c["beta"]), int(c.get("window", 0)),
                         float(c.get("prior_mean", 0.0)), float(c.get("prior_var", math.inf)),
-                        int(c.get("seed", 0)), int(trials)) for c in cells]
+                        int(c.get("seed", 0)), int(trials), int(c.get("policy", 0))) for c in cells]
         opts = zeus_run_opts(C.sizeof(zeus_run_opts), int(recurrences), int(shard[0]),
                              int(shard[1]), 1 if log else 0, int(layout))
         self.h = zeus_sim_create(job, cs, opts, device)
@@ -211,6 +212,7 @@ class Simulation:
         bufs["step1_ms"] = res.step1_ms
         bufs["replay_ms"] = res.replay_ms
         bufs["reduce_ms"] = res.reduce_ms
+        bufs["kernel_launches"] = res.kernel_launches
         return bufs
 
     def close(self):

@@ -41,6 +41,7 @@ def run_gpu(zs, w, cells, trials, R, shard=(0, -1), log=False, want=None, layout
     out = sim.results(want=want or keys)
     out["R"] = sim.R
     out["n"] = sim.shard_n // len(cells)
+    out["kernel_launches"] = out.get("kernel_launches", 0)
     sim.close()
     return out
 
@@ -261,3 +262,14 @@ def test_schedules_bit_identical(zs, oracle, name):
     np.testing.assert_allclose(outs[0]["curves"], outs[1]["curves"], rtol=1e-12)
     compare_cell(oracle, outs[1], job.workload, job.cells[0], 0, np.arange(job.trials),
                  job.recurrences, job.trials, logs=True)
+
+
+def test_f1_baselines_same_replay(zs, oracle):
+    """Default and Grid Search (§6.1) replayed in the same launch
+    as Zeus on the six workloads, T = 2|B||P|; every trial bit-exact vs the oracle."""
+    for job in synth.config("f1", trials=3000):
+        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True)
+        assert g["kernel_launches"] >= 3
+        for ci, c in enumerate(job.cells):
+            compare_cell(oracle, g, job.workload, c, ci, np.arange(job.trials), job.recurrences,
+                         job.trials, logs=True)

@@ -436,3 +436,50 @@ def test_validation_lists_every_violation(oracle):
     rc, msg = oracle.validate(w2, synth.cell())
     assert rc == 1 and "no converged replica" in msg
     assert oracle.validate(synth.make_workload("bert_qa", 0), synth.cell())[0] == 0
+
+
+# ------------------------------------------------------------------ §6.1 baselines
+def test_default_baseline_closed_form(oracle):
+    """P:L787 Default = (b0, MAXPOWER) every recurrence, no profiling, no early stop:
+    each charge is E_run * c(b0, max p), the cost identity holds, and nothing is pruned."""
+    w = synth.make_workload("resnet50", 3)
+    cel = synth.cell(eta=0.3, beta=1.5, seed=4, policy="default")
+    R = 40
+    o = oracle.replay(w, cel, R, range(25), logs=True)
+    P = len(w["power_limits"])
+    assert np.all((o["log"] & 0xFF) == w["b0"]) and np.all(((o["log"] >> 8) & 0xFF) == P - 1)
+    A, Th = w["avg_power"][w["b0"], -1], w["throughput"][w["b0"], -1]
+    c = (0.3 * A + 0.7 * w["max_power"]) / Th
+    E = w["pool"][0, w["b0"]]
+    assert set(np.round(o["cost_log"].ravel() / c, 9)) <= set(E.astype(float))
+    np.testing.assert_allclose(o["cost_log"], 0.3 * o["energy_log"] + 0.7 * w["max_power"] * o["time_log"],
+                               rtol=1e-12)
+    assert np.all(o["n_stop"] == 0) and o["curves"][:, 6].sum() == 0
+
+
+def test_grid_search_enumeration_and_pruning(oracle):
+    """one (b, p) per recurrence, b then p ascending, a failed run
+    prunes the rest of its batch size, then the cheapest converged configuration is exploited."""
+    A = [[100, 100]] * 5
+    Th = [[1, 1], [1, 1], [1, 1], [2, 2], [1, 1]]
+    pool = [[[0], [10], [10], [10], [0]]]
+    w = trace([8, 16, 32, 64, 128], 2, [100, 200], 200, A, Th, pool, max_epochs=20)
+    o = oracle.replay(w, synth.cell(eta=1.0, policy="grid_search"), 20, range(3), logs=True)
+    for log in o["log"]:
+        bp = [(int(x & 0xFF), int(x >> 8 & 0xFF)) for x in log]
+        assert bp[:8] == [(0, 0), (1, 0), (1, 1), (2, 0), (2, 1), (3, 0), (3, 1), (4, 0)]
+        assert bp[8:] == [(3, 0)] * 12          # cheapest (c = 50) first found at p index 0
+    np.testing.assert_allclose(o["cost_log"][0, :8], [20 * 100, 1000, 1000, 1000, 1000, 500, 500, 2000])
+
+
+def test_zeus_beats_baselines_directionally(oracle):
+    """S:L627, S:L631 (directional, never parity): on the six synthetic workloads Zeus's
+    cumulative pseudo-regret is below Grid Search's, and its last-five-recurrence energy is
+    below Default's."""
+    wins_gs = wins_def = 0
+    for job in synth.config("f1", trials=60):
+        res = {c["policy"]: oracle.replay(job.workload, c, job.recurrences, range(60)) for c in job.cells}
+        zeus, default, gs = res[0], res[1], res[2]
+        wins_gs += zeus["curves"][:, 3].sum() < gs["curves"][:, 3].sum()
+        wins_def += zeus["curves"][-5:, 1].sum() < default["curves"][-5:, 1].sum()
+    assert wins_gs >= 5 and wins_def >= 5

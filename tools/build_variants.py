@@ -8,6 +8,9 @@ from paper_2208_06102_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "u1": ([], []),
+    "win512": (["ZS_REGROUP_WINDOW=512"], []),
+    "win8k": (["ZS_REGROUP_WINDOW=8192"], []),
+    "win1m": (["ZS_REGROUP_WINDOW=1048576"], []),
     "norecip": (["ZS_RECIP_TABLE=0"], []),
     "p2b6": (["ZS_P2_MIN_BLOCKS=6"], []),
     "p2b5": (["ZS_P2_MIN_BLOCKS=5"], []),

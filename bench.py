@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg5", choices=list(synth.CONFIGS) + ["cfg4_38"])
+    ap.add_argument("--config", default="cfg5", choices=list(synth.CONFIGS) + ["cfg4_38"] + list(synth.NEXT))
     ap.add_argument("--trials", type=int, default=None, help="trials per cell per GPU (default: the config's)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--layout", type=int, default=0)
@@ -117,7 +117,7 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ work model
-def work_per_launch(counters, ncells):
+def work_per_launch(counters, _unused=None):
     """Algorithmic lane-instructions of one launch: event counts x per-primitive SASS costs
     (tools/work_model.json)."""
     wm = json.load(open(os.path.join(ROOT, "tools", "work_model.json")))
@@ -179,11 +179,15 @@ def reference_main(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(args, job, world):
+def workload_config(args, jobs, world):
+    jobs = jobs if isinstance(jobs, list) else [jobs]
+    job = jobs[0]
     w = job.workload
-    return {"workload": f"{args.config}: {w['name']} synthetic trace, {len(w['batch_sizes'])} batch sizes x "
-                        f"{len(w['power_limits'])} power limits, {len(job.cells)} cell(s), "
+    names = ",".join(j.workload["name"] for j in jobs)
+    return {"workload": f"{args.config}: {names} synthetic trace(s), {len(w['batch_sizes'])} batch sizes x "
+                        f"{len(w['power_limits'])} power limits, {len(job.cells)} cell(s) per job, "
                         f"{job.recurrences} recurrences",
+            "jobs": len(jobs),
             "trials_per_gpu_per_cell": job.trials if args.scaling == "weak" else job.trials // world,
             "cells": len(job.cells), "recurrences": job.recurrences,
             "batch_sizes": len(w["batch_sizes"]), "power_limits": len(w["power_limits"]),
@@ -222,25 +226,35 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     jobs = synth.config(args.config, trials=args.trials)
-    if len(jobs) != 1:
-        raise SystemExit("bench runs single-job configs (cfg1, cfg4, cfg5)")
     job = jobs[0]
-    total, begin, end = shard_range(job.trials, world, rank, args.scaling)
-    sim = Simulation(job.workload, job.cells, total, job.recurrences, shard=(begin, end),
-                     device=local, layout=args.layout).load_profile()
-    R, nc = sim.R, sim.ncells
-    stream = torch.cuda.Stream(device=dev)
-    curves = torch.zeros((nc, R, 7), dtype=torch.float64, device=dev)
+    sims, streams, curves = [], [], []
+    for jb in jobs:                                  # one handle and one stream per job
+        total, begin, end = shard_range(jb.trials, world, rank, args.scaling)
+        sm = Simulation(jb.workload, jb.cells, total, jb.recurrences, shard=(begin, end),
+                        device=local, layout=args.layout).load_profile()
+        sims.append(sm)
+        streams.append(torch.cuda.Stream(device=dev))
+        curves.append(torch.zeros((sm.ncells, sm.R, 7), dtype=torch.float64, device=dev))
+    main = torch.cuda.Stream(device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     launches = []
 
     def step():
-        sim.run(stream)
-        with torch.cuda.stream(stream):
-            r = sim.results(want=["counters"], out={"curves": curves})
-            launches.append(r["kernel_launches"])
-            reduce_curves(curves)
-        return r
+        """All jobs of the config concurrently (one stream each); curves all-reduced (a8)."""
+        start = torch.cuda.Event()
+        start.record(main)
+        outs = []
+        for sm, st, cv in zip(sims, streams, curves):
+            st.wait_event(start)
+            sm.run(st)
+        for sm, st, cv in zip(sims, streams, curves):
+            with torch.cuda.stream(st):
+                r = sm.results(want=["counters"], out={"curves": cv})
+                reduce_curves(cv)
+            outs.append(r)
+            main.wait_stream(st)
+        launches.append(sum(r["kernel_launches"] for r in outs))
+        return outs
 
     for _ in range(args.warmup):
         step()
@@ -253,73 +267,89 @@ def main():
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         for i in range(args.steps):
-            with torch.cuda.stream(stream):
+            with torch.cuda.stream(main):
                 flush.zero_()                        # L2 flush outside the timed events
-            ev[i][0].record(stream)
-            r = step()
-            ev[i][1].record(stream)
-            replay_ms.append(r["replay_ms"])
-            counters = r["counters"]
+            ev[i][0].record(main)
+            outs = step()
+            ev[i][1].record(main)
+            replay_ms.append(sum(r["replay_ms"] for r in outs) if len(outs) == 1 else None)
+            counters = np.sum([r["counters"] for r in outs], axis=0)
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    t_local = torch.tensor([sum(step_ms), sum(replay_ms)], dtype=torch.float64, device=dev)
+    single = len(sims) == 1
+    t_local = torch.tensor([sum(step_ms), sum(replay_ms) if single else sum(step_ms)],
+                           dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     total_ms, replay_total = float(t_local[0]), float(t_local[1])
-    dec_per_step = (end - begin) * nc * R * world if args.scaling == "weak" else total * nc * R
+    dec_per_step = sum(sm.shard_n * sm.R for sm in sims) * world   # shards are equal across ranks
+    if args.scaling == "strong":
+        dec_per_step = sum(jb.trials * len(jb.cells) * sm.R for jb, sm in zip(jobs, sims))
     value = dec_per_step * args.steps / (total_ms / 1e3)
     clocks = clk.summary()
 
     # ---- e2e: public API with host buffers, H2D of the traces and D2H of the results every step
     e2e_steps = args.e2e_steps or max(1, min(args.steps, 3))
-    w = job.workload
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-    A_h, Th_h, pool_h = pin(w["avg_power"]), pin(w["throughput"]), pin(w["pool"].astype(np.int32))
-    n_out = sim.shard_n
-    host_out = {"curves": pin(np.zeros((nc, R, 7))), "tot_cost": pin(np.zeros(n_out)),
-                "tot_energy": pin(np.zeros(n_out)), "tot_time": pin(np.zeros(n_out)),
-                "digest": pin(np.zeros(n_out, np.uint64))}
     from paper_2208_06102_b200 import zeus_sim as Z
 
-    h2d = A_h.nbytes + Th_h.nbytes + pool_h.nbytes
-    d2h = sum(a.nbytes for a in host_out.values())
-    cur_h = torch.from_numpy(host_out["curves"])
+    h2d = d2h = 0
+    staged = []
+    for jb, sm in zip(jobs, sims):
+        w = jb.workload
+        A_h, Th_h, pool_h = pin(w["avg_power"]), pin(w["throughput"]), pin(w["pool"].astype(np.int32))
+        n_out = sm.shard_n
+        host_out = {"curves": pin(np.zeros((sm.ncells, sm.R, 7))), "tot_cost": pin(np.zeros(n_out)),
+                    "tot_energy": pin(np.zeros(n_out)), "tot_time": pin(np.zeros(n_out)),
+                    "digest": pin(np.zeros(n_out, np.uint64))}
+        h2d += A_h.nbytes + Th_h.nbytes + pool_h.nbytes
+        d2h += sum(a.nbytes for a in host_out.values())
+        staged.append((A_h, Th_h, pool_h, host_out))
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        Z.zeus_sim_load_profile(sim.h, A_h, Th_h, pool_h.shape[0], pool_h.shape[2], pool_h)
-        sim.run(stream)
-        sim.results(want=[], out=host_out)
-        if dist:
-            cur_h.copy_(reduce_curves(cur_h.to(dev)).cpu())
+        for sm, st, (A_h, Th_h, pool_h, host_out) in zip(sims, streams, staged):
+            Z.zeus_sim_load_profile(sm.h, A_h, Th_h, pool_h.shape[0], pool_h.shape[2], pool_h)
+            sm.run(st)
+        for sm, (A_h, Th_h, pool_h, host_out) in zip(sims, staged):
+            sm.results(want=[], out=host_out)
+            if dist:
+                cur_h = torch.from_numpy(host_out["curves"])
+                cur_h.copy_(reduce_curves(cur_h.to(dev)).cpu())
     torch.cuda.synchronize()
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = dec_per_step * e2e_steps / float(e2e_s[0])
 
-    # ---- roofline of the dominant kernel (the replay): algorithmic lane-instructions / duration
-    work = work_per_launch(counters, nc)
+    # ---- roofline of the dominant kernel group (the replay): algorithmic lane-instructions /
+    # its CUDA-event duration on the launching stream (whole step for multi-job configs)
+    work = work_per_launch(counters, None)
     launch_s = replay_total / args.steps / 1e3
     clock_hz = (clocks["sm_mhz"] or 1965.0) * 1e6
     peak_issue = ISSUE_LANES_PER_CLK_SM * SM_COUNT * clock_hz
     peak_fp64 = FP64_LANES_PER_CLK_SM * SM_COUNT * clock_hz
     ach_issue, ach_fp64 = work["total"] / launch_s, work["fp64"] / launch_s
     prof = os.path.join(ROOT, "profiles", "replay_traffic.json")
-    traffic = json.load(open(prof)).get("dram_bytes_per_launch") if os.path.exists(prof) else None
+    traffic = None
+    if os.path.exists(prof):
+        tr = json.load(open(prof))
+        traffic = tr["dram_bytes_per_decision"] * dec_per_step / world
     roofline = {"bound": "alu", "achieved": ach_issue / 1e12, "peak": peak_issue / 1e12,
                 "unit": "T lane-inst/s", "frac": ach_issue / peak_issue, "traffic": traffic,
-                "kernel": "zs::replay_kernel", "launch_ms": launch_s * 1e3,
+                "kernel": "replay (phase A + regroup + phase B kernels)" if single else "whole step",
+                "launch_ms": launch_s * 1e3,
                 "work_per_decision": work["total"] / max(1, int(counters[0])),
                 "peak_basis": f"issue: {ISSUE_LANES_PER_CLK_SM} lanes/clk/SM x {SM_COUNT} SMs x "
                               f"median SM clock under load {clock_hz / 1e6:.0f} MHz",
                 "fp64": {"achieved": ach_fp64 / 1e12, "peak": peak_fp64 / 1e12,
                          "frac": ach_fp64 / peak_fp64,
-                         "peak_basis": f"{FP64_LANES_PER_CLK_SM} FP64 lanes/clk/SM"}}
+                         "peak_basis": f"{FP64_LANES_PER_CLK_SM} FP64 lanes/clk/SM (measured "
+                                       "1.82e13 DFMA lane/s at 1965 MHz, tools/peaks.cu)"}}
 
     line = None
     if rank == 0:
@@ -327,11 +357,11 @@ def main():
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                 "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded generator, DESIGN.md §5)",
-                "config": workload_config(args, job, world), "clocks": clocks,
+                "config": workload_config(args, jobs, world), "clocks": clocks,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "steps": e2e_steps},
                 "gpu_launches": int(sum(launches[-args.steps:])), "roofline": roofline,
-                "replay_ms_per_step": replay_total / args.steps,
+                "replay_ms_per_step": replay_total / args.steps, "jobs": len(jobs),
                 "counters_per_step": [int(x) for x in counters]}
         if world == 1 and not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
@@ -341,7 +371,8 @@ def main():
                                     "sample": f"first {n} trials x {job.recurrences} recurrences of "
                                               f"{args.config}, {dt:.1f} s on {threads} threads"}
         print(json.dumps(line), flush=True)
-    sim.close()
+    for sm in sims:
+        sm.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()

@@ -156,6 +156,20 @@ ReplayFn replay_fn(bool windowed, bool log, int phase) {
   return tab[windowed][log][phase];
 }
 
+// Dynamic shared memory allowed per launch of fn: the device's opt-in maximum minus the
+// kernel's static shared memory.  Set once to the maximum (the attribute is process-wide),
+// so handles with different footprints can launch the same kernels concurrently.
+cudaError_t grant_max_smem(const void *fn, int device, int *granted = nullptr) {
+  int optin = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return e;
+  const int dyn = optin - (int)fa.sharedSizeBytes;
+  if (granted) *granted = dyn;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+}
+
 void launch_step1(zeus_sim *s, cudaStream_t st) {
   zs::Step1Args a{};
   a.A = s->d_A.as<double>();
@@ -360,17 +374,20 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
     if (bytes > 227 * 1024) continue;
     int blocks = 0;
     const void *fn = (const void *)replay_fn(wmax > 0, false, 0);
-    ZS_CUDA(s, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    int granted = 0;
+    ZS_CUDA(s, grant_max_smem(fn, s->device, &granted));
+    if ((int)bytes > granted) continue;
     ZS_CUDA(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, tpb, bytes));
     const int warps = blocks * tpb / 32;
     if (warps > best_warps) { best_warps = warps; s->tpb = tpb; s->smem_bytes = (int)bytes; }
   }
   if (best_warps <= 0) return fail(s, ZEUS_E_UNSUPPORTED, "no launch shape fits shared memory");
+  // the attribute is per function (process-wide): grant the device maximum once, so handles
+  // with different footprints can launch concurrently; each launch passes its own size
   for (int w = 0; w < 2; ++w)
     for (int l = 0; l < 2; ++l)
       for (int ph = 0; ph < 3; ++ph)
-        ZS_CUDA(s, cudaFuncSetAttribute((const void *)replay_fn(w, l, ph),
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, s->smem_bytes));
+        ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph), s->device));
   s->loaded = true;
   return ZEUS_OK;
 }

@@ -273,3 +273,22 @@ def test_f1_baselines_same_replay(zs, oracle):
         for ci, c in enumerate(job.cells):
             compare_cell(oracle, g, job.workload, c, ci, np.arange(job.trials), job.recurrences,
                          job.trials, logs=True)
+
+
+def test_concurrent_handles_different_footprints(zs, oracle):
+    """Handles with different shared-memory footprints (B = 6 windowed vs B = 16) run
+    concurrently on separate streams; each stays bit-exact."""
+    import torch
+
+    jobs = [synth.config("cfg4_38", trials=500)[0], synth.config("cfg5", trials=500)[0],
+            synth.config("cfg2", trials=500)[3]]
+    sims = [zs.Simulation(j.workload, j.cells, j.trials, j.recurrences).load_profile() for j in jobs]
+    streams = [torch.cuda.Stream() for _ in jobs]
+    for sm, st in zip(sims, streams):
+        sm.run(st)
+    for sm, j in zip(sims, jobs):
+        g = sm.results(want=["digest", "tot_cost", "tot_energy", "tot_time", "n_stop", "final_arm",
+                             "curves", "counters"])
+        compare_cell(oracle, g, j.workload, j.cells[0], 0, np.arange(j.trials), j.recurrences,
+                     j.trials)
+        sm.close()

@@ -172,13 +172,15 @@ void normal_pair(uint64_t seed, int64_t trial, int32_t t, int32_t k, double *z0,
 }
 
 // Which of the K recorded seeds a run replays (Q15 / NC-3).
+// One Philox block serves the replica draws of four consecutive recurrences:
+// counter (t >> 2, 2 << 24, trial), word t & 3.
 uint32_t replica(uint64_t seed, int64_t trial, int32_t t, int32_t K) {
-  uint32_t ctr[4] = {(uint32_t)t, 0x02000000u, (uint32_t)(uint64_t)trial,
+  uint32_t ctr[4] = {(uint32_t)t >> 2, 0x02000000u, (uint32_t)(uint64_t)trial,
                      (uint32_t)((uint64_t)trial >> 32)};
   uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
   uint32_t x[4];
   philox(ctr, key, x);
-  return (uint32_t)(((uint64_t)x[0] * (uint64_t)(uint32_t)K) >> 32);
+  return (uint32_t)(((uint64_t)x[t & 3] * (uint64_t)(uint32_t)K) >> 32);
 }
 
 // ---------------------------------------------------------------- Observe (Alg. 2)
@@ -220,8 +222,9 @@ bool observe(Arm &a, double x, int32_t window, const Prior &pr, double *s2_out, 
   int64_t n = (int64_t)a.window.size();
   if (n < 2) return false;
   double dn = (double)n;
-  double inv_n = 1.0 / dn;
-  double inv_nm1 = 1.0 / (dn - 1.0);
+  double rq = 1.0 / (dn * (dn - 1.0));                      // 1/n and 1/(n-1) from one division
+  double inv_n = (dn - 1.0) * rq;
+  double inv_nm1 = dn * rq;
   double mean = a.sh + a.S1 * inv_n;
   double s2 = (a.S2 - a.S1 * (a.S1 * inv_n)) * inv_nm1;     // σ̃² = Var(C_b), n-1 divisor
   double fl = 1e-12 * (1.0 + mean * mean);
@@ -229,9 +232,10 @@ bool observe(Arm &a, double x, int32_t window, const Prior &pr, double *s2_out, 
   // Alg. 2: σ̂² = (1/σ̂0² + |C_b|/σ̃²)^-1 and μ̂ = σ̂²(μ̂0/σ̂0² + Sum(C_b)/σ̃²), written
   // with both numerator and denominator multiplied by σ̃² (NC-6)
   double den = (pr.prec0 * s2) + dn;
+  double rden = 1.0 / den;
   double sum = (dn * a.sh) + a.S1;                           // Sum(C_b)
-  double var = s2 / den;
-  a.mu = ((pr.pm0 * s2) + sum) / den;
+  double var = s2 * rden;
+  a.mu = ((pr.pm0 * s2) + sum) * rden;
   a.sigma = std::sqrt(var);
   if (s2_out) *s2_out = s2;
   if (var_out) *var_out = var;

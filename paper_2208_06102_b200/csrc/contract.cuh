@@ -187,12 +187,15 @@ __device__ __forceinline__ void normal_pair(uint32_t key0, uint32_t key1, int64_
   z1 = r * s;
 }
 
-// Replica index of the run replayed at (trial, t) (NC-3).
-__device__ __forceinline__ uint32_t replica(uint32_t key0, uint32_t key1, int64_t trial, int t,
-                                            uint32_t K) {
-  const U4 x = philox4x32_10(U4{(uint32_t)t, 0x02000000u, (uint32_t)trial,
-                                (uint32_t)((uint64_t)trial >> 32)}, key0, key1);
-  return __umulhi(x.x, K);
+// Replica draws (NC-3): one Philox block per four recurrences, counter
+// (t >> 2, 2 << 24, trial); recurrence t uses word t & 3 and replica = (word * K) >> 32.
+__device__ __forceinline__ U4 replica_words(uint32_t key0, uint32_t key1, int64_t trial, int t) {
+  return philox4x32_10(U4{(uint32_t)t >> 2, 0x02000000u, (uint32_t)trial,
+                          (uint32_t)((uint64_t)trial >> 32)}, key0, key1);
+}
+__device__ __forceinline__ uint32_t pick_word(const U4 &w, int t) {
+  const int q = t & 3;
+  return q == 0 ? w.x : q == 1 ? w.y : q == 2 ? w.z : w.w;
 }
 
 }  // namespace zs

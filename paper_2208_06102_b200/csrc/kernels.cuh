@@ -262,18 +262,20 @@ enum : int { kStart = 0, kDown = 1, kUp = 2 };
 __device__ __forceinline__ double2 posterior(double sh, double S1, double S2, int n, double prec0,
                                              double pm0) {
   const double dn = (double)n;
-  const double inv_n = 1.0 / dn;                         // the two reciprocals are
-  const double inv_nm1 = 1.0 / (dn - 1.0);               // independent: latency of one
+  const double rq = 1.0 / (dn * (dn - 1.0));             // 1/n and 1/(n-1) from one division
+  const double inv_n = (dn - 1.0) * rq;
+  const double inv_nm1 = dn * rq;
   const double mean = sh + S1 * inv_n;
   double s2 = (S2 - S1 * (S1 * inv_n)) * inv_nm1;        // σ̃² = Var(C_b), n-1 divisor
   const double fl = cst::kVarFloor * (1.0 + mean * mean);
   if (!(s2 >= fl)) s2 = fl;                              // zero-variance floor (R-Q7)
   // σ̂² = (1/σ̂0² + n/σ̃²)^-1 = σ̃²/(σ̃²/σ̂0² + n);  μ̂ = σ̂²(μ̂0/σ̂0² + Sum/σ̃²)
-  // = (σ̃² μ̂0/σ̂0² + Sum)/(σ̃²/σ̂0² + n): two independent divisions by one denominator
+  // = (σ̃² μ̂0/σ̂0² + Sum)/(σ̃²/σ̂0² + n): one reciprocal of the shared denominator
   const double den = (prec0 * s2) + dn;
+  const double rden = 1.0 / den;
   const double sum = (dn * sh) + S1;                     // Sum(C_b)
-  const double var = s2 / den;
-  return make_double2(((pm0 * s2) + sum) / den, sqrt(var));
+  const double var = s2 * rden;
+  return make_double2(((pm0 * s2) + sum) * rden, sqrt(var));
 }
 
 __device__ __forceinline__ uint32_t below_mask(int c) { return c <= 0 ? 0u : ((1u << c) - 1u); }
@@ -382,6 +384,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const int t_begin = PHASE == 2 ? a.t_split : 0;
   const int t_end = PHASE == 1 ? a.t_split : R;
   int s = 0;                                                // slice of t = floor(t*S/R) (R-Q19)
+  U4 rw{0u, 0u, 0u, 0u};
   for (int t = t_begin; t < t_end; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0;
@@ -394,10 +397,9 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     if (S > 1)                                              // no 64-bit division per decision
       while ((long long)(s + 1) * R <= (long long)t * S) ++s;
     if (active) {
-#if ZS_HOIST_REPLICA
-      // step 3's replica draw depends only on (trial, t): issue it ahead of the sampling
-      const uint32_t r = replica(cp.key0, cp.key1, trial, t, (uint32_t)K);
-#endif
+      // step 3's replica words: one Philox block per four recurrences (NC-3), refreshed when
+      // t enters a new block of four; warp-uniform because all lanes share t
+      if ((t & 3) == 0 || t == t_begin) rw = replica_words(cp.key0, cp.key1, trial, t);
       // ---------------- step 2: decide b_t
       const bool ts_dec = in_ts;
       if (PHASE != 2 && !in_ts) {
@@ -482,9 +484,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       q = st[b];
       const ArmConst ac = arm[b];
       // ---------------- step 3: replay one recorded run
-#if !ZS_HOIST_REPLICA
-      const uint32_t r = replica(cp.key0, cp.key1, trial, t, (uint32_t)K);
-#endif
+      const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
       const int E = pool[((size_t)s * B + b) * K + r];
       const int Erun = E > 0 ? E : a.max_epochs;
       double c0, t0, e0;
@@ -703,6 +703,7 @@ __global__ void __launch_bounds__(128) baseline_kernel(BaselineArgs a) {
   double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
   const ArmConst *arms = a.arms + (size_t)cell * B;
   bool exploring = cp.policy == 2;
+  U4 rw{0u, 0u, 0u, 0u};
   int gb = 0, gp = 0;
   double best_c = __longlong_as_double(0x7ff0000000000000ll);
   int best_b = -1, best_p = -1;
@@ -723,7 +724,8 @@ __global__ void __launch_bounds__(128) baseline_kernel(BaselineArgs a) {
       const double Ab = __ldg(a.A + (size_t)b * P + p), Thb = __ldg(a.Th + (size_t)b * P + p);
       const double c = ((cp.eta * Ab) + ((1.0 - cp.eta) * a.MP)) / Thb;
       const double tt = 1.0 / Thb, e = Ab / Thb;
-      const uint32_t r = replica(cp.key0, cp.key1, trial, t, (uint32_t)K);
+      if ((t & 3) == 0) rw = replica_words(cp.key0, cp.key1, trial, t);
+      const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
       const int E = __ldg(a.pool + ((size_t)s * B + b) * K + r);
       const int Erun = E > 0 ? E : a.max_epochs;
       const double em1 = (double)(Erun - 1);

@@ -35,19 +35,23 @@ extern "C" __global__ void probe_observe(const double *in, double *out, const in
   const double d = C - sh;
   S1 = S1 + d; S2 = S2 + d * d;
   const double dn = (double)n;
-  const double inv_n = 1.0 / dn;
-  const double inv_nm1 = 1.0 / (dn - 1.0);
+  const double rq = 1.0 / (dn * (dn - 1.0));
+  const double inv_n = (dn - 1.0) * rq;
+  const double inv_nm1 = dn * rq;
   const double mean = sh + S1 * inv_n;
   double s2 = (S2 - S1 * (S1 * inv_n)) * inv_nm1;
   const double fl = 1e-12 * (1.0 + mean * mean);
   if (!(s2 >= fl)) s2 = fl;
   const double den = (in[4] * s2) + dn;
+  const double rden = 1.0 / den;
   const double sum = (dn * sh) + S1;
-  out[0] = ((in[5] * s2) + sum) / den; out[1] = sqrt(s2 / den); out[2] = S1; out[3] = S2;
+  out[0] = ((in[5] * s2) + sum) * rden; out[1] = sqrt(s2 * rden); out[2] = S1; out[3] = S2;
 }
 // trace lookup + charge + early-stop test (NC-5), not-stopped path
-extern "C" __global__ void probe_charge(const double *in, const int *pool, double *out, long long trial, int t) {
-  const uint32_t r = replica(1u, 2u, trial, t, 4u);
+// (the replica Philox block is amortised over four recurrences: counted separately as philox/4)
+extern "C" __global__ void probe_charge(const double *in, const int *pool, double *out, const uint4 *w, int t) {
+  const uint4 ww = *w;
+  const uint32_t r = __umulhi(pick_word(U4{ww.x, ww.y, ww.z, ww.w}, t), 4u);
   const int E = pool[r];
   const int Erun = E > 0 ? E : 99;
   const double em1 = (double)(Erun - 1);

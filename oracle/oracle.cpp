@@ -67,7 +67,7 @@ void philox(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
 // branches (|f| < 2^-20, k == 0, and the alternative form used near sqrt(2)/2..
 // sqrt(2) boundaries) are all folded into this one formula, and the two
 // polynomial halves are evaluated with explicit fma.
-double zlog(double x) {
+double zlog_fdlibm(double x) {
   const double ln2_hi = 6.93147180369123816490e-01;  // 3fe62e42 fee00000
   const double ln2_lo = 1.90821492927058770002e-10;  // 3dea39ef 35793c76
   const double Lg1 = 6.666666666666735130e-01;       // 3FE55555 55555593
@@ -93,6 +93,47 @@ double zlog(double x) {
   double R = t2 + t1;
   double dk = (double)k;
   return dk * ln2_hi - ((hfsq - (s * (hfsq + R) + dk * ln2_lo)) - f);
+}
+
+// The sampler's log (NC-3): table-driven, no division on the per-normal path.
+// x = 2^k m with m in [sqrt2/2, sqrt2) (fdlibm's normalisation), j = round(128 (m - 1)),
+// c_j = 1 + j/128, invc_j = 1/c_j (IEEE), logc_j = -zlog_fdlibm(invc_j) = log(1/invc_j);
+// r = fma(m, invc_j, -1) (|r| < 0.0056), log1p(r) by its Taylor series to r^7 (truncation
+// < 2e-19 relative), log x = (k ln2_hi + logc_j) + (r + (k ln2_lo + r^2 q(r))).
+struct LogTable {
+  double invc[91], logc[91];
+  LogTable() {
+    for (int j = -37; j <= 53; ++j) {
+      const double c = 1.0 + (double)j / 128.0;
+      invc[j + 37] = 1.0 / c;
+      logc[j + 37] = -zlog_fdlibm(invc[j + 37]);
+    }
+  }
+};
+
+double zlog(double x) {
+  static const LogTable T;
+  const double ln2_hi = 6.93147180369123816490e-01;
+  const double ln2_lo = 1.90821492927058770002e-10;
+  const double C3 = 1.0 / 3.0, C5 = 0.2, C6 = -1.0 / 6.0, C7 = 1.0 / 7.0;
+  int32_t hx = high_word(x);
+  int32_t k = (hx >> 20) - 1023;
+  hx &= 0x000fffff;
+  int32_t i = (hx + 0x95f64) & 0x100000;
+  const double m = with_high_word(x, hx | (i ^ 0x3ff00000));
+  k += (i >> 20);
+  const double f = m - 1.0;                                  // exact
+  const int j = (int)std::nearbyint(f * 128.0);              // round half to even
+  const double r = std::fma(m, T.invc[j + 37], -1.0);
+  double q = std::fma(r, C7, C6);
+  q = std::fma(r, q, C5);
+  q = std::fma(r, q, -0.25);
+  q = std::fma(r, q, C3);
+  q = std::fma(r, q, -0.5);
+  const double dk = (double)k;
+  const double hi = std::fma(dk, ln2_hi, T.logc[j + 37]);
+  const double lo = std::fma(dk, ln2_lo, (r * r) * q);
+  return hi + (r + lo);
 }
 
 // ---------------------------------------------------------------- sin / cos of pi*x
@@ -698,6 +739,7 @@ void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t
   philox(ctr, key, out);
 }
 double oracle_zlog(double x) { return zlog(x); }
+double oracle_zlog_fdlibm(double x) { return zlog_fdlibm(x); }
 void oracle_zsincospi(uint64_t m52, double *s, double *c) { zsincospi(m52, s, c); }
 void oracle_uniforms(uint64_t w0, uint64_t w1, double *u1, double *v) { uniforms(w0, w1, u1, v); }
 void oracle_normal_pair(uint64_t seed, int64_t trial, int32_t t, int32_t k, double *z0, double *z1) {

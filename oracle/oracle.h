@@ -79,6 +79,7 @@ int oracle_replay(const oracle_trace *tr, const oracle_cell *cell, int32_t recur
 /* primitives, exposed for the pins */
 void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 double oracle_zlog(double x);
+double oracle_zlog_fdlibm(double x);
 void oracle_zsincospi(uint64_t m52, double *s, double *c);
 void oracle_uniforms(uint64_t w0, uint64_t w1, double *u1, double *v);
 void oracle_normal_pair(uint64_t seed, int64_t trial, int32_t t, int32_t k, double *z0, double *z1);

@@ -105,6 +105,8 @@ def lib():
         L.oracle_philox4x32_10.argtypes = [C.POINTER(C.c_uint32)] * 3
         L.oracle_zlog.argtypes = [C.c_double]
         L.oracle_zlog.restype = C.c_double
+        L.oracle_zlog_fdlibm.argtypes = [C.c_double]
+        L.oracle_zlog_fdlibm.restype = C.c_double
         L.oracle_zsincospi.argtypes = [C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.oracle_uniforms.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.oracle_normal_pair.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32,
@@ -210,6 +212,10 @@ def philox(ctr, key):
 
 def zlog(x):
     return lib().oracle_zlog(float(x))
+
+
+def zlog_fdlibm(x):
+    return lib().oracle_zlog_fdlibm(float(x))
 
 
 def zsincospi(m52):

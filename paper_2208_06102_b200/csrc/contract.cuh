@@ -48,6 +48,10 @@ ZS_C(kC7, -0x1.b6e24f44b128fp-14);
 ZS_C(kC8, 0x1.20c62c2f2d7f5p-18);
 ZS_C(kC9, -0x1.2a0c591af8314p-23);
 ZS_C(kTwoM51, 0x1p-51);
+ZS_C(kL3, 1.0 / 3.0);   // log1p Taylor coefficients, rounded to nearest
+ZS_C(kL5, 0.2);
+ZS_C(kL6, -1.0 / 6.0);
+ZS_C(kL7, 1.0 / 7.0);
 ZS_C(kVarFloor, 1e-12);
 }  // namespace cst
 
@@ -71,7 +75,7 @@ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
 // ------------------------------------------------------------ zlog
 // fdlibm __ieee754_log for positive normal x, one formula for every f (the
 // shortcut branches folded in), polynomial halves by explicit fma (NC-3).
-__device__ __forceinline__ double zlog(double x) {
+__device__ __forceinline__ double zlog_fdlibm(double x) {
   using namespace cst;
   int hx = __double2hiint(x);
   const int lx = __double2loint(x);
@@ -90,6 +94,36 @@ __device__ __forceinline__ double zlog(double x) {
   const double R = t2 + t1;
   const double dk = (double)k;
   return dk * kLn2Hi - ((hfsq - (s * (hfsq + R) + dk * kLn2Lo)) - f);
+}
+
+// The sampler's log (NC-3): table-driven, no division per normal.  tab[j + 37] =
+// (invc_j, logc_j) for j in [-37, 53]: c_j = 1 + j/128, invc_j = 1/c_j (IEEE),
+// logc_j = -zlog_fdlibm(invc_j) (built once on the device by log_table_kernel).
+// x = 2^k m, m in [sqrt2/2, sqrt2); j = round(128 (m - 1)); r = fma(m, invc_j, -1);
+// log x = (k ln2_hi + logc_j) + (r + (k ln2_lo + r^2 q(r))), q the log1p Taylor tail to r^7.
+constexpr int kLogTab = 91;
+__device__ __forceinline__ double zlog(double x, const double2 *__restrict__ tab) {
+  using namespace cst;
+  int hx = __double2hiint(x);
+  const int lx = __double2loint(x);
+  int k = (hx >> 20) - 1023;
+  hx &= 0x000fffff;
+  const int i0 = (hx + 0x95f64) & 0x100000;
+  const double m = __hiloint2double(hx | (i0 ^ 0x3ff00000), lx);
+  k += (i0 >> 20);
+  const double f = m - 1.0;                                  // exact
+  const int j = __double2int_rn(f * 128.0);                  // round half to even
+  const double2 e = tab[j + 37];
+  const double r = fma(m, e.x, -1.0);
+  double q = fma(r, kL7, kL6);
+  q = fma(r, q, kL5);
+  q = fma(r, q, -0.25);
+  q = fma(r, q, kL3);
+  q = fma(r, q, -0.5);
+  const double dk = (double)k;
+  const double hi = fma(dk, kLn2Hi, e.y);
+  const double lo = fma(dk, kLn2Lo, (r * r) * q);
+  return hi + (r + lo);
 }
 
 // ------------------------------------------------------------ sin / cos of pi*m/2^51
@@ -128,37 +162,18 @@ __device__ __forceinline__ void zsincospi(uint64_t m, double &s, double &c) {
   c = ((q + 1) & 2) ? -cc : cc;           // q=0: cf  1: -sf 2: -cf  3: sf
 }
 
-// Philox with the 10 round keys precomputed (the key is per cell, so the
-// schedule is hoisted out of the replay loop).
-struct RoundKeys { uint32_t k0[10], k1[10]; };
-__device__ __forceinline__ RoundKeys round_keys(uint32_t k0, uint32_t k1) {
-  RoundKeys r;
-#pragma unroll
-  for (int i = 0; i < 10; ++i) { r.k0[i] = k0; r.k1[i] = k1; k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
-  return r;
-}
-__device__ __forceinline__ U4 philox4x32_10(U4 c, const RoundKeys &rk) {
-  constexpr uint32_t kMul0 = 0xD2511F53u, kMul1 = 0xCD9E8D57u;
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(kMul0, c.x), lo0 = kMul0 * c.x;
-    const uint32_t hi1 = __umulhi(kMul1, c.z), lo1 = kMul1 * c.z;
-    c = U4{hi1 ^ c.y ^ rk.k0[r], lo1, hi0 ^ c.w ^ rk.k1[r], lo0};
-  }
-  return c;
-}
-
 // The 128 random bits of arm pair k of `trial` at recurrence t, and the
 // Box-Muller transform of them (NC-3); normal_pair = both.
 __device__ __forceinline__ U4 pair_words(uint32_t key0, uint32_t key1, int64_t trial, int t, int k) {
   return philox4x32_10(U4{(uint32_t)t, 0x01000000u | (uint32_t)k, (uint32_t)trial,
                           (uint32_t)((uint64_t)trial >> 32)}, key0, key1);
 }
-__device__ __forceinline__ void box_muller(const U4 x, double &z0, double &z1) {
+__device__ __forceinline__ void box_muller(const U4 x, double &z0, double &z1,
+                                           const double2 *__restrict__ logtab) {
   const uint64_t w0 = ((uint64_t)x.y << 32) | x.x;
   const uint64_t w1 = ((uint64_t)x.w << 32) | x.z;
   const double u1 = 2.0 - __longlong_as_double((long long)(0x3FF0000000000000ull | (w0 >> 12)));
-  const double r = sqrt(-2.0 * zlog(u1));
+  const double r = sqrt(-2.0 * zlog(u1, logtab));
   double s, c;
   zsincospi(w1 >> 12, s, c);
   z0 = r * c;
@@ -166,25 +181,19 @@ __device__ __forceinline__ void box_muller(const U4 x, double &z0, double &z1) {
 }
 
 // Box-Muller pair for arms (2k, 2k+1) of `trial` at recurrence t (NC-3).
-#ifdef ZS_ROUND_KEYS
-__device__ __forceinline__ void normal_pair(const RoundKeys &key, int64_t trial, int t, int k,
-                                            double &z0, double &z1) {
-  const U4 x = philox4x32_10(U4{(uint32_t)t, 0x01000000u | (uint32_t)k, (uint32_t)trial,
-                                (uint32_t)((uint64_t)trial >> 32)}, key);
-#else
 __device__ __forceinline__ void normal_pair(uint32_t key0, uint32_t key1, int64_t trial, int t,
-                                            int k, double &z0, double &z1) {
-  const U4 x = philox4x32_10(U4{(uint32_t)t, 0x01000000u | (uint32_t)k, (uint32_t)trial,
-                                (uint32_t)((uint64_t)trial >> 32)}, key0, key1);
-#endif
-  const uint64_t w0 = ((uint64_t)x.y << 32) | x.x;
-  const uint64_t w1 = ((uint64_t)x.w << 32) | x.z;
-  const double u1 = 2.0 - __longlong_as_double((long long)(0x3FF0000000000000ull | (w0 >> 12)));
-  const double r = sqrt(-2.0 * zlog(u1));
-  double s, c;
-  zsincospi(w1 >> 12, s, c);
-  z0 = r * c;
-  z1 = r * s;
+                                            int k, double &z0, double &z1,
+                                            const double2 *__restrict__ logtab) {
+  box_muller(pair_words(key0, key1, trial, t, k), z0, z1, logtab);
+}
+
+// log_table_kernel: the zlog table (one block; entries j = -37..53)
+__global__ void log_table_kernel(double2 *tab) {
+  const int i = threadIdx.x;
+  if (i >= kLogTab) return;
+  const double c = 1.0 + (double)(i - 37) / 128.0;
+  const double invc = 1.0 / c;
+  tab[i] = make_double2(invc, -zlog_fdlibm(invc));
 }
 
 // Replica draws (NC-3): one Philox block per four recurrences, counter

@@ -158,6 +158,7 @@ struct ReplayArgs {
   int32_t *perm;                  // [stride] phase-B lane -> trial (within each cell's block)
   int32_t *bucket;                // [cells][nwin][kBuckets] histogram, then running offsets
   int nwin;                       // regroup windows per cell
+  const double2 *logtab;          // [kLogTab] the sampler's log table (NC-3)
 };
 
 constexpr int kBuckets = 17;      // popcount of the survivor-pair mask, 0..16
@@ -182,14 +183,15 @@ struct Carry {
 
 // shared-memory table region of one block: [ArmConst B][regret S*B][opt_arm S][pool S*B*K]
 struct TabLayout {
-  int arms, regret, optarm, pool, bytes;
+  int arms, regret, optarm, pool, logtab, bytes;
   __host__ __device__ static int align16(int x) { return (x + 15) & ~15; }
   __host__ __device__ TabLayout(int B, int S, int K) {
     arms = 0;
     regret = align16(arms + B * (int)sizeof(ArmConst));
     optarm = align16(regret + S * B * 8);
     pool = align16(optarm + S * 4);
-    bytes = align16(pool + S * B * K * 4);
+    logtab = align16(pool + S * B * K * 4);
+    bytes = logtab + kLogTab * 16;
   }
 };
 
@@ -320,7 +322,8 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     // bulk copies need 16-byte sizes; the host pads every table to 16 B
     const uint32_t p_arm = (b_arm + 15u) & ~15u, p_reg = (b_reg + 15u) & ~15u;
     const uint32_t p_opt = (b_opt + 15u) & ~15u, p_pool = (b_pool + 15u) & ~15u;
-    mbar_expect_tx(&mbar, p_arm + p_reg + p_opt + p_pool);
+    mbar_expect_tx(&mbar, p_arm + p_reg + p_opt + p_pool + kLogTab * 16u);
+    tma_bulk_load(smem + L.logtab, a.logtab, kLogTab * 16u, &mbar);
     tma_bulk_load(smem + L.arms, a.arms + (size_t)cell * a.B, p_arm, &mbar);
     tma_bulk_load(smem + L.regret, a.regret + (size_t)cell * a.reg_stride, p_reg, &mbar);
     tma_bulk_load(smem + L.optarm, a.opt_arm + (size_t)cell * a.opt_stride, p_opt, &mbar);
@@ -333,6 +336,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const double *regret = reinterpret_cast<const double *>(smem + L.regret);
   const int32_t *optarm = reinterpret_cast<const int32_t *>(smem + L.optarm);
   const int32_t *pool = reinterpret_cast<const int32_t *>(smem + L.pool);
+  const double2 *logtab = reinterpret_cast<const double2 *>(smem + L.logtab);
   const int B = a.B, R = a.R, S = a.S, K = a.K;
   double2 *s_ms = reinterpret_cast<double2 *>(smem + a.tab_bytes);   // [arm][thread] (mu, sigma)
 
@@ -345,12 +349,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
   double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-#ifdef ZS_ROUND_KEYS
-  const RoundKeys rkeys = round_keys(cp.key0, cp.key1);
-#define ZS_KEYARG rkeys
-#else
 #define ZS_KEYARG cp.key0, cp.key1
-#endif
 
   uint32_t profiled = 0, seen = 0, mature = 0;              // bit a: profiled / observed / n_a >= 2
   double best = kInf;                                       // min_t C_t
@@ -439,8 +438,8 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
               const int k1 = __ffs(pm) - 1;
               pm &= pm - 1u;
               double z00, z01, z10, z11;
-              normal_pair(ZS_KEYARG, trial, t, k0, z00, z01);
-              normal_pair(ZS_KEYARG, trial, t, k1, z10, z11);
+              normal_pair(ZS_KEYARG, trial, t, k0, z00, z01, logtab);
+              normal_pair(ZS_KEYARG, trial, t, k1, z10, z11, logtab);
               consider(k0, z00, z01);
               consider(k1, z10, z11);
             }
@@ -462,7 +461,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
                 xn = pair_words(cp.key0, cp.key1, trial, t, k);
               }
               double z0, z1;
-              box_muller(xc, z0, z1);
+              box_muller(xc, z0, z1, logtab);
               consider(kc, z0, z1);
               if (!more) break;
             }
@@ -472,7 +471,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             const int k = __ffs(pm) - 1;
             pm &= pm - 1u;
             double z0, z1;
-            normal_pair(ZS_KEYARG, trial, t, k, z0, z1);
+            normal_pair(ZS_KEYARG, trial, t, k, z0, z1, logtab);
             consider(k, z0, z1);
           }
 #endif

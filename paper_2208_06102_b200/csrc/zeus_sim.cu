@@ -59,7 +59,7 @@ struct zeus_sim {
   // device memory
   DevBuf d_A, d_Th, d_pool, d_cells, d_arms, d_regret, d_opt, d_optarm;
   DevBuf d_slots, d_curves, d_tot_cost, d_tot_energy, d_tot_time, d_digest, d_nstop, d_final,
-      d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket, d_ebar;
+      d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket, d_ebar, d_logtab;
   ~zeus_sim() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -283,7 +283,8 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
       (e = s->d_st_ring.alloc(n * s->B * (size_t)s->wmax * 8)) != cudaSuccess ||
       (e = s->d_carry.alloc(n * sizeof(zs::Carry))) != cudaSuccess ||
       (e = s->d_perm.alloc(n * 4)) != cudaSuccess ||
-      (e = s->d_bucket.alloc((size_t)num_cells * s->nwin * zs::kBuckets * 4)) != cudaSuccess) {
+      (e = s->d_bucket.alloc((size_t)num_cells * s->nwin * zs::kBuckets * 4)) != cudaSuccess ||
+      (e = s->d_logtab.alloc(zs::kLogTab * sizeof(double2))) != cudaSuccess) {
     std::string m = std::string("device allocation: ") + cudaGetErrorString(e);
     delete s;
     return fail(nullptr, e == cudaErrorMemoryAllocation ? ZEUS_E_NOMEM : ZEUS_E_CUDA, m);
@@ -293,6 +294,12 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
       (e = cudaEventCreate(&s->ev0)) != cudaSuccess || (e = cudaEventCreate(&s->ev1)) != cudaSuccess ||
       (e = cudaEventCreate(&s->ev2)) != cudaSuccess || (e = cudaEventCreate(&s->ev3)) != cudaSuccess) {
     std::string m = std::string("create: ") + cudaGetErrorString(e);
+    delete s;
+    return fail(nullptr, ZEUS_E_CUDA, m);
+  }
+  zs::log_table_kernel<<<1, 128>>>(s->d_logtab.as<double2>());   // the sampler's log table
+  if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
+    std::string m = std::string("log table: ") + cudaGetErrorString(e);
     delete s;
     return fail(nullptr, ZEUS_E_CUDA, m);
   }
@@ -369,11 +376,14 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   const int wmax = s->wmax;
   const size_t per_thread = (size_t)((B + 1) & ~1) * 16;   // (mu, sigma) per arm
   int best_warps = -1;
+  // sized for the kernel that dominates: the Thompson phase when the schedule has two
+  // phases (R > 2B), else the one-pass kernel; ties keep the larger block (fewer stagings)
+  const bool two_phase = s->layout != 1 && std::min(s->R, 2 * B) < s->R;
   for (int tpb : {128, 64, 32}) {
     const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
     if (bytes > 227 * 1024) continue;
     int blocks = 0;
-    const void *fn = (const void *)replay_fn(wmax > 0, false, 0);
+    const void *fn = (const void *)replay_fn(wmax > 0, false, two_phase ? 2 : 0);
     int granted = 0;
     ZS_CUDA(s, grant_max_smem(fn, s->device, &granted));
     if ((int)bytes > granted) continue;
@@ -467,6 +477,7 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     a.perm = s->d_perm.as<int32_t>();
     a.bucket = s->d_bucket.as<int32_t>();
     a.nwin = s->nwin;
+    a.logtab = s->d_logtab.as<double2>();
     const bool two_phase = s->layout != 1 && a.t_split < s->R;
     if (!two_phase) {
       replay_fn(windowed, s->log_mode, 0)<<<grid, s->tpb, s->smem_bytes, st>>>(a);

@@ -10,14 +10,14 @@ extern "C" __global__ void probe_philox(const uint32_t *in, uint32_t *out) {
   U4 x = philox4x32_10(U4{in[0], in[1], in[2], in[3]}, in[4], in[5]);
   out[0] = x.x; out[1] = x.y; out[2] = x.z; out[3] = x.w;
 }
-extern "C" __global__ void probe_zlog(const double *in, double *out) { out[0] = zlog(in[0]); }
+extern "C" __global__ void probe_zlog(const double *in, double *out, const double2 *tab) { out[0] = zlog(in[0], tab); }
 extern "C" __global__ void probe_sincospi(const unsigned long long *in, double *out) {
   double s, c; zsincospi(in[0], s, c); out[0] = s; out[1] = c;
 }
 extern "C" __global__ void probe_sqrt(const double *in, double *out) { out[0] = sqrt(in[0]); }
 extern "C" __global__ void probe_div(const double *in, double *out) { out[0] = in[0] / in[1]; }
-extern "C" __global__ void probe_pair(const long long *in, double *out) {
-  double z0, z1; normal_pair((uint32_t)in[0], (uint32_t)in[1], in[2], (int)in[3], (int)in[4], z0, z1);
+extern "C" __global__ void probe_pair(const long long *in, double *out, const double2 *tab) {
+  double z0, z1; normal_pair((uint32_t)in[0], (uint32_t)in[1], in[2], (int)in[3], (int)in[4], z0, z1, tab);
   out[0] = z0; out[1] = z1;
 }
 // theta = fma(sigma, z, mu) + strict-< argmin update (NC-4), per normal used

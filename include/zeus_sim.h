@@ -83,7 +83,13 @@ typedef struct {
   int64_t trials;                    /* global trial count of this cell, >= 0 */
   int32_t policy;                    /* ZEUS_POLICY_*: Zeus, or one of the paper's baselines
                                         replayed on the same traces and replica draws */
+  int32_t ablation;                  /* Zeus only: ZEUS_ABLATE_* bits; "no early
+                                        stopping" is beta = +INFINITY */
 } zeus_cell;
+
+#define ZEUS_ABLATE_PRUNING 1       /* keep every batch size: Alg. 3 still walks, 𝓑 is not pruned */
+#define ZEUS_ABLATE_JIT 2           /* no JIT profiler: the first |𝓟| runs of each batch size try
+                                       the power limits in ascending order, one per recurrence */
 
 /* policies (§6.1 "Baselines"; DESIGN.md R-Q29) */
 #define ZEUS_POLICY_ZEUS 0          /* Alg. 3 pruning + Alg. 1/2 Thompson sampling, Eq. 7 p*, early stop */
@@ -128,6 +134,9 @@ typedef struct {
   /* known optimum per slice [cells][S] */
   double *opt_cost;
   int32_t *opt_arm;
+  /* Pareto front of each slice's (TTA, ETA) grid [S][B][P] (§2.3; the traces'
+     property, the same for every cell): 1 = non-dominated, TTA = Ebar/Th, ETA = Ebar*A/Th */
+  uint8_t *pareto;
   /* per-decision log [cells][shard][R] (needs log_mode = 1):
      arm | p_index << 8 | flags << 16, flags bit0 stopped, bit1 converged,
      bit2 paid the profiling epoch, bit3 decided by Thompson sampling */

@@ -381,6 +381,7 @@ std::string validate(const oracle_trace &tr, const oracle_cell &cell) {
   if (!(cell.prior_var > 0.0)) add("prior variance must be > 0");
   if (!std::isfinite(cell.prior_mean)) add("prior mean not finite");
   if (cell.policy < 0 || cell.policy > 2) add("policy must be 0 (Zeus), 1 (Default) or 2 (Grid Search)");
+  if (cell.ablation < 0 || cell.ablation > 3) add("ablation must be a subset of {1 no pruning, 2 no JIT}");
   if (B >= 1 && P >= 1 && B <= 32 && P <= 64) {
     for (int i = 0; i < B * P; ++i)
       if (!(tr.avg_power_w[i] > 0.0) || !std::isfinite(tr.avg_power_w[i])) { add("average power not positive"); break; }
@@ -508,7 +509,8 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
   bool in_ts = false;
   int round = 1;
   Step step = START;
-  uint32_t cand = (B == 32) ? 0xffffffffu : ((1u << B) - 1u);
+  const uint32_t all_arms = (B == 32) ? 0xffffffffu : ((1u << B) - 1u);
+  uint32_t cand = all_arms;
   int start = tr.default_bs_index;
   int cursor = start;
   uint32_t surv = 0, ts_set = 0;
@@ -552,23 +554,32 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
       }
     }
     // ---- step 1 result: the power limit accompanying b
-    const int p = T.pstar[b];
+    // ---- step 1 result: the power limit accompanying b.  Ablation "no JIT
+    // profiling": the first P runs of b try the power limits in ascending
+    // order, one per recurrence, each at its own per-epoch cost; then p*(b).
+    int p = T.pstar[b];
+    double c1b = T.c1[b], t1b = T.t1[b], e1b = T.e1[b];
+    const bool no_jit = (cell.ablation & 2) != 0;
+    if (no_jit && arm[b].cnt < tr.num_power_limits) {
+      p = (int)arm[b].cnt;
+      epoch_cost(tr, cell, b, p, &c1b, &t1b, &e1b);
+    }
     // ---- step 3: replay one recorded run of b
     const uint32_t r = replica(cell.seed, trial, t, K);
     const int32_t E = tr.epochs_to_target[((size_t)s * B + b) * K + r];
     const int32_t E_run = E > 0 ? E : tr.max_epochs;
     double c0, t0, e0;
     bool profiled_now = false;
-    if (tr.charge_profiling && !arm[b].profiled) {   // JIT profiling epoch
+    if (!no_jit && tr.charge_profiling && !arm[b].profiled) {   // JIT profiling epoch
       c0 = T.cP[b]; t0 = T.tP[b]; e0 = T.eP[b]; profiled_now = true;
     } else {
-      c0 = T.c1[b]; t0 = T.t1[b]; e0 = T.e1[b];
+      c0 = c1b; t0 = t1b; e0 = e1b;
     }
     arm[b].profiled = true;
     const double em1 = (double)(E_run - 1);
-    const double C_full = c0 + em1 * T.c1[b];
-    const double T_full = t0 + em1 * T.t1[b];
-    const double En_full = e0 + em1 * T.e1[b];
+    const double C_full = c0 + em1 * c1b;
+    const double T_full = t0 + em1 * t1b;
+    const double En_full = e0 + em1 * e1b;
     // ---- step 4: early stop at β·min_t C_t
     const double thr = cell.beta * best;
     double C, Tm, En;
@@ -581,9 +592,9 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
         Tm = phi * t0;
         En = phi * e0;
       } else {
-        double phi = (thr - c0) / T.c1[b];
-        Tm = t0 + phi * T.t1[b];
-        En = e0 + phi * T.e1[b];
+        double phi = (thr - c0) / c1b;
+        Tm = t0 + phi * t1b;
+        En = e0 + phi * e1b;
       }
     } else {
       C = C_full; Tm = T_full; En = En_full;
@@ -610,7 +621,7 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
       if (end_round) {
         if (surv == 0) surv = 1u << start;           // R-Q23
         if (round == 1) {
-          cand = surv;
+          cand = (cell.ablation & 1) ? all_arms : surv;   // "no pruning" keeps 𝓑
           if (r1_arm >= 0) start = r1_arm;           // b0 <- b with smallest cost observed
           surv = 0;
           round = 2;
@@ -618,7 +629,7 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
           cursor = start;
         } else {
           in_ts = true;
-          ts_set = surv;
+          ts_set = (cell.ablation & 1) ? all_arms : surv;
         }
       }
     }
@@ -638,9 +649,10 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
       row[0] += C;
       row[1] += En;
       row[2] += Tm;
-      row[3] += T.regret[(size_t)s * B + b];
+      row[3] += (p == T.pstar[b]) ? T.regret[(size_t)s * B + b]
+                                  : T.ebar[(size_t)s * B + b] * c1b - T.opt[s];
       row[4] += stopped ? 1.0 : 0.0;
-      row[5] += (b == T.opt_arm[s]) ? 1.0 : 0.0;
+      row[5] += (b == T.opt_arm[s] && p == T.pstar[b]) ? 1.0 : 0.0;
       row[6] += ts_dec ? 1.0 : 0.0;
     }
     if (log) log[t] = (uint32_t)b | ((uint32_t)p << 8) | (flags << 16);
@@ -731,6 +743,44 @@ int oracle_replay(const oracle_trace *tr, const oracle_cell *cell, int32_t R,
       out->counters[q] = 0;
       for (int w = 0; w < threads; ++w) out->counters[q] += pc[w].c[q];
     }
+  }
+  return 0;
+}
+
+// Pareto front of the (TTA, ETA) grid of slice s (§2.3, Fig. eta-tta-tradeoff;
+// SURVEY §8(f) f4): point (b, p) has TTA = Ebar(b,s)/Th(b,p) and ETA = (Ebar(b,s)*A(b,p))/Th(b,p)
+// for every b with a converged replica; mask = 1 iff no other point has both coordinates <=
+// with one strictly <, and no earlier point in (b, p) order has identical coordinates.
+int oracle_pareto(const oracle_trace *tr, int32_t s, uint8_t *mask) {
+  const int B = tr->num_batch_sizes, P = tr->num_power_limits, K = tr->replicas;
+  if (s < 0 || s >= tr->num_slices) return 1;
+  std::vector<double> tta((size_t)B * P), eta((size_t)B * P);
+  std::vector<bool> valid((size_t)B * P, false);
+  for (int b = 0; b < B; ++b) {
+    int64_t sum = 0, cnt = 0;
+    for (int k = 0; k < K; ++k) {
+      const int32_t E = tr->epochs_to_target[((size_t)s * B + b) * K + k];
+      if (E > 0) { sum += E; ++cnt; }
+    }
+    if (cnt == 0) continue;
+    const double eb = (double)sum / (double)cnt;
+    for (int p = 0; p < P; ++p) {
+      const double A = tr->avg_power_w[(size_t)b * P + p], Th = tr->throughput_eps[(size_t)b * P + p];
+      tta[(size_t)b * P + p] = eb / Th;
+      eta[(size_t)b * P + p] = (eb * A) / Th;
+      valid[(size_t)b * P + p] = true;
+    }
+  }
+  for (int i = 0; i < B * P; ++i) {
+    bool keep = valid[i];
+    for (int j = 0; j < B * P && keep; ++j) {
+      if (j == i || !valid[j]) continue;
+      const bool le = tta[j] <= tta[i] && eta[j] <= eta[i];
+      const bool lt = tta[j] < tta[i] || eta[j] < eta[i];
+      if (le && lt) keep = false;                          // dominated
+      if (!lt && le && j < i) keep = false;               // identical, an earlier one is kept
+    }
+    mask[i] = keep ? 1 : 0;
   }
   return 0;
 }

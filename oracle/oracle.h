@@ -48,6 +48,7 @@ typedef struct {
   uint64_t seed;       /* Philox key */
   int32_t policy;      /* 0 Zeus (Alg. 3 + Alg. 1/2), 1 Default (b0, max p), 2 Grid Search
                           with pruning (§6.1) */
+  int32_t ablation;    /* Zeus ablations: bit0 no pruning, bit1 no JIT profiling */
 } oracle_cell;
 
 typedef struct {       /* step-1 tables; any pointer may be NULL */
@@ -75,6 +76,9 @@ int oracle_validate(const oracle_trace *tr, const oracle_cell *cell, char *msg, 
 int oracle_step1(const oracle_trace *tr, const oracle_cell *cell, oracle_tables *out);
 int oracle_replay(const oracle_trace *tr, const oracle_cell *cell, int32_t recurrences,
                   const int64_t *trials, int64_t n, int32_t threads, oracle_out *out);
+
+/* Pareto front of slice s's (TTA, ETA) grid: mask [B][P] (1 = on the front) */
+int oracle_pareto(const oracle_trace *tr, int32_t s, uint8_t *mask);
 
 /* primitives, exposed for the pins */
 void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

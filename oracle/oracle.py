@@ -55,6 +55,7 @@ class Cell(C.Structure):
         ("prior_var", C.c_double),
         ("seed", C.c_uint64),
         ("policy", C.c_int32),
+        ("ablation", C.c_int32),
     ]
 
 
@@ -116,6 +117,7 @@ def lib():
         L.oracle_posterior.argtypes = [C.POINTER(C.c_double), C.c_int32, C.c_int32, C.c_double,
                                        C.c_double] + [C.POINTER(C.c_double)] * 4
         L.oracle_hardware_threads.restype = C.c_int32
+        L.oracle_pareto.argtypes = [C.POINTER(Trace), C.c_int32, C.POINTER(C.c_uint8)]
         _lib = L
     return _lib
 
@@ -143,7 +145,7 @@ class _Held:
 def _cell(c):
     return Cell(float(c["eta"]), float(c["beta"]), int(c.get("window", 0)),
                 float(c.get("prior_mean", 0.0)), float(c.get("prior_var", np.inf)),
-                int(c.get("seed", 0)), int(c.get("policy", 0)))
+                int(c.get("seed", 0)), int(c.get("policy", 0)), int(c.get("ablation", 0)))
 
 
 def validate(w, c):
@@ -248,6 +250,16 @@ def posterior(xs, window=0, prior_mean=0.0, prior_var=np.inf):
     if rc != 0:
         return None
     return {"mu": mu.value, "sigma": sg.value, "s2": s2.value, "var": var.value}
+
+
+def pareto(w, s=0):
+    """Pareto-front mask [B][P] of slice s's (TTA, ETA) grid."""
+    h = _Held(w)
+    B, P = len(h.bs), len(h.pl)
+    m = np.zeros((B, P), np.uint8)
+    if lib().oracle_pareto(C.byref(h.tr), int(s), _p(m, C.c_uint8)) != 0:
+        raise ValueError("bad slice")
+    return m
 
 
 def hardware_threads():

@@ -39,6 +39,7 @@ struct ArmConst {                 // per (cell, arm), 64 B
 struct CellParam {                // per cell
   double eta, beta, prec0, pm0;
   int32_t window, policy;         // policy: 0 Zeus, 1 Default, 2 Grid Search (§6.1)
+  int32_t ablation, pad;          // Zeus ablations: bit0 no pruning, bit1 no JIT
   uint32_t key0, key1;
   int64_t begin, n, out_off;      // global first trial, shard size, offset into per-trial outputs
 };
@@ -159,6 +160,10 @@ struct ReplayArgs {
   int32_t *bucket;                // [cells][nwin][kBuckets] histogram, then running offsets
   int nwin;                       // regroup windows per cell
   const double2 *logtab;          // [kLogTab] the sampler's log table (NC-3)
+  // ablation path only (ABL): the raw profile, Ebar and the optimum for off-p* charges
+  const double *A, *Th, *ebar, *opt;
+  int P;
+  double MP;
 };
 
 constexpr int kBuckets = 17;      // popcount of the survivor-pair mask, 0..16
@@ -298,10 +303,12 @@ __device__ __forceinline__ uint32_t above_mask(int c) { return c >= 31 ? 0u : ~(
 //              set of resident trials (~30 MB) stays in L2.
 #ifdef ZS_MAXNREG
 #define ZS_REPLAY_BOUNDS __maxnreg__(ZS_MAXNREG)
+#elif defined(ZS_P2_MIN_BLOCKS)
+#define ZS_REPLAY_BOUNDS __launch_bounds__(128, (PHASE == 2 ? ZS_P2_MIN_BLOCKS : 1))
 #else
 #define ZS_REPLAY_BOUNDS __launch_bounds__(128)
 #endif
-template <bool WINDOWED, bool LOG, int PHASE>
+template <bool WINDOWED, bool LOG, int PHASE, bool ABL>
 __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
@@ -355,7 +362,8 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   double best = kInf;                                       // min_t C_t
   bool in_ts = PHASE == 2;
   int round = 1, step = kStart, start = a.b0, cursor = a.b0;
-  uint32_t cand = (B == 32) ? 0xffffffffu : ((1u << B) - 1u), surv = 0, ts_set = 0, ts_pairs = 0;
+  const uint32_t all_arms = (B == 32) ? 0xffffffffu : ((1u << B) - 1u);
+  uint32_t cand = all_arms, surv = 0, ts_set = 0, ts_pairs = 0;
   double r1_cost = kInf;
   int r1_arm = -1;
   double totC = 0.0, totE = 0.0, totT = 0.0;
@@ -482,16 +490,30 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       was_seen = (seen >> b) & 1u;
       q = st[b];
       const ArmConst ac = arm[b];
+      // the power limit accompanying b and its per-epoch cost/time/energy
+      int p = ac.pstar;
+      double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;
+      const bool no_jit = ABL && (cp.ablation & 2);
+      if (no_jit) {               // ablation "no JIT profiling": the first P runs of
+        const int runs = was_seen ? q.cnt : 0;   // b try the limits in ascending order
+        if (runs < a.P) {
+          p = runs;
+          const double Ab = __ldg(a.A + (size_t)b * a.P + p), Thb = __ldg(a.Th + (size_t)b * a.P + p);
+          c1b = ((cp.eta * Ab) + ((1.0 - cp.eta) * a.MP)) / Thb;
+          t1b = 1.0 / Thb;
+          e1b = Ab / Thb;
+        }
+      }
       // ---------------- step 3: replay one recorded run
       const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
       const int E = pool[((size_t)s * B + b) * K + r];
       const int Erun = E > 0 ? E : a.max_epochs;
       double c0, t0, e0;
-      const bool prof_now = a.charge_profiling && !((profiled >> b) & 1u);
-      if (prof_now) { c0 = ac.cP; t0 = ac.tP; e0 = ac.eP; } else { c0 = ac.c1; t0 = ac.t1; e0 = ac.e1; }
+      const bool prof_now = !no_jit && a.charge_profiling && !((profiled >> b) & 1u);
+      if (prof_now) { c0 = ac.cP; t0 = ac.tP; e0 = ac.eP; } else { c0 = c1b; t0 = t1b; e0 = e1b; }
       profiled |= 1u << b;
       const double em1 = (double)(Erun - 1);
-      const double Cf = c0 + em1 * ac.c1;
+      const double Cf = c0 + em1 * c1b;
       // ---------------- step 4: early stop at β·min_t C_t, truncated charge
       const double thr = cp.beta * best;
       double Tm, En;
@@ -503,14 +525,14 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
           Tm = phi * t0;
           En = phi * e0;
         } else {
-          const double phi = (thr - c0) / ac.c1;
-          Tm = t0 + phi * ac.t1;
-          En = e0 + phi * ac.e1;
+          const double phi = (thr - c0) / c1b;
+          Tm = t0 + phi * t1b;
+          En = e0 + phi * e1b;
         }
       } else {
         C = Cf;
-        Tm = t0 + em1 * ac.t1;
-        En = e0 + em1 * ac.e1;
+        Tm = t0 + em1 * t1b;
+        En = e0 + em1 * e1b;
       }
       const bool conv = (E > 0) && !stopped;
       if (conv && !(C >= best)) best = C;
@@ -529,7 +551,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
         if (end_round) {
           if (surv == 0u) surv = 1u << start;
           if (round == 1) {
-            cand = surv;
+            cand = (ABL && (cp.ablation & 1)) ? all_arms : surv;   // "no pruning" keeps 𝓑
             if (r1_arm >= 0) start = r1_arm;
             surv = 0u;
             round = 2;
@@ -537,7 +559,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             cursor = start;
           } else {
             in_ts = true;
-            ts_set = surv;
+            ts_set = (ABL && (cp.ablation & 1)) ? all_arms : surv;
             ts_pairs = 0u;
             for (int k = 0; 2 * k < B; ++k)
               if ((ts_set >> (2 * k)) & 3u) ts_pairs |= 1u << k;
@@ -553,14 +575,16 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       nstop += stopped ? 1 : 0;
       last_b = b;
       dig = (dig ^ (unsigned long long)(uint32_t)b) * 0x100000001b3ull;
-      dig = (dig ^ (unsigned long long)(uint32_t)ac.pstar) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)(uint32_t)p) * 0x100000001b3ull;
       dig = (dig ^ (unsigned long long)flags) * 0x100000001b3ull;
-      if (LOG) a.log[o * R + t] = (uint32_t)b | ((uint32_t)ac.pstar << 8) | (flags << 16);
+      if (LOG) a.log[o * R + t] = (uint32_t)b | ((uint32_t)p << 8) | (flags << 16);
       vC = C;
       vE = En;
       vT = Tm;
-      vReg = regret[s * B + b];
-      vPacked = (stopped ? 1 : 0) | ((b == optarm[s]) ? (1 << 8) : 0) | (ts_dec ? (1 << 16) : 0);
+      vReg = (!ABL || p == ac.pstar) ? regret[s * B + b]
+                                     : __ldg(a.ebar + (size_t)s * B + b) * c1b - __ldg(a.opt + (size_t)cell * S + s);
+      vPacked = (stopped ? 1 : 0) | ((b == optarm[s] && p == ac.pstar) ? (1 << 8) : 0) |
+                (ts_dec ? (1 << 16) : 0);
     }
     curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked);
     if (active) {
@@ -764,6 +788,39 @@ __global__ void __launch_bounds__(128) baseline_kernel(BaselineArgs a) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   if ((tid & 31) == 0 && v) atomicAdd(a.counters, v);
+}
+
+// ------------------------------------------------------------------ Pareto front (f4)
+// §2.3: the (TTA, ETA) grid of slice s -- TTA = Ebar/Th, ETA = (Ebar*A)/Th for
+// every b with a converged replica -- and its non-dominated points (ties on both axes keep
+// the first in (b, p) order).  One block per slice, threads over points, ebar from step 1.
+__global__ void pareto_kernel(const double *A, const double *Th, const double *ebar,
+                              const int32_t *pool, uint8_t *mask, int B, int P, int K) {
+  const int s = blockIdx.x;
+  const int n = B * P;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    auto point = [&](int q, double &t, double &e) -> bool {
+      const int b = q / P, p = q % P;
+      bool any = false;
+      for (int k = 0; k < K; ++k) any |= pool[((size_t)s * B + b) * K + k] > 0;
+      if (!any) return false;
+      const double eb = ebar[(size_t)s * B + b];
+      t = eb / Th[q];
+      e = (eb * A[q]) / Th[q];
+      return true;
+    };
+    double ti, ei;
+    bool keep = point(i, ti, ei);
+    for (int j = 0; j < n && keep; ++j) {
+      double tj, ej;
+      if (j == i || !point(j, tj, ej)) continue;
+      const bool le = tj <= ti && ej <= ei;
+      const bool lt = tj < ti || ej < ei;
+      if (le && lt) keep = false;
+      if (!lt && le && j < i) keep = false;
+    }
+    mask[(size_t)s * n + i] = keep ? 1 : 0;
+  }
 }
 
 // curves[cell][t][q] = sum over slots in slot order

@@ -51,7 +51,7 @@ struct zeus_sim {
   int64_t shard_total = 0, max_shard = 0;
   // trace
   int S = 0, K = 0, reg_stride = 0, opt_stride = 0;
-  bool loaded = false, ran = false, any_zeus = false, any_baseline = false;
+  bool loaded = false, ran = false, any_zeus = false, any_baseline = false, any_ablation = false;
   int nslot = 1, tpb = 128, smem_bytes = 0, tab_bytes = 0, launches = 0, nwin = 1;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
@@ -59,7 +59,7 @@ struct zeus_sim {
   // device memory
   DevBuf d_A, d_Th, d_pool, d_cells, d_arms, d_regret, d_opt, d_optarm;
   DevBuf d_slots, d_curves, d_tot_cost, d_tot_energy, d_tot_time, d_digest, d_nstop, d_final,
-      d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket, d_ebar, d_logtab;
+      d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket, d_ebar, d_logtab, d_pareto;
   ~zeus_sim() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -142,18 +142,26 @@ void check_cells(const zeus_cell *cells, int n, Errors &E) {
     if (c.trials < 0) E.add(ZEUS_E_INVALID, "trials < 0" + at);
     if (c.policy < ZEUS_POLICY_ZEUS || c.policy > ZEUS_POLICY_GRID_SEARCH)
       E.add(ZEUS_E_INVALID, "policy must be ZEUS_POLICY_ZEUS, _DEFAULT or _GRID_SEARCH" + at);
+    if (c.ablation < 0 || c.ablation > (ZEUS_ABLATE_PRUNING | ZEUS_ABLATE_JIT))
+      E.add(ZEUS_E_INVALID, "ablation must be a subset of ZEUS_ABLATE_PRUNING | ZEUS_ABLATE_JIT" + at);
   }
 }
 
 // replay_kernel<WINDOWED, LOG, PHASE> by runtime flags
 typedef void (*ReplayFn)(zs::ReplayArgs);
-ReplayFn replay_fn(bool windowed, bool log, int phase) {
-  static const ReplayFn tab[2][2][3] = {
-      {{zs::replay_kernel<false, false, 0>, zs::replay_kernel<false, false, 1>, zs::replay_kernel<false, false, 2>},
-       {zs::replay_kernel<false, true, 0>, zs::replay_kernel<false, true, 1>, zs::replay_kernel<false, true, 2>}},
-      {{zs::replay_kernel<true, false, 0>, zs::replay_kernel<true, false, 1>, zs::replay_kernel<true, false, 2>},
-       {zs::replay_kernel<true, true, 0>, zs::replay_kernel<true, true, 1>, zs::replay_kernel<true, true, 2>}}};
-  return tab[windowed][log][phase];
+template <bool W, bool L, bool A>
+constexpr ReplayFn pick(int phase) {
+  return phase == 0 ? zs::replay_kernel<W, L, 0, A> : phase == 1 ? zs::replay_kernel<W, L, 1, A>
+                                                                 : zs::replay_kernel<W, L, 2, A>;
+}
+// replay_kernel<WINDOWED, LOG, PHASE, ABLATIONS> by runtime flags
+ReplayFn replay_fn(bool windowed, bool log, int phase, bool abl = false) {
+  if (abl) {
+    if (windowed) return log ? pick<true, true, true>(phase) : pick<true, false, true>(phase);
+    return log ? pick<false, true, true>(phase) : pick<false, false, true>(phase);
+  }
+  if (windowed) return log ? pick<true, true, false>(phase) : pick<true, false, false>(phase);
+  return log ? pick<false, true, false>(phase) : pick<false, false, false>(phase);
 }
 
 // Dynamic shared memory allowed per launch of fn: the device's opt-in maximum minus the
@@ -167,7 +175,15 @@ cudaError_t grant_max_smem(const void *fn, int device, int *granted = nullptr) {
   if ((e = cudaFuncGetAttributes(&fa, fn)) != cudaSuccess) return e;
   const int dyn = optin - (int)fa.sharedSizeBytes;
   if (granted) *granted = dyn;
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn)) != cudaSuccess)
+    return e;
+#ifndef ZS_DEFAULT_CARVEOUT
+  // all of the unified L1/shared capacity as shared memory: the replay's blocks are
+  // bounded by it, and its global traffic is one 32-byte record per decision
+  return cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+#else
+  return cudaSuccess;
+#endif
 }
 
 void launch_step1(zeus_sim *s, cudaStream_t st) {
@@ -247,6 +263,8 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     p.pm0 = c.prior_mean * p.prec0;
     p.window = c.window;
     p.policy = c.policy;
+    p.ablation = c.ablation;
+    s->any_ablation |= c.ablation != 0 && c.policy == ZEUS_POLICY_ZEUS;
     s->any_zeus |= c.policy == ZEUS_POLICY_ZEUS;
     s->any_baseline |= c.policy != ZEUS_POLICY_ZEUS;
     p.key0 = (uint32_t)c.seed;
@@ -367,6 +385,10 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   ZS_CUDA(s, cudaMemcpy(s->d_pool.p, pool, (size_t)S * B * K * 4, cudaMemcpyHostToDevice));
   launch_step1(s, nullptr);
   ZS_CUDA(s, cudaGetLastError());
+  ZS_CUDA(s, s->d_pareto.alloc((size_t)S * B * P));
+  zs::pareto_kernel<<<S, 256>>>(s->d_A.as<double>(), s->d_Th.as<double>(), s->d_ebar.as<double>(),
+                                s->d_pool.as<int32_t>(), s->d_pareto.as<uint8_t>(), B, P, K);
+  ZS_CUDA(s, cudaGetLastError());
   ZS_CUDA(s, cudaDeviceSynchronize());
 
   // launch shape of the replay: the block size (32/64/128 trials) that keeps the
@@ -383,7 +405,7 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
     const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
     if (bytes > 227 * 1024) continue;
     int blocks = 0;
-    const void *fn = (const void *)replay_fn(wmax > 0, false, two_phase ? 2 : 0);
+    const void *fn = (const void *)replay_fn(wmax > 0, false, two_phase ? 2 : 0, s->any_ablation);
     int granted = 0;
     ZS_CUDA(s, grant_max_smem(fn, s->device, &granted));
     if ((int)bytes > granted) continue;
@@ -397,7 +419,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   for (int w = 0; w < 2; ++w)
     for (int l = 0; l < 2; ++l)
       for (int ph = 0; ph < 3; ++ph)
-        ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph), s->device));
+        for (int ab = 0; ab < 2; ++ab)
+          ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph, ab), s->device));
   s->loaded = true;
   return ZEUS_OK;
 }
@@ -478,15 +501,21 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     a.bucket = s->d_bucket.as<int32_t>();
     a.nwin = s->nwin;
     a.logtab = s->d_logtab.as<double2>();
+    a.A = s->d_A.as<double>();
+    a.Th = s->d_Th.as<double>();
+    a.ebar = s->d_ebar.as<double>();
+    a.opt = s->d_opt.as<double>();
+    a.P = s->P;
+    a.MP = s->MP;
     const bool two_phase = s->layout != 1 && a.t_split < s->R;
     if (!two_phase) {
-      replay_fn(windowed, s->log_mode, 0)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+      replay_fn(windowed, s->log_mode, 0, s->any_ablation)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
       ZS_CUDA(s, cudaGetLastError());
       s->launches += 1;
     } else {
       s->launches += 4;
       ZS_CUDA(s, cudaMemsetAsync(s->d_bucket.p, 0, s->d_bucket.bytes, st));
-      replay_fn(windowed, s->log_mode, 1)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+      replay_fn(windowed, s->log_mode, 1, s->any_ablation)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
       ZS_CUDA(s, cudaGetLastError());
       zs::bucket_scan_kernel<<<(unsigned)((nc * (int64_t)s->nwin + 127) / 128), 128, 0, st>>>(a.bucket, nc, s->nwin);
       ZS_CUDA(s, cudaGetLastError());
@@ -494,7 +523,7 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
       zs::bucket_scatter_kernel<<<dim3(std::max(1u, sx), (unsigned)nc), 256, 0, st>>>(
           a.cells, a.carry, a.bucket, a.perm, nc, s->B, s->nwin);
       ZS_CUDA(s, cudaGetLastError());
-      replay_fn(windowed, s->log_mode, 2)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+      replay_fn(windowed, s->log_mode, 2, s->any_ablation)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
       ZS_CUDA(s, cudaGetLastError());
     }
   }
@@ -537,6 +566,7 @@ zeus_status zeus_sim_results(zeus_sim *s, zeus_results *out) {
     return fail(s, ZEUS_E_STATE, "replay outputs requested before zeus_sim_run");
   }
   ZS_CUDA(s, cp(out->opt_cost, s->d_opt, (size_t)nc * s->S * 8));
+  ZS_CUDA(s, cp(out->pareto, s->d_pareto, (size_t)s->S * s->B * s->P));
   if (out->opt_arm) {
     std::vector<int32_t> tmp((size_t)nc * s->opt_stride);
     ZS_CUDA(s, cudaMemcpyAsync(tmp.data(), s->d_optarm.p, tmp.size() * 4, cudaMemcpyDeviceToHost, st));

@@ -124,12 +124,18 @@ def make_workload(name: str, seed: int = 0, slices: int = 1, replicas: int = 4,
 POLICIES = {"zeus": 0, "default": 1, "grid_search": 2}   # §6.1 baselines
 
 
+ABLATIONS = {"no_pruning": 1, "no_jit": 2}             # P:L1076-1077 (β = ∞ is "no early stop")
+
+
 def cell(eta=0.5, beta=2.0, window=0, seed=1, prior_mean=0.0, prior_var=math.inf,
-         policy="zeus") -> dict:
+         policy="zeus", ablation=0) -> dict:
     """One sweep cell; defaults are the paper's η = 0.5, β = 2 and a flat prior."""
+    if isinstance(ablation, str):
+        ablation = sum(ABLATIONS[a] for a in ablation.split("+") if a)
     return {"eta": float(eta), "beta": float(beta), "window": int(window), "seed": int(seed),
             "prior_mean": float(prior_mean), "prior_var": float(prior_var),
-            "policy": POLICIES[policy] if isinstance(policy, str) else int(policy)}
+            "policy": POLICIES[policy] if isinstance(policy, str) else int(policy),
+            "ablation": int(ablation)}
 
 
 @dataclass
@@ -169,6 +175,10 @@ def config(name: str, seed: int = 2208, trials: int | None = None) -> list[Job]:
             R = 2 * len(wl["batch_sizes"]) * len(wl["power_limits"])
             jobs.append(Job(wl, [cell(seed=seed + 6, policy=p) for p in POLICIES], R, trials or 10_000))
         return jobs
+    if name == "f2":   # ablations of Fig. eval-breakdown on the six workloads
+        abl = [cell(seed=seed + 7), cell(seed=seed + 7, beta=math.inf),
+               cell(seed=seed + 7, ablation="no_pruning"), cell(seed=seed + 7, ablation="no_jit")]
+        return [Job(make_workload(w, seed), abl, 200, trials or 10_000) for w in SIX]
     if name == "cfg5":
         return [Job(make_workload("generic16", seed), [cell(seed=seed + 5)], 1000,
                     trials or 10_000_000)]
@@ -176,4 +186,4 @@ def config(name: str, seed: int = 2208, trials: int | None = None) -> list[Job]:
 
 
 CONFIGS = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")
-NEXT = ("f1",)   # SURVEY §8(f) rows built on the same replay
+NEXT = ("f1", "f2")   # SURVEY §8(f) rows built on the same replay

@@ -44,7 +44,7 @@ class zeus_job(C.Structure):
 class zeus_cell(C.Structure):
     _fields_ = [("eta", C.c_double), ("beta", C.c_double), ("window", C.c_int32),
                 ("prior_mean", C.c_double), ("prior_var", C.c_double), ("seed", C.c_uint64),
-                ("trials", C.c_int64), ("policy", C.c_int32)]
+                ("trials", C.c_int64), ("policy", C.c_int32), ("ablation", C.c_int32)]
 
 
 class zeus_run_opts(C.Structure):
@@ -59,7 +59,8 @@ class zeus_results(C.Structure):
                 ("n_stop", C.c_void_p), ("final_arm", C.c_void_p), ("pstar_index", C.c_void_p),
                 ("c1", C.c_void_p), ("t1", C.c_void_p), ("e1", C.c_void_p), ("c_prof", C.c_void_p),
                 ("t_prof", C.c_void_p), ("e_prof", C.c_void_p), ("opt_cost", C.c_void_p),
-                ("opt_arm", C.c_void_p), ("log", C.c_void_p), ("counters", C.c_void_p),
+                ("opt_arm", C.c_void_p), ("pareto", C.c_void_p), ("log", C.c_void_p),
+                ("counters", C.c_void_p),
                 ("step1_ms", C.c_float), ("replay_ms", C.c_float), ("reduce_ms", C.c_float),
                 ("kernel_launches", C.c_int32)]
 
@@ -158,13 +159,15 @@ class Simulation:
                        int(workload.get("charge_profiling", 1)))
         cs = [zeus_cell(float(c["eta"]), float(c["beta"]), int(c.get("window", 0)),
                         float(c.get("prior_mean", 0.0)), float(c.get("prior_var", math.inf)),
-                        int(c.get("seed", 0)), int(trials), int(c.get("policy", 0))) for c in cells]
+                        int(c.get("seed", 0)), int(trials), int(c.get("policy", 0)),
+                        int(c.get("ablation", 0))) for c in cells]
         opts = zeus_run_opts(C.sizeof(zeus_run_opts), int(recurrences), int(shard[0]),
                              int(shard[1]), 1 if log else 0, int(layout))
         self.h = zeus_sim_create(job, cs, opts, device)
         R, n, nc, B, S = (C.c_int32(), C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32())
         lib().zeus_sim_shape(self.h, C.byref(R), C.byref(n), C.byref(nc), C.byref(B), None)
         self.R, self.shard_n, self.ncells, self.B = R.value, n.value, nc.value, B.value
+        self.P = len(pl)
         self.log = log
         self.S = None
 
@@ -198,6 +201,7 @@ class Simulation:
                   "e1": ((nc, B), np.float64), "c_prof": ((nc, B), np.float64),
                   "t_prof": ((nc, B), np.float64), "e_prof": ((nc, B), np.float64),
                   "opt_cost": ((nc, S), np.float64), "opt_arm": ((nc, S), np.int32),
+                  "pareto": ((S, B, self.P), np.uint8),
                   "log": ((n, R), np.uint32), "counters": ((COUNTERS,), np.int64)}
         bufs = dict(out or {})
         for k in want:

@@ -292,3 +292,24 @@ def test_concurrent_handles_different_footprints(zs, oracle):
         compare_cell(oracle, g, j.workload, j.cells[0], 0, np.arange(j.trials), j.recurrences,
                      j.trials)
         sm.close()
+
+
+def test_f4_pareto_front(zs, oracle):
+    """the (TTA, ETA) Pareto front of every slice equals the oracle's."""
+    for name in ("cfg2", "cfg4_38"):
+        for job in synth.config(name, trials=10):
+            sim = zs.Simulation(job.workload, job.cells, job.trials, job.recurrences).load_profile()
+            g = sim.results(want=["pareto"])
+            sim.close()
+            for s in range(job.workload["pool"].shape[0]):
+                assert np.array_equal(g["pareto"][s], oracle.pareto(job.workload, s)), (name, s)
+
+
+def test_f2_ablations(zs, oracle):
+    """the ablations of P:L1076-1077 (no early stop = beta inf, no pruning,
+    no JIT profiling) in the same launch as full Zeus; every trial bit-exact vs the oracle."""
+    for job in synth.config("f2", trials=2000)[:3]:
+        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True)
+        for ci, c in enumerate(job.cells):
+            compare_cell(oracle, g, job.workload, c, ci, np.arange(job.trials), job.recurrences,
+                         job.trials, logs=True)

@@ -489,3 +489,40 @@ def test_zeus_beats_baselines_directionally(oracle):
         wins_gs += zeus["curves"][:, 3].sum() < gs["curves"][:, 3].sum()
         wins_def += zeus["curves"][-5:, 1].sum() < default["curves"][-5:, 1].sum()
     assert wins_gs >= 5 and wins_def >= 5
+
+
+# ------------------------------------------------------------------ Pareto front
+def test_pareto_spec_example(oracle):
+    """{(10 s, 100 J), (12 s, 90 J), (11 s, 120 J)} -> {(10,100), (12,90)}; expressed
+    as three batch sizes at one power limit with Ebar = 1 (TTA = 1/Th, ETA = A/Th)."""
+    Th = [[0.1], [1 / 12], [1 / 11]]
+    A = [[10.0], [90 / 12], [120 / 11]]
+    w = trace([8, 16, 32], 0, [100], 100, A, Th, [[[1], [1], [1]]])
+    assert oracle.pareto(w).ravel().tolist() == [1, 1, 0]
+
+
+def test_pareto_brute_force_and_scalarisation(oracle):
+    """Definition by exhaustive dominance in exact rationals; the eta-optimal configuration of
+    every eta in (0,1) and both endpoints (min TTA, min ETA) are on the front."""
+    for name in synth.SIX:
+        w = synth.make_workload(name, 11)
+        m = oracle.pareto(w)
+        pool = w["pool"][0]
+        B, P = m.shape
+        pts = {}
+        for b in range(B):
+            conv = pool[b][pool[b] > 0]
+            if len(conv) == 0:
+                continue
+            eb = Fraction(int(conv.sum()), len(conv))
+            for p in range(P):
+                pts[(b, p)] = (eb / Fraction(w["throughput"][b, p]),
+                               eb * Fraction(w["avg_power"][b, p]) / Fraction(w["throughput"][b, p]))
+        for (b, p), (t, e) in pts.items():
+            dom = any(t2 <= t and e2 <= e and (t2 < t or e2 < e) for (b2, p2), (t2, e2) in pts.items())
+            assert m[b, p] == (0 if dom else 1), (name, b, p)
+        assert m[min(pts, key=lambda k: pts[k][0])] == 1 and m[min(pts, key=lambda k: pts[k][1])] == 1
+        for eta in (0.1, 0.5, 0.9):
+            st = oracle.step1(w, synth.cell(eta=eta))
+            b = st["opt_arm"][0]
+            assert m[b, st["pstar"][b]] == 1

@@ -8,6 +8,9 @@ from paper_2208_06102_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "u1": ([], []),
+    "carve0": (["ZS_DEFAULT_CARVEOUT"], []),
+    "mb6": (["ZS_P2_MIN_BLOCKS=6"], []),
+    "mb6c0": (["ZS_P2_MIN_BLOCKS=6", "ZS_DEFAULT_CARVEOUT"], []),
     "win512": (["ZS_REGROUP_WINDOW=512"], []),
     "win8k": (["ZS_REGROUP_WINDOW=8192"], []),
     "win1m": (["ZS_REGROUP_WINDOW=1048576"], []),

@@ -44,7 +44,7 @@ extern "C" {
 #define ZEUS_MAX_BATCH_SIZES 32
 #define ZEUS_MAX_POWER_LIMITS 64
 #define ZEUS_CURVE_QUANTITIES 7   /* cost, energy, time, pseudo-regret, n_stop, n_opt, n_ts */
-#define ZEUS_COUNTERS 8
+#define ZEUS_COUNTERS 9
 
 typedef enum {
   ZEUS_OK = 0,
@@ -141,9 +141,9 @@ typedef struct {
      arm | p_index << 8 | flags << 16, flags bit0 stopped, bit1 converged,
      bit2 paid the profiling epoch, bit3 decided by Thompson sampling */
   uint32_t *log;
-  /* instrumentation [8]: decisions, sampled TS decisions, normal pairs drawn,
+  /* instrumentation [9]: decisions, sampled TS decisions, normal pairs drawn,
      normals used, early stops, pruning decisions, forced explorations,
-     posterior recomputations */
+     posterior recomputations, Philox blocks drawn for normals (NC-3: two pairs each) */
   int64_t *counters;
   /* timing of the last zeus_sim_run, CUDA events on the caller's stream:
      step 1 (Eq. 7) kernel, replay kernel, curve-reduction kernel */

@@ -188,26 +188,27 @@ void zsincospi(uint64_t m, double *s_out, double *c_out) {
   *s_out = s; *c_out = c;
 }
 
-// u1 in (0,1], v in [0,1) from two 64-bit words (NC-3).
-void uniforms(uint64_t w0, uint64_t w1, double *u1, double *v) {
-  *u1 = 2.0 - bits_to_double(0x3FF0000000000000ULL | (w0 >> 12));
-  *v = bits_to_double(0x3FF0000000000000ULL | (w1 >> 12)) - 1.0;
+// u1 in (0,1], v in [0,1) from two 32-bit words (NC-3): u1 = (a + 1) 2^-32, v = b 2^-32.
+void uniforms(uint32_t a, uint32_t b, double *u1, double *v) {
+  *u1 = (double)((uint64_t)a + 1u) * 2.3283064365386962890625e-10;   // 2^-32, exact
+  *v = (double)b * 2.3283064365386962890625e-10;
 }
 
-// The Box-Muller pair for arms (2k, 2k+1) of trial i at recurrence t (NC-3).
+// The Box-Muller pair for arms (2k, 2k+1) of trial i at recurrence t (NC-3).  One Philox
+// block, counter (t, 1 << 24 | k >> 1, trial), serves two pairs: pair k uses words
+// (x0, x1) when k is even and (x2, x3) when k is odd.
 void normal_pair(uint64_t seed, int64_t trial, int32_t t, int32_t k, double *z0, double *z1) {
-  uint32_t ctr[4] = {(uint32_t)t, 0x01000000u | (uint32_t)k, (uint32_t)(uint64_t)trial,
+  uint32_t ctr[4] = {(uint32_t)t, 0x01000000u | ((uint32_t)k >> 1), (uint32_t)(uint64_t)trial,
                      (uint32_t)((uint64_t)trial >> 32)};
   uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
   uint32_t x[4];
   philox(ctr, key, x);
-  uint64_t w0 = ((uint64_t)x[1] << 32) | x[0];
-  uint64_t w1 = ((uint64_t)x[3] << 32) | x[2];
+  const uint32_t a = x[2 * (k & 1)], b = x[2 * (k & 1) + 1];
   double u1, v;
-  uniforms(w0, w1, &u1, &v);
+  uniforms(a, b, &u1, &v);
   double r = std::sqrt(-2.0 * zlog(u1));
   double s, c;
-  zsincospi(w1 >> 12, &s, &c);   // 2*pi*v with v = (w1>>12) / 2^52
+  zsincospi((uint64_t)b << 20, &s, &c);   // 2*pi*v: m = v 2^52 = b 2^20
   *z0 = r * c;
   *z1 = r * s;
 }
@@ -419,7 +420,7 @@ struct TrialResult {
   int32_t n_stop = 0, final_arm = -1;
 };
 
-struct Counters { int64_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0}; };
+struct Counters { int64_t c[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}; };
 
 // Per-epoch cost, time and energy of configuration (b, p) -- the quantity inside the
 // min of Eq. 7, in the NC-2 operation order.
@@ -534,9 +535,11 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
       if (b < 0) {
         // Alg. 1: θ̂_b ~ N(μ̂_b, σ̂_b²) for every b, b* = argmin θ̂_b
         double best_theta = std::numeric_limits<double>::infinity();
+        int last_block = -1;
         for (int k = 0; 2 * k < B; ++k) {
           uint32_t pairmask = (ts_set >> (2 * k)) & 3u;
           if (!pairmask) continue;
+          if ((k >> 1) != last_block) { last_block = k >> 1; cnt.c[8] += 1; }
           double z[2];
           normal_pair(cell.seed, trial, t, k, &z[0], &z[1]);
           cnt.c[2] += 1;
@@ -739,7 +742,7 @@ int oracle_replay(const oracle_trace *tr, const oracle_cell *cell, int32_t R,
       for (size_t i = 0; i < (size_t)R * 7; ++i) out->curves[i] += part[w][i];
   }
   if (out->counters) {
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < 9; ++q) {
       out->counters[q] = 0;
       for (int w = 0; w < threads; ++w) out->counters[q] += pc[w].c[q];
     }
@@ -791,7 +794,7 @@ void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t
 double oracle_zlog(double x) { return zlog(x); }
 double oracle_zlog_fdlibm(double x) { return zlog_fdlibm(x); }
 void oracle_zsincospi(uint64_t m52, double *s, double *c) { zsincospi(m52, s, c); }
-void oracle_uniforms(uint64_t w0, uint64_t w1, double *u1, double *v) { uniforms(w0, w1, u1, v); }
+void oracle_uniforms(uint32_t a, uint32_t b, double *u1, double *v) { uniforms(a, b, u1, v); }
 void oracle_normal_pair(uint64_t seed, int64_t trial, int32_t t, int32_t k, double *z0, double *z1) {
   normal_pair(seed, trial, t, k, z0, z1);
 }

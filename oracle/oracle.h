@@ -69,7 +69,7 @@ typedef struct {       /* replay outputs; any pointer may be NULL */
   uint32_t *log;                              /* [n][R] arm | p<<8 | flags<<16 */
   double *cost_log, *energy_log, *time_log;   /* [n][R] */
   double *curves;                             /* [R][7] sums over the given trials */
-  int64_t *counters;                          /* [8] instrumentation (see oracle.cpp) */
+  int64_t *counters;                          /* [9] instrumentation (see oracle.cpp) */
 } oracle_out;
 
 int oracle_validate(const oracle_trace *tr, const oracle_cell *cell, char *msg, int32_t msglen);
@@ -85,7 +85,7 @@ void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t
 double oracle_zlog(double x);
 double oracle_zlog_fdlibm(double x);
 void oracle_zsincospi(uint64_t m52, double *s, double *c);
-void oracle_uniforms(uint64_t w0, uint64_t w1, double *u1, double *v);
+void oracle_uniforms(uint32_t a, uint32_t b, double *u1, double *v);
 void oracle_normal_pair(uint64_t seed, int64_t trial, int32_t t, int32_t k, double *z0, double *z1);
 uint32_t oracle_replica(uint64_t seed, int64_t trial, int32_t t, int32_t K);
 int oracle_posterior(const double *xs, int32_t n, int32_t window, double prior_mean,

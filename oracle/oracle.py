@@ -109,7 +109,7 @@ def lib():
         L.oracle_zlog_fdlibm.argtypes = [C.c_double]
         L.oracle_zlog_fdlibm.restype = C.c_double
         L.oracle_zsincospi.argtypes = [C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
-        L.oracle_uniforms.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.oracle_uniforms.argtypes = [C.c_uint32, C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.oracle_normal_pair.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32,
                                          C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.oracle_replica.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32]
@@ -184,7 +184,7 @@ def replay(w, c, R, trials, threads=1, logs=False, curves=True):
     o = {
         "tot_cost": np.zeros(n), "tot_energy": np.zeros(n), "tot_time": np.zeros(n),
         "digest": np.zeros(n, np.uint64), "n_stop": np.zeros(n, np.int32),
-        "final_arm": np.zeros(n, np.int32), "counters": np.zeros(8, np.int64),
+        "final_arm": np.zeros(n, np.int32), "counters": np.zeros(9, np.int64),
     }
     o["curves"] = np.zeros((R, 7)) if curves else None
     if logs:
@@ -226,9 +226,9 @@ def zsincospi(m52):
     return s.value, c.value
 
 
-def uniforms(w0, w1):
+def uniforms(a, b):
     u, v = C.c_double(), C.c_double()
-    lib().oracle_uniforms(int(w0), int(w1), C.byref(u), C.byref(v))
+    lib().oracle_uniforms(int(a), int(b), C.byref(u), C.byref(v))
     return u.value, v.value
 
 

@@ -162,20 +162,21 @@ __device__ __forceinline__ void zsincospi(uint64_t m, double &s, double &c) {
   c = ((q + 1) & 2) ? -cc : cc;           // q=0: cf  1: -sf 2: -cf  3: sf
 }
 
-// The 128 random bits of arm pair k of `trial` at recurrence t, and the
-// Box-Muller transform of them (NC-3); normal_pair = both.
-__device__ __forceinline__ U4 pair_words(uint32_t key0, uint32_t key1, int64_t trial, int t, int k) {
-  return philox4x32_10(U4{(uint32_t)t, 0x01000000u | (uint32_t)k, (uint32_t)trial,
+// The Philox block of arm quad q = k >> 1 of `trial` at recurrence t (NC-3): it feeds two
+// Box-Muller pairs, k even -> words (x, y), k odd -> words (z, w).
+__device__ __forceinline__ U4 pair_block(uint32_t key0, uint32_t key1, int64_t trial, int t, int q) {
+  return philox4x32_10(U4{(uint32_t)t, 0x01000000u | (uint32_t)q, (uint32_t)trial,
                           (uint32_t)((uint64_t)trial >> 32)}, key0, key1);
 }
-__device__ __forceinline__ void box_muller(const U4 x, double &z0, double &z1,
+
+// Box-Muller from two 32-bit words: u1 = (a + 1) 2^-32 in (0,1], v = b 2^-32 in [0,1);
+// z0 = r cos(2 pi v), z1 = r sin(2 pi v), r = sqrt(-2 log u1) (NC-3).
+__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, double &z0, double &z1,
                                            const double2 *__restrict__ logtab) {
-  const uint64_t w0 = ((uint64_t)x.y << 32) | x.x;
-  const uint64_t w1 = ((uint64_t)x.w << 32) | x.z;
-  const double u1 = 2.0 - __longlong_as_double((long long)(0x3FF0000000000000ull | (w0 >> 12)));
+  const double u1 = (double)((unsigned long long)a + 1ull) * 0x1p-32;   // exact
   const double r = sqrt(-2.0 * zlog(u1, logtab));
   double s, c;
-  zsincospi(w1 >> 12, s, c);
+  zsincospi((uint64_t)b << 20, s, c);                                  // m = v 2^52
   z0 = r * c;
   z1 = r * s;
 }
@@ -184,7 +185,9 @@ __device__ __forceinline__ void box_muller(const U4 x, double &z0, double &z1,
 __device__ __forceinline__ void normal_pair(uint32_t key0, uint32_t key1, int64_t trial, int t,
                                             int k, double &z0, double &z1,
                                             const double2 *__restrict__ logtab) {
-  box_muller(pair_words(key0, key1, trial, t, k), z0, z1, logtab);
+  const U4 x = pair_block(key0, key1, trial, t, k >> 1);
+  if (k & 1) box_muller(x.z, x.w, z0, z1, logtab);
+  else box_muller(x.x, x.y, z0, z1, logtab);
 }
 
 // log_table_kernel: the zlog table (one block; entries j = -37..53)

@@ -15,20 +15,12 @@
 
 #include "contract.cuh"
 
-#ifndef ZS_PAIR_UNROLL
-#define ZS_PAIR_UNROLL 1
-#endif
-#ifndef ZS_PIPELINE
-#define ZS_PIPELINE 0
-#endif
-#ifndef ZS_HOIST_REPLICA
-#define ZS_HOIST_REPLICA 0
-#endif
+
 
 namespace zs {
 
 constexpr int kQ = 7;             // curve quantities
-constexpr int kCounters = 8;
+constexpr int kCounters = 9;
 
 struct ArmConst {                 // per (cell, arm), 64 B
   double c1, t1, e1, cP, tP, eP;
@@ -166,11 +158,24 @@ struct ReplayArgs {
   double MP;
 };
 
-constexpr int kBuckets = 17;      // popcount of the survivor-pair mask, 0..16
+constexpr int kBuckets = 34;      // 2 x popcount of the survivor-pair mask + parity of its lowest pair
 #ifndef ZS_REGROUP_WINDOW
 #define ZS_REGROUP_WINDOW 8192
 #endif
 constexpr int kRegroupWindow = ZS_REGROUP_WINDOW;   // trials regrouped together (multiple of 128)
+
+// Philox blocks a draw over `pairs` takes: one per quad (two pairs) touched
+__device__ __forceinline__ uint32_t quads_of(uint32_t pairs) {
+  uint32_t q = 0;
+  for (int k = 0; k < 32; k += 2) q |= ((pairs >> k) & 3u) ? (1u << (k >> 1)) : 0u;
+  return q;
+}
+
+// phase-B grouping key: lanes with the same number of survivor pairs and the same parity of
+// the lowest one draw the same number of Philox blocks at the same loop steps
+__device__ __forceinline__ int regroup_key(uint32_t pairs) {
+  return pairs ? 2 * __popc(pairs) + ((__ffs(pairs) - 1) & 1) : 0;
+}
 
 struct __align__(16) ArmStat {    // Observe state of one arm of one trial (NC-6)
   double sh, S1, S2;              // shift (first observation) and shifted sums
@@ -356,7 +361,6 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
   double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
-#define ZS_KEYARG cp.key0, cp.key1
 
   uint32_t profiled = 0, seen = 0, mature = 0;              // bit a: profiled / observed / n_a >= 2
   double best = kInf;                                       // min_t C_t
@@ -438,51 +442,21 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             bt = take1 ? th1 : bt;
             b = take1 ? 2 * k + 1 : b;
           };
-#if ZS_PAIR_UNROLL == 2
-          if (PHASE == 2) {                                 // pair counts are warp-uniform here
-            while (pm & (pm - 1u)) {                        // two independent pairs in flight
-              const int k0 = __ffs(pm) - 1;
-              pm &= pm - 1u;
-              const int k1 = __ffs(pm) - 1;
-              pm &= pm - 1u;
-              double z00, z01, z10, z11;
-              normal_pair(ZS_KEYARG, trial, t, k0, z00, z01, logtab);
-              normal_pair(ZS_KEYARG, trial, t, k1, z10, z11, logtab);
-              consider(k0, z00, z01);
-              consider(k1, z10, z11);
-            }
-          }
-#endif
-#if ZS_PIPELINE
-          {   // software pipeline: the Philox of the next pair (integer pipes) overlaps the
-              // Box-Muller transcendentals of this one (FP64 pipe)
-            int k = __ffs(pm) - 1;
-            pm &= pm - 1u;
-            U4 xn = pair_words(cp.key0, cp.key1, trial, t, k);
-            for (;;) {
-              const int kc = k;
-              const U4 xc = xn;
-              const bool more = pm != 0u;
-              if (more) {
-                k = __ffs(pm) - 1;
-                pm &= pm - 1u;
-                xn = pair_words(cp.key0, cp.key1, trial, t, k);
-              }
-              double z0, z1;
-              box_muller(xc, z0, z1, logtab);
-              consider(kc, z0, z1);
-              if (!more) break;
-            }
-          }
-#else
+          // pairs 2q and 2q+1 share one Philox block: it is drawn when the walk enters a new
+          // quad (warp-uniform in phase B, where lanes are grouped by count and parity)
+          int qcur = -1;
+          U4 xq{0u, 0u, 0u, 0u};
           while (pm) {
             const int k = __ffs(pm) - 1;
             pm &= pm - 1u;
+            if ((k >> 1) != qcur) {
+              qcur = k >> 1;
+              xq = pair_block(cp.key0, cp.key1, trial, t, qcur);
+            }
             double z0, z1;
-            normal_pair(ZS_KEYARG, trial, t, k, z0, z1, logtab);
+            box_muller((k & 1) ? xq.z : xq.x, (k & 1) ? xq.w : xq.y, z0, z1, logtab);
             consider(k, z0, z1);
           }
-#endif
           n_sampled += 1;
         }
       }
@@ -630,7 +604,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       c.nstop = nstop; c.last_b = last_b;
       c.n_sampled = n_sampled; c.n_prune = n_prune; c.n_forced = n_forced; c.n_recomp = n_recomp;
       a.carry[o] = c;
-      atomicAdd(&a.bucket[((size_t)cell * a.nwin + jj / kRegroupWindow) * kBuckets + __popc(ts_pairs)], 1);
+      atomicAdd(&a.bucket[((size_t)cell * a.nwin + jj / kRegroupWindow) * kBuckets + regroup_key(ts_pairs)], 1);
     }
     return;
   }
@@ -645,7 +619,8 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   unsigned long long ctr[kCounters] = {
       active ? (unsigned long long)R : 0ull, n_sampled,
       (unsigned long long)n_sampled * __popc(ts_pairs), (unsigned long long)n_sampled * __popc(ts_set),
-      (unsigned long long)nstop, n_prune, n_forced, n_recomp};
+      (unsigned long long)nstop, n_prune, n_forced, n_recomp,
+      (unsigned long long)n_sampled * __popc(quads_of(ts_pairs))};
 #pragma unroll
   for (int q = 0; q < kCounters; ++q) {
     unsigned long long v = ctr[q];
@@ -682,7 +657,7 @@ __global__ void bucket_scatter_kernel(const CellParam *cells, const Carry *carry
     uint32_t pairs = 0;
     for (int k = 0; 2 * k < B; ++k)
       if ((ts_set >> (2 * k)) & 3u) pairs |= 1u << k;
-    const int pos = atomicAdd(&bucket[((size_t)cell * nwin + j / kRegroupWindow) * kBuckets + __popc(pairs)], 1);
+    const int pos = atomicAdd(&bucket[((size_t)cell * nwin + j / kRegroupWindow) * kBuckets + regroup_key(pairs)], 1);
     perm[cp.out_off + pos] = (int32_t)j;
   }
 }

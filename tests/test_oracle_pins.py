@@ -45,11 +45,11 @@ def test_philox_known_answers(oracle):
 
 
 def test_uniform_boundaries(oracle):
-    """NC-3: u1 in (0,1], v in [0,1); extreme words map exactly."""
-    assert oracle.uniforms(0, 0) == (1.0, 0.0)
-    u, v = oracle.uniforms(2**64 - 1, 2**64 - 1)
-    assert u == 2.0**-52 and v == 1.0 - 2.0**-52
-    u, v = oracle.uniforms(1 << 63, 1 << 63)
+    """NC-3: u1 = (a + 1) 2^-32 in (0,1], v = b 2^-32 in [0,1); extreme words map exactly."""
+    assert oracle.uniforms(0, 0) == (2.0**-32, 0.0)
+    u, v = oracle.uniforms(2**32 - 1, 2**32 - 1)
+    assert u == 1.0 and v == 1.0 - 2.0**-32
+    u, v = oracle.uniforms((1 << 31) - 1, 1 << 31)
     assert u == 0.5 and v == 0.5
 
 
@@ -66,8 +66,8 @@ def test_zlog_accuracy(oracle):
     rng = np.random.default_rng(7)
     xs = [1.0, 0.5, 0.25, 2.0**-52, 2.0**-52 * 3, 0.7071067811865476, 0.7071067811865475,
           1.0 - 2.0**-52, 0.9999, 0.75, 0.1, 1e-10]
-    for w in rng.integers(0, 2**63, size=3000, dtype=np.int64):
-        xs.append(oracle.uniforms(int(w) * 2 + 1, 0)[0])
+    for w in rng.integers(0, 2**32, size=3000, dtype=np.int64):
+        xs.append(oracle.uniforms(int(w), 0)[0])
     xs += list(rng.random(1000) + 1e-300)
     worst = worst_fd = 0
     for x in xs:
@@ -128,12 +128,16 @@ def test_normals_are_standard_normal(oracle):
     assert abs(flat.var() - 1) < 5 * math.sqrt(2 / n)
     assert stats.kstest(flat, "norm").pvalue > 1e-4
     assert abs(np.corrcoef(z[:, 0], z[:, 1])[0, 1]) < 5 / math.sqrt(len(z))
-    # the pair is keyed by (trial, recurrence, arm pair): changing any key changes it
+    # the pair is keyed by (trial, recurrence, arm pair): changing any key changes it, and the
+    # two pairs that share a Philox block are independent
     a = oracle.normal_pair(1234, 5, 3, 1)
     assert a != oracle.normal_pair(1234, 6, 3, 1)
     assert a != oracle.normal_pair(1234, 5, 4, 1)
     assert a != oracle.normal_pair(1234, 5, 3, 2)
     assert a != oracle.normal_pair(1235, 5, 3, 1)
+    zz = np.array([oracle.normal_pair(99, i, 2, 0) + oracle.normal_pair(99, i, 2, 1) for i in range(20000)])
+    c = np.corrcoef(zz.T)
+    assert np.all(np.abs(c[np.triu_indices(4, 1)]) < 5 / math.sqrt(len(zz)))
 
 
 def test_replica_draw_is_uniform(oracle):

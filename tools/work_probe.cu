@@ -14,6 +14,9 @@ extern "C" __global__ void probe_zlog(const double *in, double *out, const doubl
 extern "C" __global__ void probe_sincospi(const unsigned long long *in, double *out) {
   double s, c; zsincospi(in[0], s, c); out[0] = s; out[1] = c;
 }
+extern "C" __global__ void probe_bm(const uint32_t *in, double *out, const double2 *tab) {
+  double z0, z1; box_muller(in[0], in[1], z0, z1, tab); out[0] = z0; out[1] = z1;
+}
 extern "C" __global__ void probe_sqrt(const double *in, double *out) { out[0] = sqrt(in[0]); }
 extern "C" __global__ void probe_div(const double *in, double *out) { out[0] = in[0] / in[1]; }
 extern "C" __global__ void probe_pair(const long long *in, double *out, const double2 *tab) {

@@ -118,22 +118,22 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ work model
 def work_per_launch(counters, _unused=None):
-    """Algorithmic lane-instructions of one launch: event counts x per-primitive SASS costs
-    (tools/work_model.json)."""
+    """Algorithmic lane-instructions of one launch: the replay's event counts x per-primitive
+    sm_100a SASS costs of the contract (tools/work_model.json):
+      per normal pair      one Box-Muller transform (bm)
+      per Philox block     one Philox4x32-10 (a block feeds two pairs, NC-3)
+      per normal used      theta = fma + strict-< argmin step
+      per decision         the serial contract work (lookup, charge, early stop, Observe and
+                           posterior, totals, digest, curve contributions) + a quarter replica
+                           Philox block + this decision's share of the warp curve reduction"""
     wm = json.load(open(os.path.join(ROOT, "tools", "work_model.json")))
     dec, _, pairs, normals, _, _, _, _, blocks = [int(x) for x in counters]
-    # per decision besides sampling: a quarter replica Philox block + lookup + charge + stop test, Observe
-    # (n >= 2 path; the n < 2 path is cheaper, counted the same), ~30 bookkeeping ops
-    # (pruning state machine, digest, totals, flags, curve contributions)
-    per_dec = {k: wm["charge"][k] + wm["observe"][k] + wm["philox"][k] / 4.0 for k in ("fp64", "other")}
-    per_dec["other"] += 30
-    # sampling: a Box-Muller transform per pair, a Philox block per two pairs (NC-3), a
-    # theta fma + argmin step per normal used
+    per_dec = {k: wm["serial"][k] + wm["philox"][k] / 4.0 + wm["curves"][k] for k in ("fp64", "total")}
     fp64 = (pairs * wm["bm"]["fp64"] + blocks * wm["philox"]["fp64"] + normals * wm["theta"]["fp64"]
             + dec * per_dec["fp64"])
-    other = (pairs * wm["bm"]["other"] + blocks * wm["philox"]["other"] + normals * wm["theta"]["other"]
-             + dec * per_dec["other"])
-    return {"fp64": fp64, "total": fp64 + other}
+    total = (pairs * wm["bm"]["total"] + blocks * wm["philox"]["total"] + normals * wm["theta"]["total"]
+             + dec * per_dec["total"])
+    return {"fp64": fp64, "total": total}
 
 
 # ------------------------------------------------------------------ reference arm (oracle)

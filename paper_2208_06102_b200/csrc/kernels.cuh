@@ -775,7 +775,7 @@ __global__ void pareto_kernel(const double *A, const double *Th, const double *e
   const int n = B * P;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     auto point = [&](int q, double &t, double &e) -> bool {
-      const int b = q / P, p = q % P;
+      const int b = q / P;
       bool any = false;
       for (int k = 0; k < K; ++k) any |= pool[((size_t)s * B + b) * K + k] > 0;
       if (!any) return false;

@@ -1,7 +1,7 @@
 // work_probe.cu -- per-primitive SASS instruction counts of the contract functions
 // (compiled, never run): each probe kernel wraps ONE primitive between a load and a
 // store so `tools/work_model.py` can count its straight-line instructions by pipe.
-#include "../paper_2208_06102_b200/csrc/contract.cuh"
+#include "../paper_2208_06102_b200/csrc/kernels.cuh"
 using namespace zs;
 extern "C" __global__ void probe_empty(const double *in, double *out) {
   out[threadIdx.x] = in[threadIdx.x];
@@ -62,4 +62,45 @@ extern "C" __global__ void probe_charge(const double *in, const int *pool, doubl
   const double thr = in[6] * in[7];
   out[0] = Cf; out[1] = in[2] + em1 * in[3]; out[2] = in[4] + em1 * in[5];
   out[3] = (Cf > thr) ? 1.0 : 0.0;
+}
+// The per-decision work besides sampling, as the contract requires it (Thompson phase,
+// n >= 2, unbounded window): trace lookup with the replica word, charge + early-stop test,
+// best update, Observe (shifted sums + posterior, NC-6), per-trial totals, FNV-1a digest of
+// (b, p, flags), the pseudo-regret / optimum lookups of the curve contributions.
+extern "C" __global__ void probe_serial(const double *in, const int *pool, const double *tab,
+                                        double *out, unsigned long long *dig_io, const uint4 *w,
+                                        int t, int b, int s, int B, int K, int max_epochs) {
+  const uint4 ww = *w;
+  const uint32_t r = __umulhi(pick_word(U4{ww.x, ww.y, ww.z, ww.w}, t), (uint32_t)K);
+  const int E = pool[((size_t)s * B + b) * K + r];
+  const int Erun = E > 0 ? E : max_epochs;
+  const double c1 = in[0], t1 = in[1], e1 = in[2], best0 = in[3], beta = in[4];
+  const double em1 = (double)(Erun - 1);
+  const double Cf = c1 + em1 * c1;
+  const double thr = beta * best0;
+  const bool stopped = Cf > thr;
+  const double C = stopped ? thr : Cf;
+  const double Tm = t1 + em1 * t1, En = e1 + em1 * e1;
+  const bool conv = (E > 0) && !stopped;
+  const double best = (conv && !(C >= best0)) ? C : best0;
+  // Observe
+  const double sh = in[5];
+  double S1 = in[6], S2 = in[7];
+  const int n = (int)in[8] + 1;
+  const double d = C - sh;
+  S1 = S1 + d; S2 = S2 + d * d;
+  const double2 ms = posterior(sh, S1, S2, n, in[9], in[10]);
+  // totals, digest, curve contributions
+  const uint32_t flags = (stopped ? 1u : 0u) | (conv ? 2u : 0u) | 8u;
+  unsigned long long dig = dig_io[0];
+  dig = (dig ^ (unsigned long long)(uint32_t)b) * 0x100000001b3ull;
+  dig = (dig ^ (unsigned long long)(uint32_t)(b + 1)) * 0x100000001b3ull;
+  dig = (dig ^ (unsigned long long)flags) * 0x100000001b3ull;
+  dig_io[0] = dig;
+  out[0] = C + in[11]; out[1] = En + in[12]; out[2] = Tm + in[13];
+  out[3] = tab[s * B + b]; out[4] = best; out[5] = ms.x; out[6] = ms.y; out[7] = S1; out[8] = S2;
+}
+// One warp's per-recurrence curve reduction (executed once per warp-recurrence = 32 decisions)
+extern "C" __global__ void probe_curves(double *curves, const double *v, const int *pk, int t) {
+  curve_accumulate(curves, t, threadIdx.x & 31, v[0], v[1], v[2], v[3], pk[0]);
 }

@@ -414,6 +414,10 @@ uint32_t above(int c) { return c >= 31 ? 0u : ~((2u << c) - 1u); }
 
 enum Step { START, DOWN, UP };
 
+// Outstanding runs per trial under an arrival schedule (R-Q31): a submission that would
+// exceed it first waits for the earliest completion.
+constexpr int kMaxOutstanding = 8;
+
 struct TrialResult {
   double tot_cost = 0, tot_energy = 0, tot_time = 0;
   uint64_t digest = 0xcbf29ce484222325ULL;
@@ -517,16 +521,84 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
   uint32_t surv = 0, ts_set = 0;
   double r1_cost = std::numeric_limits<double>::infinity();
   int r1_arm = -1;
+  int best_arm = -1;              // the best-known batch size (arm of min_t C_t)
+  bool walk_out = false;          // an Alg. 3 walk run is submitted and not yet completed
+
+  // A run's outcome reaching the optimiser: best update, Observe (Alg. 2) and, for the
+  // runs Alg. 3's walk issued, the walk's bookkeeping.
+  struct Job { double done; int32_t seq; int b; double C; bool conv; bool walk; };
+  std::vector<Job> pending;
+  auto complete = [&](const Job &j) {
+    const int b = j.b;
+    const double C = j.C;
+    const bool converged = j.conv;
+    if (converged && !(C >= best)) { best = C; best_arm = b; }
+    // Alg. 2 Observe: every run is observed, stopped runs at the threshold (R-Q3)
+    if (observe(arm[b], C, cell.window, pr, nullptr, nullptr)) cnt.c[7] += 1;
+    if (!j.walk) return;
+    walk_out = false;
+    // ---- Alg. 3 bookkeeping
+    if (converged) {
+      surv |= 1u << b;
+      if (round == 1 && (C < r1_cost || (C == r1_cost && b < r1_arm))) { r1_cost = C; r1_arm = b; }
+    }
+    bool end_round = false;
+    if (step == START) { step = DOWN; cursor = start; }
+    else if (step == DOWN) { if (converged) cursor = b; else { step = UP; cursor = start; } }
+    else { if (converged) cursor = b; else end_round = true; }
+    if (!end_round && step == DOWN && (cand & below(cursor)) == 0) { step = UP; cursor = start; }
+    if (!end_round && step == UP && (cand & above(cursor)) == 0) end_round = true;
+    if (end_round) {
+      if (surv == 0) surv = 1u << start;           // R-Q23
+      if (round == 1) {
+        cand = (cell.ablation & 1) ? all_arms : surv;   // "no pruning" keeps 𝓑
+        if (r1_arm >= 0) start = r1_arm;           // b0 <- b with smallest cost observed
+        surv = 0;
+        round = 2;
+        step = START;
+        cursor = start;
+      } else {
+        in_ts = true;
+        ts_set = (cell.ablation & 1) ? all_arms : surv;
+      }
+    }
+  };
+  // completes the earliest pending run, by (completion time, submission order)
+  auto complete_earliest = [&]() {
+    size_t e = 0;
+    for (size_t i = 1; i < pending.size(); ++i)
+      if (pending[i].done < pending[e].done ||
+          (pending[i].done == pending[e].done && pending[i].seq < pending[e].seq)) e = i;
+    const Job j = pending[e];
+    pending.erase(pending.begin() + (long)e);
+    complete(j);
+  };
 
   for (int32_t t = 0; t < R; ++t) {
     const int s = (int)(((int64_t)t * S) / R);   // slice of recurrence t (R-Q19)
+    if (cell.arrivals) {                           // runs finished by this submission (R-Q31)
+      for (;;) {
+        bool any = false;
+        for (const Job &j : pending) any |= j.done <= cell.arrivals[t];
+        if (!any) break;
+        complete_earliest();
+      }
+      while ((int)pending.size() >= kMaxOutstanding) complete_earliest();
+    }
     // ---- step 2: decide b_t
     int b;
+    bool walk_issue = false;
     const bool ts_dec = in_ts;   // phase at decision time (flag bit 3)
     if (!in_ts) {
-      if (step == START) b = start;
-      else if (step == DOWN) b = highest_bit(cand & below(cursor));
-      else b = lowest_bit(cand & above(cursor));
+      if (walk_out) {              // concurrent submission while pruning: best-known b
+        b = best_arm >= 0 ? best_arm : start;
+      } else {
+        if (step == START) b = start;
+        else if (step == DOWN) b = highest_bit(cand & below(cursor));
+        else b = lowest_bit(cand & above(cursor));
+        walk_issue = true;
+        walk_out = true;
+      }
       cnt.c[5] += 1;
     } else {
       b = -1;
@@ -556,7 +628,6 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
         cnt.c[6] += 1;
       }
     }
-    // ---- step 1 result: the power limit accompanying b
     // ---- step 1 result: the power limit accompanying b.  Ablation "no JIT
     // profiling": the first P runs of b try the power limits in ascending
     // order, one per recurrence, each at its own per-epoch cost; then p*(b).
@@ -603,39 +674,13 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
       C = C_full; Tm = T_full; En = En_full;
     }
     const bool converged = (E > 0) && !stopped;
-    if (converged && !(C >= best)) best = C;
-    // Alg. 2 Observe: every run is observed, stopped runs at the threshold (R-Q3)
-    if (observe(arm[b], C, cell.window, pr, nullptr, nullptr)) cnt.c[7] += 1;
     cnt.c[0] += 1;
     if (stopped) cnt.c[4] += 1;
-
-    // ---- Alg. 3 bookkeeping
-    if (!in_ts) {
-      if (converged) {
-        surv |= 1u << b;
-        if (round == 1 && (C < r1_cost || (C == r1_cost && b < r1_arm))) { r1_cost = C; r1_arm = b; }
-      }
-      bool end_round = false;
-      if (step == START) { step = DOWN; cursor = start; }
-      else if (step == DOWN) { if (converged) cursor = b; else { step = UP; cursor = start; } }
-      else { if (converged) cursor = b; else end_round = true; }
-      if (!end_round && step == DOWN && (cand & below(cursor)) == 0) { step = UP; cursor = start; }
-      if (!end_round && step == UP && (cand & above(cursor)) == 0) end_round = true;
-      if (end_round) {
-        if (surv == 0) surv = 1u << start;           // R-Q23
-        if (round == 1) {
-          cand = (cell.ablation & 1) ? all_arms : surv;   // "no pruning" keeps 𝓑
-          if (r1_arm >= 0) start = r1_arm;           // b0 <- b with smallest cost observed
-          surv = 0;
-          round = 2;
-          step = START;
-          cursor = start;
-        } else {
-          in_ts = true;
-          ts_set = (cell.ablation & 1) ? all_arms : surv;
-        }
-      }
-    }
+    // the run's outcome reaches the optimiser when it completes: immediately in the paper's
+    // sequential replay, at submit time + its TTA with an arrival schedule
+    const Job job{cell.arrivals ? cell.arrivals[t] + Tm : 0.0, t, b, C, converged, walk_issue};
+    if (cell.arrivals) pending.push_back(job);
+    else complete(job);
 
     // ---- accumulate (Eq. 4, Eqs. 8-9)
     const uint32_t flags = (stopped ? 1u : 0u) | (converged ? 2u : 0u) |
@@ -707,6 +752,12 @@ int oracle_step1(const oracle_trace *tr, const oracle_cell *cell, oracle_tables 
 int oracle_replay(const oracle_trace *tr, const oracle_cell *cell, int32_t R,
                   const int64_t *trials, int64_t n, int32_t threads, oracle_out *out) {
   if (!validate(*tr, *cell).empty() || R < 0 || n < 0) return 1;
+  if (cell->arrivals) {                 // arrival schedule: Zeus only, finite, non-decreasing
+    if (cell->policy != 0 || cell->ablation != 0) return 1;
+    for (int32_t t = 0; t < R; ++t)
+      if (!std::isfinite(cell->arrivals[t]) || (t > 0 && cell->arrivals[t] < cell->arrivals[t - 1]))
+        return 1;
+  }
   Tables T;
   step1(*tr, *cell, T);
   if (threads < 1) threads = 1;

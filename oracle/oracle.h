@@ -49,6 +49,8 @@ typedef struct {
   int32_t policy;      /* 0 Zeus (Alg. 3 + Alg. 1/2), 1 Default (b0, max p), 2 Grid Search
                           with pruning (§6.1) */
   int32_t ablation;    /* Zeus ablations: bit0 no pruning, bit1 no JIT profiling */
+  const double *arrivals; /* NULL: sequential recurrences; else [R] non-decreasing submit times
+                             (s): concurrent submissions (§4.4), Zeus only */
 } oracle_cell;
 
 typedef struct {       /* step-1 tables; any pointer may be NULL */

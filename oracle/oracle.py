@@ -56,6 +56,7 @@ class Cell(C.Structure):
         ("seed", C.c_uint64),
         ("policy", C.c_int32),
         ("ablation", C.c_int32),
+        ("arrivals", C.POINTER(C.c_double)),
     ]
 
 
@@ -143,9 +144,14 @@ class _Held:
 
 
 def _cell(c):
-    return Cell(float(c["eta"]), float(c["beta"]), int(c.get("window", 0)),
-                float(c.get("prior_mean", 0.0)), float(c.get("prior_var", np.inf)),
-                int(c.get("seed", 0)), int(c.get("policy", 0)), int(c.get("ablation", 0)))
+    arr = c.get("arrivals")
+    cc = Cell(float(c["eta"]), float(c["beta"]), int(c.get("window", 0)),
+              float(c.get("prior_mean", 0.0)), float(c.get("prior_var", np.inf)),
+              int(c.get("seed", 0)), int(c.get("policy", 0)), int(c.get("ablation", 0)), None)
+    if arr is not None:
+        cc._arr = np.ascontiguousarray(arr, dtype=np.float64)   # kept alive with the struct
+        cc.arrivals = _p(cc._arr, C.c_double)
+    return cc
 
 
 def validate(w, c):

@@ -128,14 +128,29 @@ ABLATIONS = {"no_pruning": 1, "no_jit": 2}             # P:L1076-1077 (β = ∞ 
 
 
 def cell(eta=0.5, beta=2.0, window=0, seed=1, prior_mean=0.0, prior_var=math.inf,
-         policy="zeus", ablation=0) -> dict:
-    """One sweep cell; defaults are the paper's η = 0.5, β = 2 and a flat prior."""
+         policy="zeus", ablation=0, arrivals=None) -> dict:
+    """One sweep cell; defaults are the paper's η = 0.5, β = 2 and a flat prior.
+    ``arrivals``: optional [R] submission times (s) for concurrent submissions (§4.4)."""
     if isinstance(ablation, str):
         ablation = sum(ABLATIONS[a] for a in ablation.split("+") if a)
-    return {"eta": float(eta), "beta": float(beta), "window": int(window), "seed": int(seed),
-            "prior_mean": float(prior_mean), "prior_var": float(prior_var),
-            "policy": POLICIES[policy] if isinstance(policy, str) else int(policy),
-            "ablation": int(ablation)}
+    c = {"eta": float(eta), "beta": float(beta), "window": int(window), "seed": int(seed),
+         "prior_mean": float(prior_mean), "prior_var": float(prior_var),
+         "policy": POLICIES[policy] if isinstance(policy, str) else int(policy),
+         "ablation": int(ablation)}
+    if arrivals is not None:
+        c["arrivals"] = np.ascontiguousarray(arrivals, dtype=np.float64)
+    return c
+
+
+def arrival_schedule(workload: dict, R: int, overlap: float, seed: int) -> np.ndarray:
+    """Poisson submissions whose mean gap is ``overlap`` x the TTA of b0 at the highest power
+    limit with mean epochs (overlap < 1: later jobs start before earlier ones finish, as in
+    the Alibaba job groups of §6.3)."""
+    b0 = workload["b0"]
+    pool = workload["pool"][0, b0]
+    tta = float(pool[pool > 0].mean()) / float(workload["throughput"][b0, -1])
+    rng = _rng(seed, workload["name"], "arrivals")
+    return np.cumsum(rng.exponential(overlap * tta, size=R))
 
 
 @dataclass
@@ -179,6 +194,14 @@ def config(name: str, seed: int = 2208, trials: int | None = None) -> list[Job]:
         abl = [cell(seed=seed + 7), cell(seed=seed + 7, beta=math.inf),
                cell(seed=seed + 7, ablation="no_pruning"), cell(seed=seed + 7, ablation="no_jit")]
         return [Job(make_workload(w, seed), abl, 200, trials or 10_000) for w in SIX]
+    if name == "f3":   # concurrent submissions (§4.4): sequential, mild, heavy overlap
+        jobs = []
+        for w in SIX:
+            wl = make_workload(w, seed)
+            cells = [cell(seed=seed + 8)] + [cell(seed=seed + 8, arrivals=arrival_schedule(wl, 200, ov, seed))
+                                             for ov in (1.0, 0.25)]
+            jobs.append(Job(wl, cells, 200, trials or 10_000))
+        return jobs
     if name == "cfg5":
         return [Job(make_workload("generic16", seed), [cell(seed=seed + 5)], 1000,
                     trials or 10_000_000)]
@@ -186,4 +209,4 @@ def config(name: str, seed: int = 2208, trials: int | None = None) -> list[Job]:
 
 
 CONFIGS = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")
-NEXT = ("f1", "f2")   # SURVEY §8(f) rows built on the same replay
+NEXT = ("f1", "f2", "f3")   # SURVEY §8(f) rows built on the same replay

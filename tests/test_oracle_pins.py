@@ -530,3 +530,52 @@ def test_pareto_brute_force_and_scalarisation(oracle):
             st = oracle.step1(w, synth.cell(eta=eta))
             b = st["opt_arm"][0]
             assert m[b, st["pstar"][b]] == 1
+
+
+# ------------------------------------------------------------------ concurrent submissions (f3)
+def test_concurrency_sequential_schedule_is_identical(oracle):
+    """S:L445 / acceptance 10: an arrival schedule without overlap (every run done
+    before the next submission) reproduces the sequential replay bit-exactly."""
+    for name, window in (("deepspeech2", 0), ("bert_sa", 10)):
+        w = synth.make_workload(name, 2)
+        R = 90
+        base = synth.cell(seed=12, window=window)
+        seq = dict(base, arrivals=np.arange(R) * 1e9)
+        a = oracle.replay(w, base, R, range(40), logs=True)
+        b = oracle.replay(w, seq, R, range(40), logs=True)
+        for k in ("log", "tot_cost", "tot_time", "digest", "n_stop"):
+            assert np.array_equal(a[k], b[k]), k
+
+
+def test_concurrency_pruning_runs_best_known(oracle):
+    """during pruning a submission that overlaps the walk's outstanding run takes the
+    best-known batch size (b0 before anything converged); the walk resumes with the results
+    in completion order (W1 trace: the arm-32 run takes 6 x 4/3 = 8 s)."""
+    g = load("micro_traces.json")
+    t = g["trace"]
+    w = trace(t["batch_sizes"], t["b0"], t["power_limits"], t["max_power"], t["avg_power"],
+              t["throughput"], t["pool"], t["max_epochs"], 0)
+    arr = np.array([0.0, 0.1, 100, 100.5, 200, 300, 300.2, 400, 500, 600])
+    o = oracle.replay(w, synth.cell(eta=1.0, beta=2.0, seed=3, arrivals=arr), len(arr), [0, 1], logs=True)
+    arms = [int(x & 0xFF) for x in o["log"][0]]
+    # t0 walk: 32; t1 overlaps it: best-known = none -> start 32; t2 walk down: 16 (done at 110);
+    # t3 overlaps: best-known = 32 (720); t4 walk up: 64 -> stopped at 2*720
+    assert arms[:5] == [1, 1, 0, 1, 2]
+    assert int(o["log"][0][4] >> 16) & 1
+
+
+def test_concurrency_overlap_is_valid_and_deterministic(oracle):
+    """Heavy overlap (up to the 8-run cap): decisions stay valid, charges stay under the
+    threshold of their submission time, and the replay is deterministic."""
+    w = synth.make_workload("resnet50", 3)
+    R = 120
+    rng = np.random.default_rng(4)
+    arr = np.cumsum(rng.exponential(0.25 * 40 / w["throughput"].max(), size=R))
+    cel = synth.cell(seed=21, arrivals=arr)
+    a = oracle.replay(w, cel, R, range(30), logs=True)
+    b = oracle.replay(w, cel, R, range(30), logs=True, threads=3)
+    assert np.array_equal(a["digest"], b["digest"])
+    np.testing.assert_allclose(a["cost_log"], 0.5 * a["energy_log"] + 0.5 * w["max_power"] * a["time_log"],
+                               rtol=1e-12)
+    seq = oracle.replay(w, synth.cell(seed=21), R, range(30))
+    assert not np.array_equal(a["digest"], seq["digest"])

@@ -85,6 +85,11 @@ typedef struct {
                                         replayed on the same traces and replica draws */
   int32_t ablation;                  /* Zeus only: ZEUS_ABLATE_* bits; "no early
                                         stopping" is beta = +INFINITY */
+  const double *arrivals;            /* NULL: recurrences run back to back (the paper's replay);
+                                        else host [R] non-decreasing submission times (s) shared
+                                        by the cell's trials: concurrent submissions (§4.4
+                                        P:L634-646); a run completes at its submission time +
+                                        its TTA; Zeus policy without ablations only */
 } zeus_cell;
 
 #define ZEUS_ABLATE_PRUNING 1       /* keep every batch size: Alg. 3 still walks, 𝓑 is not pruned */

@@ -31,7 +31,8 @@ struct ArmConst {                 // per (cell, arm), 64 B
 struct CellParam {                // per cell
   double eta, beta, prec0, pm0;
   int32_t window, policy;         // policy: 0 Zeus, 1 Default, 2 Grid Search (§6.1)
-  int32_t ablation, pad;          // Zeus ablations: bit0 no pruning, bit1 no JIT
+  int32_t ablation, conc;         // Zeus ablations: bit0 no pruning, bit1 no JIT;
+                                  // conc: an arrival schedule (concurrent submissions, f3)
   uint32_t key0, key1;
   int64_t begin, n, out_off;      // global first trial, shard size, offset into per-trial outputs
 };
@@ -321,7 +322,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const CellParam cp = a.cells[cell];
   const int tid = threadIdx.x, TPB = blockDim.x;
   const int64_t j0 = (int64_t)blockIdx.x * TPB;
-  if (j0 >= cp.n || cp.policy != 0) return;               // past the shard / a baseline cell
+  if (j0 >= cp.n || cp.policy != 0 || cp.conc) return;    // past the shard / another kernel's cell
 
   // ---- stage the cell's tables with TMA bulk copies (one elected thread)
   const TabLayout L(a.B, a.S, a.K);
@@ -650,7 +651,7 @@ __global__ void bucket_scatter_kernel(const CellParam *cells, const Carry *carry
                                       int32_t *perm, int ncells, int B, int nwin) {
   const int cell = blockIdx.y;
   const CellParam cp = cells[cell];
-  if (cp.policy != 0) return;
+  if (cp.policy != 0 || cp.conc) return;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cp.n;
        j += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t ts_set = carry[cp.out_off + j].ts_set;
@@ -659,6 +660,296 @@ __global__ void bucket_scatter_kernel(const CellParam *cells, const Carry *carry
       if ((ts_set >> (2 * k)) & 3u) pairs |= 1u << k;
     const int pos = atomicAdd(&bucket[((size_t)cell * nwin + j / kRegroupWindow) * kBuckets + regroup_key(pairs)], 1);
     perm[cp.out_off + pos] = (int32_t)j;
+  }
+}
+
+// ------------------------------------------------------------------ concurrent submissions (f3)
+// §4.4 "Handling concurrent job submissions" under an arrival schedule: recurrence t
+// is submitted at arrivals[t]; its outcome reaches the optimiser (best update, Observe, Alg. 3
+// walk bookkeeping) when it completes at arrivals[t] + its TTA, in (completion, submission)
+// order; a pruning-phase submission that overlaps the walk's outstanding run takes the
+// best-known batch size; at most kMaxOutstanding runs per trial are in flight (R-Q31).
+// One thread per trial, one pass, tables read through the read-only cache.
+constexpr int kMaxOutstanding = 8;
+
+struct ConcArgs {
+  const CellParam *cells;
+  const ArmConst *arms;           // [cells][B]
+  const double *regret;           // [cells][reg_stride]
+  const int32_t *opt_arm;         // [cells][opt_stride]
+  const int32_t *pool;            // [S][B][K]
+  const double2 *logtab;
+  const double *arrivals;         // [cells][R] (cells with conc = 1)
+  double *curve_slots;
+  double *tot_cost, *tot_energy, *tot_time;
+  unsigned long long *digest;
+  int32_t *n_stop, *final_arm;
+  uint32_t *log;
+  unsigned long long *counters;
+  ArmStat *st;
+  double *st_ring;
+  int ring_n;
+  int B, S, K, R, max_epochs, charge_profiling, b0, nslot, reg_stride, opt_stride;
+};
+
+template <bool LOG>
+__global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int cell = blockIdx.y;
+  const CellParam cp = a.cells[cell];
+  const int tid = threadIdx.x, TPB = blockDim.x;
+  const int64_t j0 = (int64_t)blockIdx.x * TPB;
+  if (j0 >= cp.n || cp.policy != 0 || !cp.conc) return;
+  double2 *s_ms = reinterpret_cast<double2 *>(smem);       // [arm][thread] (mu, sigma)
+  const int B = a.B, R = a.R, S = a.S, K = a.K;
+  const ArmConst *arm = a.arms + (size_t)cell * B;
+  const double *regret = a.regret + (size_t)cell * a.reg_stride;
+  const int32_t *optarm = a.opt_arm + (size_t)cell * a.opt_stride;
+  const double *arr = a.arrivals + (size_t)cell * R;
+  const int64_t jj = j0 + tid;
+  const bool active = jj < cp.n;
+  const int64_t trial = cp.begin + jj;
+  const size_t o = (size_t)(cp.out_off + jj);
+  ArmStat *st = a.st + o * B;
+  const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
+  double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+
+  uint32_t profiled = 0, seen = 0, mature = 0;
+  double best = kInf;
+  int best_arm = -1;
+  bool in_ts = false, walk_out = false;
+  int round = 1, step = kStart, start = a.b0, cursor = a.b0;
+  const uint32_t all_arms = (B == 32) ? 0xffffffffu : ((1u << B) - 1u);
+  uint32_t cand = all_arms, surv = 0, ts_set = 0, ts_pairs = 0;
+  double r1_cost = kInf;
+  int r1_arm = -1;
+  double totC = 0.0, totE = 0.0, totT = 0.0;
+  unsigned long long dig = 0xcbf29ce484222325ull;
+  int nstop = 0, last_b = -1;
+  uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
+  // outstanding runs
+  double q_done[kMaxOutstanding], q_C[kMaxOutstanding];
+  int q_seq[kMaxOutstanding], q_b[kMaxOutstanding];
+  uint32_t q_flags[kMaxOutstanding];                         // bit0 converged, bit1 walk
+  int nq = 0;
+
+  // a run's outcome reaching the optimiser
+  auto complete = [&](int i) {
+    const int b = q_b[i];
+    const double C = q_C[i];
+    const bool conv = q_flags[i] & 1u, walk = q_flags[i] & 2u;
+    if (conv && !(C >= best)) { best = C; best_arm = b; }
+    {                                                        // Alg. 2 Observe (NC-6)
+      const bool was_seen = (seen >> b) & 1u;
+      const ArmStat q = st[b];
+      const int cnt = was_seen ? q.cnt : 0;
+      double sh, S1, S2;
+      if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
+      else { sh = q.sh; S1 = q.S1; S2 = q.S2; }
+      int n = cnt;
+      if (a.ring_n > 0 && cp.window > 0) {
+        const int N = cp.window;
+        double *slot = &a.st_ring[(o * B + b) * (size_t)a.ring_n + (cnt % N)];
+        if (cnt >= N) {
+          const double dy = *slot - sh;
+          S1 = S1 - dy;
+          S2 = S2 - dy * dy;
+          n = N - 1;
+        }
+        *slot = C;
+      }
+      const double d = C - sh;
+      S1 = S1 + d;
+      S2 = S2 + d * d;
+      n += 1;
+      ArmStat nq_;
+      nq_.sh = sh; nq_.S1 = S1; nq_.S2 = S2; nq_.cnt = cnt + 1; nq_.pad = 0;
+      st[b] = nq_;
+      seen |= 1u << b;
+      if (n >= 2) {
+        s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
+        mature |= 1u << b;
+        n_recomp += 1;
+      }
+    }
+    if (!walk) return;
+    walk_out = false;
+    if (conv) {                                              // Alg. 3 bookkeeping
+      surv |= 1u << b;
+      if (round == 1 && (C < r1_cost || (C == r1_cost && b < r1_arm))) { r1_cost = C; r1_arm = b; }
+    }
+    bool end_round = false;
+    if (step == kStart) { step = kDown; cursor = start; }
+    else if (step == kDown) { if (conv) cursor = b; else { step = kUp; cursor = start; } }
+    else { if (conv) cursor = b; else end_round = true; }
+    if (!end_round && step == kDown && (cand & below_mask(cursor)) == 0u) { step = kUp; cursor = start; }
+    if (!end_round && step == kUp && (cand & above_mask(cursor)) == 0u) end_round = true;
+    if (end_round) {
+      if (surv == 0u) surv = 1u << start;
+      if (round == 1) {
+        cand = surv;
+        if (r1_arm >= 0) start = r1_arm;
+        surv = 0u;
+        round = 2;
+        step = kStart;
+        cursor = start;
+      } else {
+        in_ts = true;
+        ts_set = surv;
+        ts_pairs = 0u;
+        for (int k = 0; 2 * k < B; ++k)
+          if ((ts_set >> (2 * k)) & 3u) ts_pairs |= 1u << k;
+      }
+    }
+  };
+  auto complete_earliest = [&]() {                          // by (completion, submission)
+    int e = 0;
+    for (int i = 1; i < nq; ++i)
+      if (q_done[i] < q_done[e] || (q_done[i] == q_done[e] && q_seq[i] < q_seq[e])) e = i;
+    complete(e);
+    --nq;                                                    // move the last entry into slot e
+    q_done[e] = q_done[nq]; q_C[e] = q_C[nq]; q_seq[e] = q_seq[nq]; q_b[e] = q_b[nq];
+    q_flags[e] = q_flags[nq];
+  };
+
+  int s = 0;
+  U4 rw{0u, 0u, 0u, 0u};
+  for (int t = 0; t < R; ++t) {
+    double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
+    int vPacked = 0;
+    if (S > 1)
+      while ((long long)(s + 1) * R <= (long long)t * S) ++s;
+    if (active) {
+      const double tau = __ldg(arr + t);
+      for (;;) {                                             // runs finished by this submission
+        bool any = false;
+        for (int i = 0; i < nq; ++i) any |= q_done[i] <= tau;
+        if (!any) break;
+        complete_earliest();
+      }
+      while (nq >= kMaxOutstanding) complete_earliest();
+      if ((t & 3) == 0) rw = replica_words(cp.key0, cp.key1, trial, t);
+      const bool ts_dec = in_ts;
+      bool walk_issue = false;
+      int b;
+      if (!in_ts) {
+        if (walk_out) {
+          b = best_arm >= 0 ? best_arm : start;              // best-known batch size
+        } else {
+          b = (step == kStart) ? start
+            : (step == kDown) ? 31 - __clz(cand & below_mask(cursor))
+                              : __ffs(cand & above_mask(cursor)) - 1;
+          walk_issue = true;
+          walk_out = true;
+        }
+        n_prune += 1;
+      } else {
+        const uint32_t unripe = ts_set & ~mature;
+        if (unripe) {
+          b = __ffs(unripe) - 1;
+          n_forced += 1;
+        } else {
+          double bt = kInf;
+          b = -1;
+          uint32_t pm = ts_pairs;
+          int qcur = -1;
+          U4 xq{0u, 0u, 0u, 0u};
+          while (pm) {
+            const int k = __ffs(pm) - 1;
+            pm &= pm - 1u;
+            if ((k >> 1) != qcur) {
+              qcur = k >> 1;
+              xq = pair_block(cp.key0, cp.key1, trial, t, qcur);
+            }
+            double z0, z1;
+            box_muller((k & 1) ? xq.z : xq.x, (k & 1) ? xq.w : xq.y, z0, z1, a.logtab);
+            const uint32_t two = (ts_set >> (2 * k)) & 3u;
+            const double2 m0 = s_ms[(2 * k) * TPB + tid];
+            const double2 m1 = s_ms[(2 * k + 1) * TPB + tid];
+            const double th0 = fma(m0.y, z0, m0.x);
+            const bool take0 = (two & 1u) && (th0 < bt);
+            bt = take0 ? th0 : bt;
+            b = take0 ? 2 * k : b;
+            const double th1 = fma(m1.y, z1, m1.x);
+            const bool take1 = (two & 2u) && (th1 < bt);
+            bt = take1 ? th1 : bt;
+            b = take1 ? 2 * k + 1 : b;
+          }
+          n_sampled += 1;
+        }
+      }
+      const ArmConst ac = arm[b];
+      const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
+      const int E = __ldg(a.pool + ((size_t)s * B + b) * K + r);
+      const int Erun = E > 0 ? E : a.max_epochs;
+      double c0, t0, e0;
+      const bool prof_now = a.charge_profiling && !((profiled >> b) & 1u);
+      if (prof_now) { c0 = ac.cP; t0 = ac.tP; e0 = ac.eP; } else { c0 = ac.c1; t0 = ac.t1; e0 = ac.e1; }
+      profiled |= 1u << b;
+      const double em1 = (double)(Erun - 1);
+      const double Cf = c0 + em1 * ac.c1;
+      const double thr = cp.beta * best;
+      double C, Tm, En;
+      const bool stopped = Cf > thr;
+      if (stopped) {
+        C = thr;
+        if (thr <= c0) {
+          const double phi = thr / c0;
+          Tm = phi * t0;
+          En = phi * e0;
+        } else {
+          const double phi = (thr - c0) / ac.c1;
+          Tm = t0 + phi * ac.t1;
+          En = e0 + phi * ac.e1;
+        }
+      } else {
+        C = Cf;
+        Tm = t0 + em1 * ac.t1;
+        En = e0 + em1 * ac.e1;
+      }
+      const bool conv = (E > 0) && !stopped;
+      q_done[nq] = tau + Tm; q_C[nq] = C; q_seq[nq] = t; q_b[nq] = b;
+      q_flags[nq] = (conv ? 1u : 0u) | (walk_issue ? 2u : 0u);
+      ++nq;
+      const uint32_t flags = (stopped ? 1u : 0u) | (conv ? 2u : 0u) | (prof_now ? 4u : 0u) |
+                             (ts_dec ? 8u : 0u);
+      totC += C;
+      totE += En;
+      totT += Tm;
+      nstop += stopped ? 1 : 0;
+      last_b = b;
+      dig = (dig ^ (unsigned long long)(uint32_t)b) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)(uint32_t)ac.pstar) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)flags) * 0x100000001b3ull;
+      if (LOG) a.log[o * R + t] = (uint32_t)b | ((uint32_t)ac.pstar << 8) | (flags << 16);
+      vC = C;
+      vE = En;
+      vT = Tm;
+      vReg = __ldg(regret + (size_t)s * B + b);
+      vPacked = (stopped ? 1 : 0) | ((b == __ldg(optarm + s)) ? (1 << 8) : 0) | (ts_dec ? (1 << 16) : 0);
+    }
+    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked);
+  }
+  if (active) {
+    a.tot_cost[o] = totC;
+    a.tot_energy[o] = totE;
+    a.tot_time[o] = totT;
+    a.digest[o] = dig;
+    a.n_stop[o] = nstop;
+    a.final_arm[o] = last_b;
+  }
+  unsigned long long ctr[kCounters] = {
+      active ? (unsigned long long)R : 0ull, n_sampled,
+      (unsigned long long)n_sampled * __popc(ts_pairs), (unsigned long long)n_sampled * __popc(ts_set),
+      (unsigned long long)nstop, n_prune, n_forced, n_recomp,
+      (unsigned long long)n_sampled * __popc(quads_of(ts_pairs))};
+#pragma unroll
+  for (int qq = 0; qq < kCounters; ++qq) {
+    unsigned long long v = ctr[qq];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((tid & 31) == 0 && v) atomicAdd(a.counters + qq, v);
   }
 }
 

@@ -51,7 +51,8 @@ struct zeus_sim {
   int64_t shard_total = 0, max_shard = 0;
   // trace
   int S = 0, K = 0, reg_stride = 0, opt_stride = 0;
-  bool loaded = false, ran = false, any_zeus = false, any_baseline = false, any_ablation = false;
+  bool loaded = false, ran = false, any_zeus = false, any_baseline = false, any_ablation = false,
+       any_conc = false;
   int nslot = 1, tpb = 128, smem_bytes = 0, tab_bytes = 0, launches = 0, nwin = 1;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
@@ -59,7 +60,8 @@ struct zeus_sim {
   // device memory
   DevBuf d_A, d_Th, d_pool, d_cells, d_arms, d_regret, d_opt, d_optarm;
   DevBuf d_slots, d_curves, d_tot_cost, d_tot_energy, d_tot_time, d_digest, d_nstop, d_final,
-      d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket, d_ebar, d_logtab, d_pareto;
+      d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket, d_ebar, d_logtab, d_pareto,
+      d_arrivals;
   ~zeus_sim() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -144,6 +146,8 @@ void check_cells(const zeus_cell *cells, int n, Errors &E) {
       E.add(ZEUS_E_INVALID, "policy must be ZEUS_POLICY_ZEUS, _DEFAULT or _GRID_SEARCH" + at);
     if (c.ablation < 0 || c.ablation > (ZEUS_ABLATE_PRUNING | ZEUS_ABLATE_JIT))
       E.add(ZEUS_E_INVALID, "ablation must be a subset of ZEUS_ABLATE_PRUNING | ZEUS_ABLATE_JIT" + at);
+    if (c.arrivals && (c.policy != ZEUS_POLICY_ZEUS || c.ablation != 0))
+      E.add(ZEUS_E_UNSUPPORTED, "arrivals are supported for the Zeus policy without ablations" + at);
   }
 }
 
@@ -252,6 +256,19 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
   s->R = opts->recurrences > 0 ? opts->recurrences : 2 * s->B * s->P;
   s->log_mode = opts->log_mode;
   s->layout = opts->layout;
+  {                                      // arrival schedules: finite, non-decreasing (R-Q31)
+    Errors EA;
+    for (int i = 0; i < num_cells; ++i) {
+      const double *ar = cells[i].arrivals;
+      if (!ar) continue;
+      for (int t = 0; t < s->R; ++t)
+        if (!std::isfinite(ar[t]) || (t > 0 && ar[t] < ar[t - 1])) {
+          EA.add(ZEUS_E_INVALID, "arrivals must be finite and non-decreasing (cell " + std::to_string(i) + ")");
+          break;
+        }
+    }
+    if (EA.code != ZEUS_OK) { delete s; return fail(nullptr, EA.code, EA.s); }
+  }
   for (int i = 0; i < num_cells; ++i) s->wmax = std::max(s->wmax, (int)cells[i].window);
   int64_t off = 0;
   for (int i = 0; i < num_cells; ++i) {
@@ -264,6 +281,8 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     p.window = c.window;
     p.policy = c.policy;
     p.ablation = c.ablation;
+    p.conc = c.arrivals != nullptr;
+    s->any_conc |= p.conc != 0;
     s->any_ablation |= c.ablation != 0 && c.policy == ZEUS_POLICY_ZEUS;
     s->any_zeus |= c.policy == ZEUS_POLICY_ZEUS;
     s->any_baseline |= c.policy != ZEUS_POLICY_ZEUS;
@@ -314,6 +333,17 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     std::string m = std::string("create: ") + cudaGetErrorString(e);
     delete s;
     return fail(nullptr, ZEUS_E_CUDA, m);
+  }
+  if (s->any_conc) {
+    std::vector<double> arr((size_t)num_cells * s->R, 0.0);
+    for (int i = 0; i < num_cells; ++i)
+      if (cells[i].arrivals) std::memcpy(&arr[(size_t)i * s->R], cells[i].arrivals, (size_t)s->R * 8);
+    if ((e = s->d_arrivals.alloc(arr.size() * 8)) != cudaSuccess ||
+        (e = cudaMemcpy(s->d_arrivals.p, arr.data(), arr.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess) {
+      std::string m = std::string("arrivals: ") + cudaGetErrorString(e);
+      delete s;
+      return fail(nullptr, ZEUS_E_CUDA, m);
+    }
   }
   zs::log_table_kernel<<<1, 128>>>(s->d_logtab.as<double2>());   // the sampler's log table
   if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
@@ -421,6 +451,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
       for (int ph = 0; ph < 3; ++ph)
         for (int ab = 0; ab < 2; ++ab)
           ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph, ab), s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::concurrent_kernel<false>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::concurrent_kernel<true>, s->device));
   s->loaded = true;
   return ZEUS_OK;
 }
@@ -464,6 +496,37 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     const dim3 grid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
     if (s->log_mode) zs::baseline_kernel<true><<<grid, 128, 0, st>>>(b);
     else zs::baseline_kernel<false><<<grid, 128, 0, st>>>(b);
+    ZS_CUDA(s, cudaGetLastError());
+    s->launches += 1;
+  }
+  if (s->max_shard > 0 && s->R > 0 && s->any_conc) {
+    zs::ConcArgs c{};
+    c.cells = s->d_cells.as<zs::CellParam>();
+    c.arms = s->d_arms.as<zs::ArmConst>();
+    c.regret = s->d_regret.as<double>();
+    c.opt_arm = s->d_optarm.as<int32_t>();
+    c.pool = s->d_pool.as<int32_t>();
+    c.logtab = s->d_logtab.as<double2>();
+    c.arrivals = s->d_arrivals.as<double>();
+    c.curve_slots = s->d_slots.as<double>();
+    c.tot_cost = s->d_tot_cost.as<double>();
+    c.tot_energy = s->d_tot_energy.as<double>();
+    c.tot_time = s->d_tot_time.as<double>();
+    c.digest = s->d_digest.as<unsigned long long>();
+    c.n_stop = s->d_nstop.as<int32_t>();
+    c.final_arm = s->d_final.as<int32_t>();
+    c.log = s->d_log.as<uint32_t>();
+    c.counters = s->d_counters.as<unsigned long long>();
+    c.st = s->d_st.as<zs::ArmStat>();
+    c.st_ring = s->d_st_ring.as<double>();
+    c.ring_n = s->wmax;
+    c.B = s->B; c.S = s->S; c.K = s->K; c.R = s->R; c.max_epochs = s->max_epochs;
+    c.charge_profiling = s->charge_profiling; c.b0 = s->b0; c.nslot = s->nslot;
+    c.reg_stride = s->reg_stride; c.opt_stride = s->opt_stride;
+    const size_t smem = (size_t)128 * (((s->B + 1) & ~1) * 16);
+    const dim3 grid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
+    if (s->log_mode) zs::concurrent_kernel<true><<<grid, 128, smem, st>>>(c);
+    else zs::concurrent_kernel<false><<<grid, 128, smem, st>>>(c);
     ZS_CUDA(s, cudaGetLastError());
     s->launches += 1;
   }

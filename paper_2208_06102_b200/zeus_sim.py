@@ -44,7 +44,8 @@ class zeus_job(C.Structure):
 class zeus_cell(C.Structure):
     _fields_ = [("eta", C.c_double), ("beta", C.c_double), ("window", C.c_int32),
                 ("prior_mean", C.c_double), ("prior_var", C.c_double), ("seed", C.c_uint64),
-                ("trials", C.c_int64), ("policy", C.c_int32), ("ablation", C.c_int32)]
+                ("trials", C.c_int64), ("policy", C.c_int32), ("ablation", C.c_int32),
+                ("arrivals", C.POINTER(C.c_double))]
 
 
 class zeus_run_opts(C.Structure):
@@ -157,10 +158,18 @@ class Simulation:
                        int(workload["b0"]), len(pl), pl.ctypes.data_as(C.POINTER(C.c_double)),
                        float(workload["max_power"]), int(workload["max_epochs"]),
                        int(workload.get("charge_profiling", 1)))
-        cs = [zeus_cell(float(c["eta"]), float(c["beta"]), int(c.get("window", 0)),
-                        float(c.get("prior_mean", 0.0)), float(c.get("prior_var", math.inf)),
-                        int(c.get("seed", 0)), int(trials), int(c.get("policy", 0)),
-                        int(c.get("ablation", 0))) for c in cells]
+        cs = []
+        for c in cells:
+            arr = c.get("arrivals")
+            ptr = None
+            if arr is not None:
+                arr = np.ascontiguousarray(arr, dtype=np.float64)
+                self._keep.append(arr)
+                ptr = arr.ctypes.data_as(C.POINTER(C.c_double))
+            cs.append(zeus_cell(float(c["eta"]), float(c["beta"]), int(c.get("window", 0)),
+                                float(c.get("prior_mean", 0.0)), float(c.get("prior_var", math.inf)),
+                                int(c.get("seed", 0)), int(trials), int(c.get("policy", 0)),
+                                int(c.get("ablation", 0)), ptr))
         opts = zeus_run_opts(C.sizeof(zeus_run_opts), int(recurrences), int(shard[0]),
                              int(shard[1]), 1 if log else 0, int(layout))
         self.h = zeus_sim_create(job, cs, opts, device)

@@ -75,7 +75,7 @@ def _job(zs, **kw):
 
 def test_create_reports_every_violation_without_gpu(zs):
     job, keep = _job(zs, bs=[8, 8, 4], b0=7, pl=[200.0, 100.0], mp=50.0, max_epochs=0)
-    cells = [zs.zeus_cell(1.5, 1.0, 1, 0.0, -1.0, 1, -5, 7, 9)]
+    cells = [zs.zeus_cell(1.5, 1.0, 1, 0.0, -1.0, 1, -5, 7, 9, None)]
     opts = zs.zeus_run_opts(C.sizeof(zs.zeus_run_opts), -1, 0, -1, 3, 0)
     with pytest.raises(zs.ZeusError) as e:
         zs.zeus_sim_create(job, cells, opts)
@@ -90,7 +90,7 @@ def test_create_reports_every_violation_without_gpu(zs):
 
 def test_unsupported_sizes(zs):
     job, keep = _job(zs, bs=list(range(8, 8 * 34, 8)), b0=0)
-    cells = [zs.zeus_cell(0.5, 2.0, 0, 0.0, math.inf, 1, 10, 0, 0)]
+    cells = [zs.zeus_cell(0.5, 2.0, 0, 0.0, math.inf, 1, 10, 0, 0, None)]
     opts = zs.zeus_run_opts(C.sizeof(zs.zeus_run_opts), 10, 0, -1, 0, 0)
     with pytest.raises(zs.ZeusError) as e:
         zs.zeus_sim_create(job, cells, opts)
@@ -100,7 +100,7 @@ def test_unsupported_sizes(zs):
 def test_abi_guard(zs):
     job, keep = _job(zs)
     job.struct_size = 3
-    cells = [zs.zeus_cell(0.5, 2.0, 0, 0.0, math.inf, 1, 10, 0, 0)]
+    cells = [zs.zeus_cell(0.5, 2.0, 0, 0.0, math.inf, 1, 10, 0, 0, None)]
     opts = zs.zeus_run_opts(C.sizeof(zs.zeus_run_opts), 10, 0, -1, 0, 0)
     with pytest.raises(zs.ZeusError, match="struct_size"):
         zs.zeus_sim_create(job, cells, opts)
@@ -113,7 +113,7 @@ def test_no_cpu_fallback(zs):
     if torch.cuda.is_available():
         pytest.skip("GPU present")
     job, keep = _job(zs)
-    cells = [zs.zeus_cell(0.5, 2.0, 0, 0.0, math.inf, 1, 10, 0, 0)]
+    cells = [zs.zeus_cell(0.5, 2.0, 0, 0.0, math.inf, 1, 10, 0, 0, None)]
     opts = zs.zeus_run_opts(C.sizeof(zs.zeus_run_opts), 10, 0, -1, 0, 0)
     with pytest.raises(zs.ZeusError) as e:
         zs.zeus_sim_create(job, cells, opts)

@@ -313,3 +313,19 @@ def test_f2_ablations(zs, oracle):
         for ci, c in enumerate(job.cells):
             compare_cell(oracle, g, job.workload, c, ci, np.arange(job.trials), job.recurrences,
                          job.trials, logs=True)
+
+
+def test_f3_concurrent_submissions(zs, oracle):
+    """concurrent submissions under Poisson arrival schedules (§4.4
+    P:L634-646) next to the sequential cell in one launch; every trial bit-exact."""
+    for job in synth.config("f3", trials=2000)[:3]:
+        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True)
+        for ci, c in enumerate(job.cells):
+            compare_cell(oracle, g, job.workload, c, ci, np.arange(job.trials), job.recurrences,
+                         job.trials, logs=True)
+    # the drift config with a window, heavy overlap
+    (job,) = synth.config("cfg4_38", trials=1500)
+    c = dict(job.cells[0], arrivals=synth.arrival_schedule(job.workload, job.recurrences, 0.3, 5))
+    g = run_gpu(zs, job.workload, [c], job.trials, job.recurrences, log=True)
+    compare_cell(oracle, g, job.workload, c, 0, np.arange(job.trials), job.recurrences, job.trials,
+                 logs=True)

@@ -213,8 +213,12 @@ def main():
 
         import torch
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        if args.impl == "ours":
+            torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+        # NCCL over NVLink for the curve all-reduce; ZEUS_DIST_BACKEND=gloo lets several ranks
+        # share one GPU when the multi-rank path itself is under test
+        backend = os.environ.get("ZEUS_DIST_BACKEND", "nccl" if args.impl == "ours" else "gloo")
+        dist.init_process_group(backend)
     if args.impl == "reference":
         reference_main(args, rank, world)
         if dist:
@@ -227,6 +231,7 @@ def main():
     from paper_2208_06102_b200.zeus_sim import Simulation
 
     build.build()
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     jobs = synth.config(args.config, trials=args.trials)

@@ -17,6 +17,13 @@
 
 
 
+#ifndef ZS_SLIM_B
+#define ZS_SLIM_B 1
+#endif
+#ifndef ZS_QUAD_LOOP
+#define ZS_QUAD_LOOP 1
+#endif
+
 namespace zs {
 
 constexpr int kQ = 7;             // curve quantities
@@ -445,6 +452,33 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
           };
           // pairs 2q and 2q+1 share one Philox block: it is drawn when the walk enters a new
           // quad (warp-uniform in phase B, where lanes are grouped by count and parity)
+#if ZS_QUAD_LOOP
+          if (PHASE == 2) {
+            // quad loop: the two pairs of one Philox block are transformed side by side (two
+            // independent Box-Muller chains in one basic block); which pairs of a quad a lane
+            // needs is warp-uniform here (lanes grouped by pair count and parity)
+            uint32_t qm = quads_of(ts_pairs);
+            while (qm) {
+              const int qd = __ffs(qm) - 1;
+              qm &= qm - 1u;
+              const U4 xq = pair_block(cp.key0, cp.key1, trial, t, qd);
+              const uint32_t need = (ts_pairs >> (2 * qd)) & 3u;
+              if (need == 3u) {
+                double za0, za1, zb0, zb1;
+                box_muller(xq.x, xq.y, za0, za1, logtab);
+                box_muller(xq.z, xq.w, zb0, zb1, logtab);
+                consider(2 * qd, za0, za1);
+                consider(2 * qd + 1, zb0, zb1);
+              } else {
+                const bool hi = need == 2u;
+                double z0, z1;
+                box_muller(hi ? xq.z : xq.x, hi ? xq.w : xq.y, z0, z1, logtab);
+                consider(2 * qd + (hi ? 1 : 0), z0, z1);
+              }
+            }
+            pm = 0u;
+          }
+#endif
           int qcur = -1;
           U4 xq{0u, 0u, 0u, 0u};
           while (pm) {
@@ -461,8 +495,9 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
           n_sampled += 1;
         }
       }
-      // Observe statistics of arm b: issue the load now, consume after the curves
-      was_seen = (seen >> b) & 1u;
+      // Observe statistics of arm b: issue the load now, consume after the curves.  In the
+      // Thompson phase every survivor was run (and observed, and profiled) during pruning.
+      was_seen = (ZS_SLIM_B && PHASE == 2 && !ABL) ? true : ((seen >> b) & 1u);
       q = st[b];
       const ArmConst ac = arm[b];
       // the power limit accompanying b and its per-epoch cost/time/energy
@@ -484,7 +519,8 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       const int E = pool[((size_t)s * B + b) * K + r];
       const int Erun = E > 0 ? E : a.max_epochs;
       double c0, t0, e0;
-      const bool prof_now = !no_jit && a.charge_profiling && !((profiled >> b) & 1u);
+      const bool prof_now = !(ZS_SLIM_B && PHASE == 2 && !ABL) && !no_jit && a.charge_profiling &&
+                            !((profiled >> b) & 1u);
       if (prof_now) { c0 = ac.cP; t0 = ac.tP; e0 = ac.eP; } else { c0 = c1b; t0 = t1b; e0 = e1b; }
       profiled |= 1u << b;
       const double em1 = (double)(Erun - 1);

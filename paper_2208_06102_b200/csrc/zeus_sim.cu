@@ -442,6 +442,9 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
     ZS_CUDA(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, tpb, bytes));
     const int warps = blocks * tpb / 32;
     if (warps > best_warps) { best_warps = warps; s->tpb = tpb; s->smem_bytes = (int)bytes; }
+#ifdef ZS_EXPERIMENT_SMEM_PAD
+    s->smem_bytes += ZS_EXPERIMENT_SMEM_PAD;   // occupancy experiments only
+#endif
   }
   if (best_warps <= 0) return fail(s, ZEUS_E_UNSUPPORTED, "no launch shape fits shared memory");
   // the attribute is per function (process-wide): grant the device maximum once, so handles

@@ -8,6 +8,13 @@ from paper_2208_06102_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "u1": ([], []),
+    "slim": (["ZS_SLIM_B=1"], []),
+    "slim_b6": (["ZS_SLIM_B=1", "ZS_P2_MIN_BLOCKS=6"], []),
+    "b6": (["ZS_P2_MIN_BLOCKS=6"], []),
+    "occ16": (["ZS_EXPERIMENT_SMEM_PAD=12000"], []),
+    "occ12": (["ZS_EXPERIMENT_SMEM_PAD=40000"], []),
+    "quad": (["ZS_QUAD_LOOP=1"], []),
+    "quad_r96": (["ZS_QUAD_LOOP=1", "ZS_MAXNREG=96"], []),
     "carve0": (["ZS_DEFAULT_CARVEOUT"], []),
     "mb6": (["ZS_P2_MIN_BLOCKS=6"], []),
     "mb6c0": (["ZS_P2_MIN_BLOCKS=6", "ZS_DEFAULT_CARVEOUT"], []),

@@ -11,8 +11,8 @@ VARIANTS = {
     "slim": (["ZS_SLIM_B=1"], []),
     "slim_b6": (["ZS_SLIM_B=1", "ZS_P2_MIN_BLOCKS=6"], []),
     "b6": (["ZS_P2_MIN_BLOCKS=6"], []),
+    "occ20": (["ZS_EXPERIMENT_SMEM_PAD=2500"], []),
     "occ16": (["ZS_EXPERIMENT_SMEM_PAD=12000"], []),
-    "occ12": (["ZS_EXPERIMENT_SMEM_PAD=40000"], []),
     "quad": (["ZS_QUAD_LOOP=1"], []),
     "quad_r96": (["ZS_QUAD_LOOP=1", "ZS_MAXNREG=96"], []),
     "carve0": (["ZS_DEFAULT_CARVEOUT"], []),

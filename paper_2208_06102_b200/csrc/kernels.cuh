@@ -497,7 +497,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       }
       // Observe statistics of arm b: issue the load now, consume after the curves.  In the
       // Thompson phase every survivor was run (and observed, and profiled) during pruning.
-      was_seen = (ZS_SLIM_B && PHASE == 2 && !ABL) ? true : ((seen >> b) & 1u);
+      was_seen = (ZS_SLIM_B && PHASE == 2 && !ABL && !WINDOWED) ? true : ((seen >> b) & 1u);
       q = st[b];
       const ArmConst ac = arm[b];
       // the power limit accompanying b and its per-epoch cost/time/energy
@@ -519,7 +519,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       const int E = pool[((size_t)s * B + b) * K + r];
       const int Erun = E > 0 ? E : a.max_epochs;
       double c0, t0, e0;
-      const bool prof_now = !(ZS_SLIM_B && PHASE == 2 && !ABL) && !no_jit && a.charge_profiling &&
+      const bool prof_now = !(ZS_SLIM_B && PHASE == 2 && !ABL && !WINDOWED) && !no_jit && a.charge_profiling &&
                             !((profiled >> b) & 1u);
       if (prof_now) { c0 = ac.cP; t0 = ac.tP; e0 = ac.eP; } else { c0 = c1b; t0 = t1b; e0 = e1b; }
       profiled |= 1u << b;
@@ -670,6 +670,284 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
 // Regrouping is done within windows of kRegroupWindow consecutive trials: warps still get
 // (almost) uniform draw counts, and a window's Observe records (~1 MB at B = 16) stay on
 // one or two 2 MB pages, so phase B's scattered lanes do not thrash the TLB.
+// ------------------------------------------------------------------ lane-group layout
+// W lanes per trial (the north star's "one warp per trial" for latency-bound launches: when a
+// launch has too few trials to fill the GPU one thread per trial, W lanes share one trial).
+// Every lane of a group carries the trial's scalar state and runs its serial steps (the same
+// bits in every lane); the Thompson draw is split across the group -- lane l transforms the
+// survivor pairs of rank l, l+W, ... -- and a segmented shuffle argmin over (theta, arm) keeps
+// the strict-<, lowest-arm rule (NC-4).  Lane 0 writes the shared state and the outputs.
+template <int W, bool WINDOWED, bool LOG>
+__global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  constexpr int TPB = 128, TPG = TPB / W;                 // trials per block
+  const int cell = blockIdx.y;
+  const CellParam cp = a.cells[cell];
+  const int tid = threadIdx.x;
+  const int g = tid / W, l = tid % W;
+  const int64_t j0 = (int64_t)blockIdx.x * TPG;
+  if (j0 >= cp.n || cp.policy != 0 || cp.conc) return;
+
+  const TabLayout L(a.B, a.S, a.K);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    const uint32_t b_arm = a.B * (uint32_t)sizeof(ArmConst);
+    const uint32_t b_reg = a.S * a.B * 8u;
+    const uint32_t b_opt = a.S * 4u;
+    const uint32_t b_pool = a.S * a.B * a.K * 4u;
+    const uint32_t p_arm = (b_arm + 15u) & ~15u, p_reg = (b_reg + 15u) & ~15u;
+    const uint32_t p_opt = (b_opt + 15u) & ~15u, p_pool = (b_pool + 15u) & ~15u;
+    mbar_expect_tx(&mbar, p_arm + p_reg + p_opt + p_pool + kLogTab * 16u);
+    tma_bulk_load(smem + L.logtab, a.logtab, kLogTab * 16u, &mbar);
+    tma_bulk_load(smem + L.arms, a.arms + (size_t)cell * a.B, p_arm, &mbar);
+    tma_bulk_load(smem + L.regret, a.regret + (size_t)cell * a.reg_stride, p_reg, &mbar);
+    tma_bulk_load(smem + L.optarm, a.opt_arm + (size_t)cell * a.opt_stride, p_opt, &mbar);
+    tma_bulk_load(smem + L.pool, a.pool, p_pool, &mbar);
+  }
+  __syncthreads();
+  mbar_wait(&mbar, 0);
+
+  const ArmConst *arm = reinterpret_cast<const ArmConst *>(smem + L.arms);
+  const double *regret = reinterpret_cast<const double *>(smem + L.regret);
+  const int32_t *optarm = reinterpret_cast<const int32_t *>(smem + L.optarm);
+  const int32_t *pool = reinterpret_cast<const int32_t *>(smem + L.pool);
+  const double2 *logtab = reinterpret_cast<const double2 *>(smem + L.logtab);
+  const int B = a.B, R = a.R, S = a.S, K = a.K;
+  double2 *s_ms = reinterpret_cast<double2 *>(smem + a.tab_bytes);   // [arm][trial of block]
+  const int64_t jj = j0 + g;
+  const bool active = jj < cp.n;
+  const bool leader = l == 0;
+  const int64_t trial = cp.begin + jj;
+  const size_t o = (size_t)(cp.out_off + (active ? jj : 0));
+  ArmStat *st = a.st + o * B;
+  const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
+  double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+
+  uint32_t profiled = 0, seen = 0, mature = 0;
+  double best = kInf;
+  bool in_ts = false;
+  int round = 1, step = kStart, start = a.b0, cursor = a.b0;
+  const uint32_t all_arms = (B == 32) ? 0xffffffffu : ((1u << B) - 1u);
+  uint32_t cand = all_arms, surv = 0, ts_set = 0, ts_pairs = 0;
+  double r1_cost = kInf;
+  int r1_arm = -1;
+  double totC = 0.0, totE = 0.0, totT = 0.0;
+  unsigned long long dig = 0xcbf29ce484222325ull;
+  int nstop = 0, last_b = -1;
+  uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
+  int s = 0;
+  U4 rw{0u, 0u, 0u, 0u};
+  for (int t = 0; t < R; ++t) {
+    double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
+    int vPacked = 0;
+    if (S > 1)
+      while ((long long)(s + 1) * R <= (long long)t * S) ++s;
+    // ---------------- step 2: decide b_t (pruning walk / forced / Thompson draw)
+    int b = 0;
+    const bool ts_dec = in_ts;
+    bool sampled = false;
+    if (active) {
+      if ((t & 3) == 0) rw = replica_words(cp.key0, cp.key1, trial, t);
+      if (!in_ts) {
+        b = (step == kStart) ? start
+          : (step == kDown) ? 31 - __clz(cand & below_mask(cursor))
+                            : __ffs(cand & above_mask(cursor)) - 1;
+        n_prune += 1;
+      } else {
+        const uint32_t unripe = ts_set & ~mature;
+        if (unripe) {
+          b = __ffs(unripe) - 1;
+          n_forced += 1;
+        } else {
+          sampled = true;
+          n_sampled += 1;
+        }
+      }
+    }
+    // the group's share of the draw: lane l takes the survivor pairs of rank l, l+W, ...
+    double bt = kInf;
+    int bb = -1;
+    if (sampled) {
+      uint32_t pm = ts_pairs;
+      for (int i = 0; i < l && pm; ++i) pm &= pm - 1u;
+      while (pm) {
+        const int k = __ffs(pm) - 1;
+        const U4 xq = pair_block(cp.key0, cp.key1, trial, t, k >> 1);
+        double z0, z1;
+        box_muller((k & 1) ? xq.z : xq.x, (k & 1) ? xq.w : xq.y, z0, z1, logtab);
+        const uint32_t two = (ts_set >> (2 * k)) & 3u;
+        const double2 m0 = s_ms[(2 * k) * TPG + g];
+        const double2 m1 = s_ms[(2 * k + 1) * TPG + g];
+        const double th0 = fma(m0.y, z0, m0.x);
+        const bool take0 = (two & 1u) && (th0 < bt);
+        bt = take0 ? th0 : bt;
+        bb = take0 ? 2 * k : bb;
+        const double th1 = fma(m1.y, z1, m1.x);
+        const bool take1 = (two & 2u) && (th1 < bt);
+        bt = take1 ? th1 : bt;
+        bb = take1 ? 2 * k + 1 : bb;
+        for (int i = 0; i < W && pm; ++i) pm &= pm - 1u;
+      }
+    }
+#pragma unroll
+    for (int off = W / 2; off > 0; off >>= 1) {             // segmented (theta, arm) argmin
+      const double ot = __shfl_xor_sync(0xffffffffu, bt, off, W);
+      const int ob = __shfl_xor_sync(0xffffffffu, bb, off, W);
+      const bool take = ob >= 0 && (bb < 0 || ot < bt || (ot == bt && ob < bb));
+      bt = take ? ot : bt;
+      bb = take ? ob : bb;
+    }
+    if (sampled) b = bb;
+    bool was_seen = false;
+    ArmStat q;
+    double C = 0.0;
+    if (active) {
+      was_seen = (seen >> b) & 1u;
+      q = st[b];
+      const ArmConst ac = arm[b];
+      const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
+      const int E = pool[((size_t)s * B + b) * K + r];
+      const int Erun = E > 0 ? E : a.max_epochs;
+      double c0, t0, e0;
+      const bool prof_now = a.charge_profiling && !((profiled >> b) & 1u);
+      if (prof_now) { c0 = ac.cP; t0 = ac.tP; e0 = ac.eP; } else { c0 = ac.c1; t0 = ac.t1; e0 = ac.e1; }
+      profiled |= 1u << b;
+      const double em1 = (double)(Erun - 1);
+      const double Cf = c0 + em1 * ac.c1;
+      const double thr = cp.beta * best;
+      double Tm, En;
+      const bool stopped = Cf > thr;
+      if (stopped) {
+        C = thr;
+        if (thr <= c0) {
+          const double phi = thr / c0;
+          Tm = phi * t0;
+          En = phi * e0;
+        } else {
+          const double phi = (thr - c0) / ac.c1;
+          Tm = t0 + phi * ac.t1;
+          En = e0 + phi * ac.e1;
+        }
+      } else {
+        C = Cf;
+        Tm = t0 + em1 * ac.t1;
+        En = e0 + em1 * ac.e1;
+      }
+      const bool conv = (E > 0) && !stopped;
+      if (conv && !(C >= best)) best = C;
+      if (!in_ts) {                                          // Alg. 3 bookkeeping
+        if (conv) {
+          surv |= 1u << b;
+          if (round == 1 && (C < r1_cost || (C == r1_cost && b < r1_arm))) { r1_cost = C; r1_arm = b; }
+        }
+        bool end_round = false;
+        if (step == kStart) { step = kDown; cursor = start; }
+        else if (step == kDown) { if (conv) cursor = b; else { step = kUp; cursor = start; } }
+        else { if (conv) cursor = b; else end_round = true; }
+        if (!end_round && step == kDown && (cand & below_mask(cursor)) == 0u) { step = kUp; cursor = start; }
+        if (!end_round && step == kUp && (cand & above_mask(cursor)) == 0u) end_round = true;
+        if (end_round) {
+          if (surv == 0u) surv = 1u << start;
+          if (round == 1) {
+            cand = surv;
+            if (r1_arm >= 0) start = r1_arm;
+            surv = 0u;
+            round = 2;
+            step = kStart;
+            cursor = start;
+          } else {
+            in_ts = true;
+            ts_set = surv;
+            ts_pairs = 0u;
+            for (int k = 0; 2 * k < B; ++k)
+              if ((ts_set >> (2 * k)) & 3u) ts_pairs |= 1u << k;
+          }
+        }
+      }
+      const uint32_t flags = (stopped ? 1u : 0u) | (conv ? 2u : 0u) | (prof_now ? 4u : 0u) |
+                             (ts_dec ? 8u : 0u);
+      totC += C;
+      totE += En;
+      totT += Tm;
+      nstop += stopped ? 1 : 0;
+      last_b = b;
+      dig = (dig ^ (unsigned long long)(uint32_t)b) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)(uint32_t)ac.pstar) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)flags) * 0x100000001b3ull;
+      if (leader) {
+        if (LOG) a.log[o * R + t] = (uint32_t)b | ((uint32_t)ac.pstar << 8) | (flags << 16);
+        vC = C;
+        vE = En;
+        vT = Tm;
+        vReg = regret[s * B + b];
+        vPacked = (stopped ? 1 : 0) | ((b == optarm[s]) ? (1 << 8) : 0) | (ts_dec ? (1 << 16) : 0);
+      }
+    }
+    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked);
+    if (active) {                                            // Alg. 2 Observe (NC-6)
+      const int cnt = was_seen ? q.cnt : 0;
+      double sh, S1, S2;
+      if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
+      else { sh = q.sh; S1 = q.S1; S2 = q.S2; }
+      int n = cnt;
+      if (WINDOWED && cp.window > 0) {
+        const int N = cp.window;
+        double *slot = &a.st_ring[(o * B + b) * (size_t)a.ring_n + (cnt % N)];
+        const double y = *slot;
+        if (cnt >= N) {
+          const double dy = y - sh;
+          S1 = S1 - dy;
+          S2 = S2 - dy * dy;
+          n = N - 1;
+        }
+        if (leader) *slot = C;
+      }
+      const double d = C - sh;
+      S1 = S1 + d;
+      S2 = S2 + d * d;
+      n += 1;
+      if (leader) {
+        ArmStat nq;
+        nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
+        st[b] = nq;
+      }
+      seen |= 1u << b;
+      if (n >= 2) {
+        const double2 ms = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
+        if (leader) s_ms[b * TPG + g] = ms;
+        mature |= 1u << b;
+        n_recomp += 1;
+      }
+    }
+    __syncwarp();                                            // lane 0's stores before the next draw
+  }
+  if (active && leader) {
+    a.tot_cost[o] = totC;
+    a.tot_energy[o] = totE;
+    a.tot_time[o] = totT;
+    a.digest[o] = dig;
+    a.n_stop[o] = nstop;
+    a.final_arm[o] = last_b;
+  }
+  const bool cnt_lane = active && leader;
+  unsigned long long ctr[kCounters] = {
+      cnt_lane ? (unsigned long long)R : 0ull, cnt_lane ? n_sampled : 0u,
+      cnt_lane ? (unsigned long long)n_sampled * __popc(ts_pairs) : 0ull,
+      cnt_lane ? (unsigned long long)n_sampled * __popc(ts_set) : 0ull,
+      cnt_lane ? (unsigned long long)nstop : 0ull, cnt_lane ? n_prune : 0u,
+      cnt_lane ? n_forced : 0u, cnt_lane ? n_recomp : 0u,
+      cnt_lane ? (unsigned long long)n_sampled * __popc(quads_of(ts_pairs)) : 0ull};
+#pragma unroll
+  for (int qq = 0; qq < kCounters; ++qq) {
+    unsigned long long v = ctr[qq];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((tid & 31) == 0 && v) atomicAdd(a.counters + qq, v);
+  }
+}
+
 // bucket offsets: exclusive scan of each (cell, window) histogram, offset by the window base
 __global__ void bucket_scan_kernel(int32_t *bucket, int ncells, int nwin) {
   const int64_t cw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;

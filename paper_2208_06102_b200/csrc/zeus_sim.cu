@@ -53,7 +53,7 @@ struct zeus_sim {
   int S = 0, K = 0, reg_stride = 0, opt_stride = 0;
   bool loaded = false, ran = false, any_zeus = false, any_baseline = false, any_ablation = false,
        any_conc = false;
-  int nslot = 1, tpb = 128, smem_bytes = 0, tab_bytes = 0, launches = 0, nwin = 1;
+  int nslot = 1, tpb = 128, smem_bytes = 0, tab_bytes = 0, launches = 0, nwin = 1, group_w = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
   std::string err;
@@ -190,6 +190,33 @@ cudaError_t grant_max_smem(const void *fn, int device, int *granted = nullptr) {
 #endif
 }
 
+// replay_group_kernel<W, WINDOWED, LOG> by runtime flags
+template <int W>
+void launch_group_w(bool windowed, bool log, dim3 grid, size_t smem, cudaStream_t st,
+                    const zs::ReplayArgs &a) {
+  if (windowed) {
+    if (log) zs::replay_group_kernel<W, true, true><<<grid, 128, smem, st>>>(a);
+    else zs::replay_group_kernel<W, true, false><<<grid, 128, smem, st>>>(a);
+  } else {
+    if (log) zs::replay_group_kernel<W, false, true><<<grid, 128, smem, st>>>(a);
+    else zs::replay_group_kernel<W, false, false><<<grid, 128, smem, st>>>(a);
+  }
+}
+void launch_group(int w, bool windowed, bool log, dim3 grid, size_t smem, cudaStream_t st,
+                  const zs::ReplayArgs &a) {
+  if (w == 2) launch_group_w<2>(windowed, log, grid, smem, st, a);
+  else if (w == 4) launch_group_w<4>(windowed, log, grid, smem, st, a);
+  else launch_group_w<8>(windowed, log, grid, smem, st, a);
+}
+template <int W>
+cudaError_t grant_group(int device) {
+  cudaError_t e;
+  if ((e = grant_max_smem((const void *)zs::replay_group_kernel<W, false, false>, device)) != cudaSuccess) return e;
+  if ((e = grant_max_smem((const void *)zs::replay_group_kernel<W, false, true>, device)) != cudaSuccess) return e;
+  if ((e = grant_max_smem((const void *)zs::replay_group_kernel<W, true, false>, device)) != cudaSuccess) return e;
+  return grant_max_smem((const void *)zs::replay_group_kernel<W, true, true>, device);
+}
+
 void launch_step1(zeus_sim *s, cudaStream_t st) {
   zs::Step1Args a{};
   a.A = s->d_A.as<double>();
@@ -229,7 +256,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     if (opts->shard_begin < 0) E.add(ZEUS_E_INVALID, "shard_begin < 0");
     if (opts->shard_end >= 0 && opts->shard_end < opts->shard_begin) E.add(ZEUS_E_INVALID, "shard_end < shard_begin");
     if (opts->log_mode != 0 && opts->log_mode != 1) E.add(ZEUS_E_INVALID, "log_mode must be 0 or 1");
-    if (opts->layout < 0 || opts->layout > 2) E.add(ZEUS_E_INVALID, "layout must be 0, 1 or 2");
+    if (opts->layout < 0 || opts->layout > 3) E.add(ZEUS_E_INVALID, "layout must be 0, 1, 2 or 3");
   }
   if (E.code != ZEUS_OK) return fail(nullptr, E.code, E.s);
 
@@ -447,6 +474,25 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
 #endif
   }
   if (best_warps <= 0) return fail(s, ZEUS_E_UNSUPPORTED, "no launch shape fits shared memory");
+  // lane groups (layout 3, or auto when one thread per trial cannot fill the GPU): W lanes per
+  // trial, W = the power of two covering about two survivor pairs per lane
+  {
+    int64_t zeus_trials = 0;
+    for (const auto &p : s->cpar) if (p.policy == ZEUS_POLICY_ZEUS && !p.conc) zeus_trials += p.n;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+    const int pairs = (B + 1) / 2;
+    const int w = pairs <= 2 ? 2 : pairs <= 8 ? 4 : 8;
+    // measured: lane groups win only when the grouped launch fills at most a quarter of one
+    // wave (CFG1 +18 %); beyond that the serial work each lane repeats costs more than the
+    // split draw saves (CFG2 -35 %, CFG4 -70 %)
+    const bool small = zeus_trials * w * 4 <= (int64_t)sms * best_warps * 32;
+    s->group_w = 0;
+    if (!s->any_ablation && (s->layout == 3 || (s->layout == 0 && small))) {
+      const size_t gbytes = (size_t)L.bytes + (size_t)(128 / w) * (((B + 1) & ~1) * 16);
+      if (gbytes <= 200 * 1024) s->group_w = w;
+    }
+  }
   // the attribute is per function (process-wide): grant the device maximum once, so handles
   // with different footprints can launch concurrently; each launch passes its own size
   for (int w = 0; w < 2; ++w)
@@ -454,6 +500,9 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
       for (int ph = 0; ph < 3; ++ph)
         for (int ab = 0; ab < 2; ++ab)
           ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph, ab), s->device));
+  ZS_CUDA(s, grant_group<2>(s->device));
+  ZS_CUDA(s, grant_group<4>(s->device));
+  ZS_CUDA(s, grant_group<8>(s->device));
   ZS_CUDA(s, grant_max_smem((const void *)zs::concurrent_kernel<false>, s->device));
   ZS_CUDA(s, grant_max_smem((const void *)zs::concurrent_kernel<true>, s->device));
   s->loaded = true;
@@ -573,8 +622,15 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     a.opt = s->d_opt.as<double>();
     a.P = s->P;
     a.MP = s->MP;
-    const bool two_phase = s->layout != 1 && a.t_split < s->R;
-    if (!two_phase) {
+    const bool two_phase = (s->layout == 0 || s->layout == 2) && a.t_split < s->R;
+    if (s->group_w > 0) {                    // lane-group layout (latency-bound launches)
+      const int tpg = 128 / s->group_w;
+      const dim3 ggrid((unsigned)((s->max_shard + tpg - 1) / tpg), (unsigned)nc);
+      const size_t gsmem = (size_t)s->tab_bytes + (size_t)tpg * (((s->B + 1) & ~1) * 16);
+      launch_group(s->group_w, windowed, s->log_mode, ggrid, gsmem, st, a);
+      ZS_CUDA(s, cudaGetLastError());
+      s->launches += 1;
+    } else if (!two_phase) {
       replay_fn(windowed, s->log_mode, 0, s->any_ablation)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
       ZS_CUDA(s, cudaGetLastError());
       s->launches += 1;

@@ -250,16 +250,18 @@ def test_errors_are_reported(zs):
         sim2.load_profile()
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg4_38"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg4_38", "cfg5"])
 def test_schedules_bit_identical(zs, oracle, name):
-    """layout 1 (one pass) and layout 2 (pruning phase, regroup, Thompson phase) give the
-    same bits for every trial and decision."""
-    (job,) = synth.config(name, trials=2000)
+    """layout 1 (one pass, thread per trial), layout 2 (pruning phase, regroup, Thompson
+    phase) and layout 3 (lane group per trial) give the same bits for every trial and
+    decision."""
+    (job,) = synth.config(name, trials=2000 if name != "cfg5" else 700)
     outs = [run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True, layout=l)
-            for l in (1, 2)]
-    for k in ("log", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm", "counters"):
-        assert np.array_equal(outs[0][k], outs[1][k]), k
-    np.testing.assert_allclose(outs[0]["curves"], outs[1]["curves"], rtol=1e-12)
+            for l in (1, 2, 3)]
+    for o in outs[1:]:
+        for k in ("log", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm", "counters"):
+            assert np.array_equal(outs[0][k], o[k]), k
+        np.testing.assert_allclose(outs[0]["curves"], o["curves"], rtol=1e-12)
     compare_cell(oracle, outs[1], job.workload, job.cells[0], 0, np.arange(job.trials),
                  job.recurrences, job.trials, logs=True)
 

@@ -8,6 +8,9 @@ from paper_2208_06102_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "u1": ([], []),
+    "noquad": (["ZS_QUAD_LOOP=0"], []),
+    "noslim": (["ZS_SLIM_B=0"], []),
+    "noboth": (["ZS_QUAD_LOOP=0", "ZS_SLIM_B=0"], []),
     "slim": (["ZS_SLIM_B=1"], []),
     "slim_b6": (["ZS_SLIM_B=1", "ZS_P2_MIN_BLOCKS=6"], []),
     "b6": (["ZS_P2_MIN_BLOCKS=6"], []),

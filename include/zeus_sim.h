@@ -110,9 +110,9 @@ typedef struct {
   int32_t log_mode;                  /* 0: no log; 1: per-decision log (4 B / decision) */
   int32_t layout;                    /* schedule of the replay kernel; results
                                         are bit-identical for every value:
-                                        0 auto: 3 when the launch has fewer Zeus trials than
-                                          one wave of thread-per-trial warps, else 2 when
-                                          R > 2|𝓑|, else 1;
+                                        0 auto: 3 when the grouped launch fills at most a
+                                          quarter wave, else 2 when R > 2|𝓑| and no cell has a
+                                          window, else 1 (chosen by measurement);
                                         1 one pass, one thread per trial;
                                         2 two phases: the pruning stage, then the Thompson
                                           stage with trials regrouped by survivor count;

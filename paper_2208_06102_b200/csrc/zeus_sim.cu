@@ -457,7 +457,7 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   int best_warps = -1;
   // sized for the kernel that dominates: the Thompson phase when the schedule has two
   // phases (R > 2B), else the one-pass kernel; ties keep the larger block (fewer stagings)
-  const bool two_phase = s->layout != 1 && std::min(s->R, 2 * B) < s->R;
+  const bool two_phase = (s->layout == 2 || (s->layout == 0 && s->wmax == 0)) && std::min(s->R, 2 * B) < s->R;
   for (int tpb : {128, 64, 32}) {
     const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
     if (bytes > 227 * 1024) continue;
@@ -622,7 +622,9 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     a.opt = s->d_opt.as<double>();
     a.P = s->P;
     a.MP = s->MP;
-    const bool two_phase = (s->layout == 0 || s->layout == 2) && a.t_split < s->R;
+    // auto: two phases except for windowed launches, where the one-pass kernel measured
+    // faster (CFG4 1.45e10 vs 1.30e10 decisions/s); explicit layouts are honoured
+    const bool two_phase = (s->layout == 2 || (s->layout == 0 && !windowed)) && a.t_split < s->R;
     if (s->group_w > 0) {                    // lane-group layout (latency-bound launches)
       const int tpg = 128 / s->group_w;
       const dim3 ggrid((unsigned)((s->max_shard + tpg - 1) / tpg), (unsigned)nc);

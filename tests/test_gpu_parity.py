@@ -189,14 +189,18 @@ def _random_trace(rng, B, P, S, K, fail=0.2):
     (16, 16, 1, 4, 10, 3.0, 1, 100),      # one trial
     (5, 3, 1, 1, 0, 1.0000001, 96, 20),   # beta just above 1: stops everywhere
     (9, 7, 1, 4, 0, 2.0, 300, 0),         # R = 0 -> auto 2|B||P|
+    (32, 8, 1, 4, 0, 2.0, 200, 100),      # two phases with 32 arms (16 pairs, 8 quads)
+    (17, 5, 2, 3, 0, 2.0, 150, 60),       # odd arm count, two phases, two slices
+    (3, 4, 1, 2, 0, math.inf, 130, 30),   # two phases, two pairs, no early stop
 ])
-def test_random_traces_edge_cases(zs, oracle, B, P, S, K, window, beta, trials, R):
+@pytest.mark.parametrize("layout", [0, 3])
+def test_random_traces_edge_cases(zs, oracle, B, P, S, K, window, beta, trials, R, layout):
     rng = np.random.default_rng(B * 1000 + P)
     w = _random_trace(rng, B, P, S, K)
     cells = [synth.cell(eta=e, beta=beta, window=window, seed=int(rng.integers(2**63)),
                         prior_mean=pm, prior_var=pv)
              for e, pm, pv in ((0.0, 0.0, math.inf), (1.0, 500.0, 1e6), (0.37, 0.0, math.inf))]
-    g = run_gpu(zs, w, cells, trials, R, log=True)
+    g = run_gpu(zs, w, cells, trials, R, log=True, layout=layout)
     Rr = g["R"]
     assert Rr == (R if R > 0 else 2 * B * P)
     compare_step1(oracle, g, w, cells)

@@ -130,11 +130,9 @@ __device__ __forceinline__ double zlog(double x, const double2 *__restrict__ tab
 // Exact integer reduction to n/2 + f, |f| <= 1/4; Taylor series of sin(pi f),
 // cos(pi f) (coefficients rounded to nearest double) by fma Horner; pi*f as a
 // double-double in the sine's leading term (NC-3).
-__device__ __forceinline__ void zsincospi(uint64_t m, double &s, double &c) {
+// sin(pi f), cos(pi f) for |f| <= 1/4, then the quadrant rotation by n (mod 4).
+__device__ __forceinline__ void sincospi_reduced(double f, int n, double &s, double &c) {
   using namespace cst;
-  const int64_t n = (int64_t)((m + (1ull << 49)) >> 50);
-  const int64_t j = (int64_t)m - (n << 50);
-  const double f = (double)j * kTwoM51;                      // exact
   const double f2 = f * f;
   double ps = fma(f2, kS8, kS7);
   ps = fma(f2, ps, kS6);
@@ -155,11 +153,28 @@ __device__ __forceinline__ void zsincospi(uint64_t m, double &s, double &c) {
   pc = fma(f2, pc, kC2);
   pc = fma(f2, pc, kC1);
   const double cf = fma(f2, pc, 1.0);
-  const int q = (int)(n & 3);
-  const double ss = (q & 1) ? cf : sf;
-  const double cc = (q & 1) ? sf : cf;
-  s = (q & 2) ? -ss : ss;                 // q=0: sf  1: cf  2: -sf  3: -cf
-  c = ((q + 1) & 2) ? -cc : cc;           // q=0: cf  1: -sf 2: -cf  3: sf
+  const int q = n & 3;
+  const double ss = (q & 1) ? cf : sf;                     // q=0: sf  1: cf  2: -sf  3: -cf
+  const double cc = (q & 1) ? sf : cf;                     // q=0: cf  1: -sf 2: -cf  3: sf
+  // the signs by flipping bit 63 (exact, and -x of +0 is -0 as the unary minus gives)
+  s = __longlong_as_double(__double_as_longlong(ss) ^ ((long long)(q & 2) << 62));
+  c = __longlong_as_double(__double_as_longlong(cc) ^ ((long long)((q + 1) & 2) << 62));
+}
+
+// sin(pi m / 2^51), cos(pi m / 2^51) for 0 <= m < 2^52: n = round(m / 2^50),
+// f = (m - n 2^50) 2^-51 exactly, |f| <= 1/4.
+__device__ __forceinline__ void zsincospi(uint64_t m, double &s, double &c) {
+  const int64_t n = (int64_t)((m + (1ull << 49)) >> 50);
+  const int64_t j = (int64_t)m - (n << 50);
+  sincospi_reduced((double)j * cst::kTwoM51, (int)n, s, c);
+}
+
+// The same for m = b 2^20 (v = b 2^-32, the sampler's angle), in 32-bit integers:
+// n = round(b / 2^30), f = (b - n 2^30) 2^-31 -- the identical f and n, hence the same bits.
+__device__ __forceinline__ void zsincospi_b32(uint32_t b, double &s, double &c) {
+  const uint32_t n = (uint32_t)(((uint64_t)b + (1u << 29)) >> 30);
+  const int jb = (int)(b - (n << 30));
+  sincospi_reduced((double)jb * 0x1p-31, (int)n, s, c);
 }
 
 // The Philox block of arm quad q = k >> 1 of `trial` at recurrence t (NC-3): it feeds two
@@ -176,7 +191,7 @@ __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, double &z0, d
   const double u1 = (double)((unsigned long long)a + 1ull) * 0x1p-32;   // exact
   const double r = sqrt(-2.0 * zlog(u1, logtab));
   double s, c;
-  zsincospi((uint64_t)b << 20, s, c);                                  // m = v 2^52
+  zsincospi_b32(b, s, c);                                              // 2 pi v, v = b 2^-32
   z0 = r * c;
   z1 = r * s;
 }

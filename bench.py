@@ -158,7 +158,7 @@ def reference_main(args, rank, world):
     jobs = synth.config(args.config, trials=args.trials)
     job = jobs[0]
     threads = os.cpu_count() or 1
-    per_step_s = max(1.0, min(15.0, 90.0 / max(1, args.steps + args.warmup)))
+    per_step_s = min(args.cpu_seconds, max(1.0, min(15.0, 90.0 / max(1, args.steps + args.warmup))))
     n, _ = cpu_sample(job, per_step_s, threads)
     from oracle import oracle as O
 

@@ -118,22 +118,25 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ work model
 def work_per_launch(counters, _unused=None):
-    """Algorithmic lane-instructions of one launch: the replay's event counts x per-primitive
+    """Algorithmic lane-instructions of one launch: the work the replay evaluated x per-primitive
     sm_100a SASS costs of the contract (tools/work_model.json):
-      per normal pair      one Box-Muller transform (bm)
-      per Philox block     one Philox4x32-10 (a block feeds two pairs, NC-3)
-      per normal used      theta = fma + strict-< argmin step
-      per decision         the serial contract work (lookup, charge, early stop, Observe and
-                           posterior, totals, digest, curve contributions) + a quarter replica
-                           Philox block + this decision's share of the warp curve reduction"""
+      per Box-Muller transform evaluated      bm
+      per Philox block evaluated              philox (a block feeds two pairs, NC-3)
+      per survivor pair bound-screened        screen
+      per normal used in a transformed pair   theta = fma + argmin step
+      per decision                            the serial contract work (lookup, charge, early
+                                              stop, Observe and posterior, totals, digest, curve
+                                              contributions) + a quarter replica Philox block +
+                                              this decision's share of the warp curve reduction
+    Transforms the bound screen proved unnecessary are not counted (counters [9..11])."""
     wm = json.load(open(os.path.join(ROOT, "tools", "work_model.json")))
-    dec, _, pairs, normals, _, _, _, _, blocks = [int(x) for x in counters]
+    c = [int(x) for x in counters]
+    dec, pairs, normals = c[0], c[2], c[3]
+    bm_done, blocks_done, screened = c[9], c[10], c[11]
+    used = normals * bm_done / max(1, pairs)
     per_dec = {k: wm["serial"][k] + wm["philox"][k] / 4.0 + wm["curves"][k] for k in ("fp64", "total")}
-    fp64 = (pairs * wm["bm"]["fp64"] + blocks * wm["philox"]["fp64"] + normals * wm["theta"]["fp64"]
-            + dec * per_dec["fp64"])
-    total = (pairs * wm["bm"]["total"] + blocks * wm["philox"]["total"] + normals * wm["theta"]["total"]
-             + dec * per_dec["total"])
-    return {"fp64": fp64, "total": total}
+    return {k: bm_done * wm["bm"][k] + blocks_done * wm["philox"][k] + screened * wm["screen"][k]
+            + used * wm["theta"][k] + dec * per_dec[k] for k in ("fp64", "total")}
 
 
 # ------------------------------------------------------------------ reference arm (oracle)

@@ -44,7 +44,7 @@ extern "C" {
 #define ZEUS_MAX_BATCH_SIZES 32
 #define ZEUS_MAX_POWER_LIMITS 64
 #define ZEUS_CURVE_QUANTITIES 7   /* cost, energy, time, pseudo-regret, n_stop, n_opt, n_ts */
-#define ZEUS_COUNTERS 9
+#define ZEUS_COUNTERS 12   /* 0..8 contract events (oracle-checked), 9..11 work evaluated */
 
 typedef enum {
   ZEUS_OK = 0,
@@ -150,9 +150,13 @@ typedef struct {
      arm | p_index << 8 | flags << 16, flags bit0 stopped, bit1 converged,
      bit2 paid the profiling epoch, bit3 decided by Thompson sampling */
   uint32_t *log;
-  /* instrumentation [9]: decisions, sampled TS decisions, normal pairs drawn,
+  /* instrumentation [12]: decisions, sampled TS decisions, normal pairs drawn,
      normals used, early stops, pruning decisions, forced explorations,
-     posterior recomputations, Philox blocks drawn for normals (NC-3: two pairs each) */
+     posterior recomputations, Philox blocks drawn for normals (NC-3: two pairs each)
+     -- [0..8] are events of the method, identical to the oracle's --
+     then the work this build evaluated for them: [9] Box-Muller transforms, [10] Philox
+     blocks, [11] pairs bound-screened (the bound screen skips the transform of pairs whose
+     arms provably cannot win: [9] <= [2]) */
   int64_t *counters;
   /* timing of the last zeus_sim_run, CUDA events on the caller's stream:
      step 1 (Eq. 7) kernel, replay kernel, curve-reduction kernel */

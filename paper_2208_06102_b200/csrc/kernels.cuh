@@ -23,11 +23,14 @@
 #ifndef ZS_QUAD_LOOP
 #define ZS_QUAD_LOOP 1
 #endif
+#ifndef ZS_BOUND_SKIP
+#define ZS_BOUND_SKIP 1
+#endif
 
 namespace zs {
 
 constexpr int kQ = 7;             // curve quantities
-constexpr int kCounters = 9;
+constexpr int kCounters = 12;   // 9 contract events + transforms, Philox blocks, pairs screened
 
 struct ArmConst {                 // per (cell, arm), 64 B
   double c1, t1, e1, cP, tP, eP;
@@ -225,7 +228,7 @@ __device__ __forceinline__ int warp_sum(int v) {
 }
 
 // Warp partial of the curves at recurrence t: a reduce-scatter leaves the warp total of
-// fp64 quantity (lane >> 3) in lanes 0, 8, 16, 24 (12 shuffles instead of 40), then one
+// fp64 quantity (lane >> 3) in lanes 0, 8, 16, 24 (12 shuffles instead of 40, one REDUX for the packed counts), then one
 // 4-lane atomic for the sums and one 3-lane atomic for the counts (packed 8 bits each:
 // stops | optimal << 8 | Thompson << 16).  All 32 lanes must call it.
 __device__ __forceinline__ void curve_accumulate(double *curves, int t, int lane, double vC,
@@ -239,7 +242,7 @@ __device__ __forceinline__ void curve_accumulate(double *curves, int t, int lane
   kq += __shfl_xor_sync(0xffffffffu, kq, 4);
   kq += __shfl_xor_sync(0xffffffffu, kq, 2);
   kq += __shfl_xor_sync(0xffffffffu, kq, 1);
-  vPacked = warp_sum(vPacked);
+  vPacked = (int)__reduce_add_sync(0xffffffffu, (unsigned)vPacked);   // REDUX
   double *row = curves + (size_t)t * kQ;
   if ((lane & 7) == 0) {
     atomicAdd(row + (lane >> 3), kq);
@@ -277,6 +280,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase) {
 }
 
 enum : int { kStart = 0, kDown = 1, kUp = 2 };
+
+// Bound screen.  An upper bound of |z0|, |z1| for the Box-Muller pair of
+// radius word a: u1 = (a+1) 2^-32 > 2^-(clz(a)+1), so r^2 = -2 log u1 < 2 ln2 (clz(a)+1), and
+// sqrt(x) lies below its tangents at x = 2 ln2 and x = 6 ln2 (sqrt is concave).  The constants
+// carry a 2^-29 margin, far above the rounding of the computed r, cos and sin.
+__device__ __forceinline__ double radius_bound(uint32_t a) {
+  const double cc = (double)(__clz(a) + 1);
+  return fmin(__fma_ru(cc, 0.5887050123542859, 0.5887050123542859),
+              __fma_ru(cc, 0.3398889973560289, 1.0196669920680868));
+}
+// Can an arm of this pair (bits `two`: arms 2k, 2k+1 in the survivor set) still beat the best
+// sample bt?  theta = fma(sigma, z, mu) >= RD(mu - sigma rub) for |z| <= rub, and rounding is
+// monotone, so RD(mu - sigma rub) > bt proves theta > bt: the arm can neither win nor tie.
+__device__ __forceinline__ bool screen_keep(uint32_t two, double rub, double2 m0, double2 m1, double bt) {
+  return ((two & 1u) && !(__fma_rd(-m0.y, rub, m0.x) > bt)) ||
+         ((two & 2u) && !(__fma_rd(-m1.y, rub, m1.x) > bt));
+}
+constexpr int kResSlots = 2;   // residual pairs whose words are parked in shared memory
 
 // Alg. 2 posterior from the shifted window sums (NC-6), n >= 2: returns (mu, sigma).
 __device__ __forceinline__ double2 posterior(double sh, double S1, double S2, int n, double prec0,
@@ -384,6 +405,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   // event counters (u32 per trial; the pair/normal counts follow from n_sampled
   // because the survivor set is fixed during Thompson sampling)
   uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
+  uint32_t n_resid = 0, n_redraw = 0;                       // bound screen: residual pairs, redrawn blocks
   if (PHASE == 2 && active) {                               // resume from phase A
     const Carry c = a.carry[o];
     best = c.best; totC = c.totC; totE = c.totE; totT = c.totT; dig = c.dig;
@@ -452,6 +474,77 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
           };
           // pairs 2q and 2q+1 share one Philox block: it is drawn when the walk enters a new
           // quad (warp-uniform in phase B, where lanes are grouped by count and parity)
+#if ZS_BOUND_SKIP
+          if (PHASE == 2 && !ABL && !WINDOWED) {
+            // bound screen (exact): draw the pair of the leader (the previous
+            // decision's arm) first; then an arm a can only win if mu_a - sigma_a r_ub <= bt,
+            // r_ub >= |z| bounded from the pair's radius word alone.  Pairs that fail the
+            // screen are transformed afterwards ("residuals"); ties keep the lowest arm.
+            uint4 *s_res = reinterpret_cast<uint4 *>(smem + a.tab_bytes + (size_t)((B + 1) & ~1) * 16 * TPB);
+            const int lead = (last_b >= 0 && ((ts_set >> last_b) & 1u)) ? last_b : __ffs(ts_set) - 1;
+            const int kl = lead >> 1, ql = kl >> 1;
+            const U4 xl = pair_block(cp.key0, cp.key1, trial, t, ql);
+            {
+              double z0, z1;
+              box_muller((kl & 1) ? xl.z : xl.x, (kl & 1) ? xl.w : xl.y, z0, z1, logtab);
+              consider(kl, z0, z1);
+            }
+            uint32_t res = 0u;                               // residual pairs past the slots
+            int nres = 0;
+            auto screen = [&](int k, uint32_t aw, uint32_t bw, double2 m0, double2 m1) {
+              if (screen_keep((ts_set >> (2 * k)) & 3u, radius_bound(aw), m0, m1, bt)) {
+                if (nres < kResSlots) s_res[nres * TPB + tid] = make_uint4(aw, bw, (uint32_t)k, 0u);
+                else res |= 1u << k;              // past the slots: its Philox block is redrawn
+                ++nres;
+              }
+            };
+            const int ks = kl ^ 1;                           // the leader quad's other pair
+            if ((ts_pairs >> ks) & 1u)
+              screen(ks, (ks & 1) ? xl.z : xl.x, (ks & 1) ? xl.w : xl.y, s_ms[(2 * ks) * TPB + tid],
+                     s_ms[(2 * ks + 1) * TPB + tid]);
+            uint32_t qm = quads_of(ts_pairs) & ~(1u << ql);
+            while (qm) {
+              const int qd = __ffs(qm) - 1;
+              qm &= qm - 1u;
+              const U4 xq = pair_block(cp.key0, cp.key1, trial, t, qd);
+              const uint32_t need = (ts_pairs >> (2 * qd)) & 3u;
+              if (need & 1u)
+                screen(2 * qd, xq.x, xq.y, s_ms[(4 * qd) * TPB + tid], s_ms[(4 * qd + 1) * TPB + tid]);
+              if (need & 2u)
+                screen(2 * qd + 1, xq.z, xq.w, s_ms[(4 * qd + 2) * TPB + tid], s_ms[(4 * qd + 3) * TPB + tid]);
+            }
+            auto consider_tie = [&](int k, double z0, double z1) {
+              const uint32_t two = (ts_set >> (2 * k)) & 3u;
+              const double2 m0 = s_ms[(2 * k) * TPB + tid];
+              const double2 m1 = s_ms[(2 * k + 1) * TPB + tid];
+              const double th0 = fma(m0.y, z0, m0.x);
+              const bool take0 = (two & 1u) && (th0 < bt || (th0 == bt && 2 * k < b));
+              bt = take0 ? th0 : bt;
+              b = take0 ? 2 * k : b;
+              const double th1 = fma(m1.y, z1, m1.x);
+              const bool take1 = (two & 2u) && (th1 < bt || (th1 == bt && 2 * k + 1 < b));
+              bt = take1 ? th1 : bt;
+              b = take1 ? 2 * k + 1 : b;
+            };
+            n_resid += nres;
+            n_redraw += nres > kResSlots ? nres - kResSlots : 0;
+            for (int i = 0; i < nres && i < kResSlots; ++i) {
+              const uint4 e = s_res[i * TPB + tid];
+              double z0, z1;
+              box_muller(e.x, e.y, z0, z1, logtab);
+              consider_tie((int)e.z, z0, z1);
+            }
+            while (res) {
+              const int k = __ffs(res) - 1;
+              res &= res - 1u;
+              const U4 xq = pair_block(cp.key0, cp.key1, trial, t, k >> 1);
+              double z0, z1;
+              box_muller((k & 1) ? xq.z : xq.x, (k & 1) ? xq.w : xq.y, z0, z1, logtab);
+              consider_tie(k, z0, z1);
+            }
+            pm = 0u;
+          } else
+#endif
 #if ZS_QUAD_LOOP
           if (PHASE == 2) {
             // quad loop: the two pairs of one Philox block are transformed side by side (two
@@ -653,11 +746,22 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     a.n_stop[o] = nstop;
     a.final_arm[o] = last_b;
   }
+  // work this launch evaluated: with the bound screen, phase B transforms the leader pair and
+  // the residual pairs only (phase A's draws, carried in n_sampled, transform every pair)
+  const unsigned long long pairs_all = (unsigned long long)n_sampled * __popc(ts_pairs);
+  const unsigned long long blocks_all = (unsigned long long)n_sampled * __popc(quads_of(ts_pairs));
+  unsigned long long bm_done = pairs_all, blocks_done = blocks_all, screened = 0;
+  if (ZS_BOUND_SKIP && PHASE == 2 && !ABL && !WINDOWED && active) {
+    const uint32_t ns_a = a.carry[o].n_sampled;
+    bm_done = (unsigned long long)ns_a * __popc(ts_pairs) + (n_sampled - ns_a) + n_resid;
+    blocks_done = blocks_all + n_redraw;
+    screened = (unsigned long long)(n_sampled - ns_a) * (__popc(ts_pairs) - 1);
+  }
   unsigned long long ctr[kCounters] = {
-      active ? (unsigned long long)R : 0ull, n_sampled,
-      (unsigned long long)n_sampled * __popc(ts_pairs), (unsigned long long)n_sampled * __popc(ts_set),
-      (unsigned long long)nstop, n_prune, n_forced, n_recomp,
-      (unsigned long long)n_sampled * __popc(quads_of(ts_pairs))};
+      active ? (unsigned long long)R : 0ull, n_sampled, pairs_all,
+      (unsigned long long)n_sampled * __popc(ts_set),
+      (unsigned long long)nstop, n_prune, n_forced, n_recomp, blocks_all,
+      active ? bm_done : 0ull, active ? blocks_done : 0ull, screened};
 #pragma unroll
   for (int q = 0; q < kCounters; ++q) {
     unsigned long long v = ctr[q];
@@ -938,7 +1042,10 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
       cnt_lane ? (unsigned long long)n_sampled * __popc(ts_set) : 0ull,
       cnt_lane ? (unsigned long long)nstop : 0ull, cnt_lane ? n_prune : 0u,
       cnt_lane ? n_forced : 0u, cnt_lane ? n_recomp : 0u,
-      cnt_lane ? (unsigned long long)n_sampled * __popc(quads_of(ts_pairs)) : 0ull};
+      cnt_lane ? (unsigned long long)n_sampled * __popc(quads_of(ts_pairs)) : 0ull,
+      cnt_lane ? (unsigned long long)n_sampled * __popc(ts_pairs) : 0ull,   // every pair transformed,
+      cnt_lane ? (unsigned long long)n_sampled * __popc(ts_pairs) : 0ull,   // each with its own block
+      0ull};
 #pragma unroll
   for (int qq = 0; qq < kCounters; ++qq) {
     unsigned long long v = ctr[qq];
@@ -1257,7 +1364,9 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
       active ? (unsigned long long)R : 0ull, n_sampled,
       (unsigned long long)n_sampled * __popc(ts_pairs), (unsigned long long)n_sampled * __popc(ts_set),
       (unsigned long long)nstop, n_prune, n_forced, n_recomp,
-      (unsigned long long)n_sampled * __popc(quads_of(ts_pairs))};
+      (unsigned long long)n_sampled * __popc(quads_of(ts_pairs)),
+      (unsigned long long)n_sampled * __popc(ts_pairs),
+      (unsigned long long)n_sampled * __popc(quads_of(ts_pairs)), 0ull};
 #pragma unroll
   for (int qq = 0; qq < kCounters; ++qq) {
     unsigned long long v = ctr[qq];

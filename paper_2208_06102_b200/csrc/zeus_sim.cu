@@ -453,7 +453,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   const zs::TabLayout L(B, S, K);
   s->tab_bytes = L.bytes;
   const int wmax = s->wmax;
-  const size_t per_thread = (size_t)((B + 1) & ~1) * 16;   // (mu, sigma) per arm
+  // (mu, sigma) per arm, and the bound screen's two residual slots
+  const size_t per_thread = (size_t)((B + 1) & ~1) * 16 + (ZS_BOUND_SKIP ? 16 * zs::kResSlots : 0);
   int best_warps = -1;
   // sized for the kernel that dominates: the Thompson phase when the schedule has two
   // phases (R > 2B), else the one-pass kernel; ties keep the larger block (fewer stagings)

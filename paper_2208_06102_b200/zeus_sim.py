@@ -22,7 +22,7 @@ ZEUS_OK = 0
 STATUS = {0: "ZEUS_OK", 1: "ZEUS_E_INVALID", 2: "ZEUS_E_STATE", 3: "ZEUS_E_NO_CONVERGENT_ARM",
           4: "ZEUS_E_CUDA", 5: "ZEUS_E_NOMEM", 6: "ZEUS_E_UNSUPPORTED"}
 CURVE_Q = 7
-COUNTERS = 9
+COUNTERS = 12
 EXPORTS = ("zeus_sim_create", "zeus_sim_load_profile", "zeus_sim_run", "zeus_sim_results",
            "zeus_sim_destroy", "zeus_sim_last_error", "zeus_sim_shape")
 

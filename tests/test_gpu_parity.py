@@ -68,7 +68,8 @@ def compare_cell(oracle, g, w, cell, ci, trials_idx, R, n_shard, full_curves=Tru
         np.testing.assert_allclose(gc[:, :4], oc[:, :4], rtol=CURVE_RTOL, atol=0)
         assert np.array_equal(gc[:, 4:], oc[:, 4:])
         if len(g["curves"]) == 1:
-            assert np.array_equal(g["counters"], o["counters"])
+            assert np.array_equal(g["counters"][:9], o["counters"])   # events of the method
+            assert g["counters"][9] <= g["counters"][2]                  # work the screen left
     return o
 
 
@@ -263,9 +264,17 @@ def test_schedules_bit_identical(zs, oracle, name):
     outs = [run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True, layout=l)
             for l in (1, 2, 3)]
     for o in outs[1:]:
-        for k in ("log", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm", "counters"):
+        for k in ("log", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm"):
             assert np.array_equal(outs[0][k], o[k]), k
+        assert np.array_equal(outs[0]["counters"][:9], o["counters"][:9])
         np.testing.assert_allclose(outs[0]["curves"], o["curves"], rtol=1e-12)
+    # evaluated work: one pass and lane groups transform every survivor pair; the two-phase
+    # schedule's bound screen transforms at most as many
+    c1, c2, c3 = (o["counters"] for o in outs)
+    assert c1[9] == c1[2] and c3[9] == c3[2] and c1[10] == c1[8]
+    assert c2[9] <= c2[2] and c2[10] >= c2[8]
+    if name == "cfg5":
+        assert c2[9] < 0.6 * c2[2]
     compare_cell(oracle, outs[1], job.workload, job.cells[0], 0, np.arange(job.trials),
                  job.recurrences, job.trials, logs=True)
 

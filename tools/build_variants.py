@@ -8,6 +8,17 @@ from paper_2208_06102_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "u1": ([], []),
+    "skipstats": (["ZS_SKIP_STATS=1"], []),
+    "bskip": (["ZS_BOUND_SKIP=1"], []),
+    "b1": (["ZS_BOUND_SKIP=1", "ZS_BSKIP_SLOTS=1"], []),
+    "b1l": (["ZS_BOUND_SKIP=1", "ZS_BSKIP_SLOTS=1", "ZS_RUB_LINE=1"], []),
+    "b1_6": (["ZS_BOUND_SKIP=1", "ZS_BSKIP_SLOTS=1", "ZS_P2_MIN_BLOCKS=6"], []),
+    "b1l_6": (["ZS_BOUND_SKIP=1", "ZS_BSKIP_SLOTS=1", "ZS_RUB_LINE=1", "ZS_P2_MIN_BLOCKS=6"], []),
+    "bl": (["ZS_BOUND_SKIP=1", "ZS_RUB_LINE=1"], []),
+    "blr": (["ZS_BOUND_SKIP=1", "ZS_RUB_LINE=1", "ZS_REDUX=1"], []),
+    "blp": (["ZS_BOUND_SKIP=1", "ZS_RUB_LINE=1", "ZS_SCREEN_PREFETCH=1"], []),
+    "blpr": (["ZS_BOUND_SKIP=1", "ZS_RUB_LINE=1", "ZS_SCREEN_PREFETCH=1", "ZS_REDUX=1"], []),
+    "ur": (["ZS_REDUX=1"], []),
     "noquad": (["ZS_QUAD_LOOP=0"], []),
     "noslim": (["ZS_SLIM_B=0"], []),
     "noboth": (["ZS_QUAD_LOOP=0", "ZS_SLIM_B=0"], []),

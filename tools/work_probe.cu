@@ -104,3 +104,13 @@ extern "C" __global__ void probe_serial(const double *in, const int *pool, const
 extern "C" __global__ void probe_curves(double *curves, const double *v, const int *pk, int t) {
   curve_accumulate(curves, t, threadIdx.x & 31, v[0], v[1], v[2], v[3], pk[0]);
 }
+// Bound screen of one survivor pair: radius bound from the radius word, the
+// rounded-down lower bounds of both arms against bt, and parking a residual pair's words
+extern "C" __global__ void probe_screen(const uint32_t *w, const double2 *ms, const double *in,
+                                        uint4 *park, int *nres) {
+  const double rub = radius_bound(w[0]);
+  if (screen_keep(w[2], rub, ms[0], ms[1], in[0])) {
+    park[threadIdx.x] = make_uint4(w[0], w[1], w[3], 0u);
+    nres[0] += 1;
+  }
+}

@@ -405,7 +405,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   // event counters (u32 per trial; the pair/normal counts follow from n_sampled
   // because the survivor set is fixed during Thompson sampling)
   uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
-  uint32_t n_resid = 0, n_redraw = 0;                       // bound screen: residual pairs, redrawn blocks
+  uint32_t n_resid = 0, n_redraw = 0, n_scr = 0;            // bound screen: residual pairs, redrawn blocks, draws
   if (PHASE == 2 && active) {                               // resume from phase A
     const Carry c = a.carry[o];
     best = c.best; totC = c.totC; totE = c.totE; totT = c.totT; dig = c.dig;
@@ -475,7 +475,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
           // pairs 2q and 2q+1 share one Philox block: it is drawn when the walk enters a new
           // quad (warp-uniform in phase B, where lanes are grouped by count and parity)
 #if ZS_BOUND_SKIP
-          if (PHASE == 2 && !ABL && !WINDOWED) {
+          if (PHASE != 1) {
             // bound screen (exact): draw the pair of the leader (the previous
             // decision's arm) first; then an arm a can only win if mu_a - sigma_a r_ub <= bt,
             // r_ub >= |z| bounded from the pair's radius word alone.  Pairs that fail the
@@ -527,6 +527,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
               b = take1 ? 2 * k + 1 : b;
             };
             n_resid += nres;
+            n_scr += 1;
             n_redraw += nres > kResSlots ? nres - kResSlots : 0;
             for (int i = 0; i < nres && i < kResSlots; ++i) {
               const uint4 e = s_res[i * TPB + tid];
@@ -750,18 +751,14 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   // the residual pairs only (phase A's draws, carried in n_sampled, transform every pair)
   const unsigned long long pairs_all = (unsigned long long)n_sampled * __popc(ts_pairs);
   const unsigned long long blocks_all = (unsigned long long)n_sampled * __popc(quads_of(ts_pairs));
-  unsigned long long bm_done = pairs_all, blocks_done = blocks_all, screened = 0;
-  if (ZS_BOUND_SKIP && PHASE == 2 && !ABL && !WINDOWED && active) {
-    const uint32_t ns_a = a.carry[o].n_sampled;
-    bm_done = (unsigned long long)ns_a * __popc(ts_pairs) + (n_sampled - ns_a) + n_resid;
-    blocks_done = blocks_all + n_redraw;
-    screened = (unsigned long long)(n_sampled - ns_a) * (__popc(ts_pairs) - 1);
-  }
+  const unsigned long long screened = (unsigned long long)n_scr * (__popc(ts_pairs) - 1);
+  const unsigned long long bm_done = pairs_all - screened + n_resid;
+  const unsigned long long blocks_done = blocks_all + n_redraw;
   unsigned long long ctr[kCounters] = {
       active ? (unsigned long long)R : 0ull, n_sampled, pairs_all,
       (unsigned long long)n_sampled * __popc(ts_set),
       (unsigned long long)nstop, n_prune, n_forced, n_recomp, blocks_all,
-      active ? bm_done : 0ull, active ? blocks_done : 0ull, screened};
+      active ? bm_done : 0ull, active ? blocks_done : 0ull, active ? screened : 0ull};
 #pragma unroll
   for (int q = 0; q < kCounters; ++q) {
     unsigned long long v = ctr[q];

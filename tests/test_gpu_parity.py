@@ -268,13 +268,15 @@ def test_schedules_bit_identical(zs, oracle, name):
             assert np.array_equal(outs[0][k], o[k]), k
         assert np.array_equal(outs[0]["counters"][:9], o["counters"][:9])
         np.testing.assert_allclose(outs[0]["curves"], o["curves"], rtol=1e-12)
-    # evaluated work: one pass and lane groups transform every survivor pair; the two-phase
-    # schedule's bound screen transforms at most as many
+    # evaluated work: lane groups transform every survivor pair (each with its own Philox
+    # block); the bound screen of the one-pass and Thompson-phase kernels
+    # transforms at most as many, and far fewer once the posteriors separate
     c1, c2, c3 = (o["counters"] for o in outs)
-    assert c1[9] == c1[2] and c3[9] == c3[2] and c1[10] == c1[8]
-    assert c2[9] <= c2[2] and c2[10] >= c2[8]
-    if name == "cfg5":
-        assert c2[9] < 0.6 * c2[2]
+    assert c3[9] == c3[2] and c3[10] == c3[2]
+    for c in (c1, c2):
+        assert c[9] <= c[2] and c[10] >= c[8]
+        if name == "cfg5":
+            assert c[9] < 0.6 * c[2]
     compare_cell(oracle, outs[1], job.workload, job.cells[0], 0, np.arange(job.trials),
                  job.recurrences, job.trials, logs=True)
 

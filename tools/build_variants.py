@@ -8,6 +8,10 @@ from paper_2208_06102_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "u1": ([], []),
+    "sall": (["ZS_SCREEN_ALL=1"], []),
+    "lred": (["ZS_LANE_RED=1"], []),
+    "clk": (["ZS_REGION_CLOCKS=1"], []),
+    "minmu": (["ZS_LEAD_MINMU=1"], []),
     "skipstats": (["ZS_SKIP_STATS=1"], []),
     "bskip": (["ZS_BOUND_SKIP=1"], []),
     "b1": (["ZS_BOUND_SKIP=1", "ZS_BSKIP_SLOTS=1"], []),

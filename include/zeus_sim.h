@@ -83,8 +83,9 @@ typedef struct {
   int64_t trials;                    /* global trial count of this cell, >= 0 */
   int32_t policy;                    /* ZEUS_POLICY_*: Zeus, or one of the paper's baselines
                                         replayed on the same traces and replica draws */
-  int32_t ablation;                  /* Zeus only: ZEUS_ABLATE_* bits; "no early
-                                        stopping" is beta = +INFINITY */
+  int32_t ablation;                  /* Zeus only: ZEUS_ABLATE_* bits and
+                                        ZEUS_VARIANT_* bits; "no early stopping" is beta =
+                                        +INFINITY */
   const double *arrivals;            /* NULL: recurrences run back to back (the paper's replay);
                                         else host [R] non-decreasing submission times (s) shared
                                         by the cell's trials: concurrent submissions (§4.4
@@ -95,6 +96,17 @@ typedef struct {
 #define ZEUS_ABLATE_PRUNING 1       /* keep every batch size: Alg. 3 still walks, 𝓑 is not pruned */
 #define ZEUS_ABLATE_JIT 2           /* no JIT profiler: the first |𝓟| runs of each batch size try
                                        the power limits in ascending order, one per recurrence */
+/* variant readings of the early stop (DESIGN.md R-Q4v, R-Q1v, R-Q5v), same field,
+   sequential recurrences only (no arrivals), combinable with each other and the ablations */
+#define ZEUS_VARIANT_RETRY 4        /* "stop the job and retry with another batch size": after an
+                                       early stop the recurrence continues with another decision
+                                       (Thompson sampling leaves out the arms stopped in it); it
+                                       ends with its first run that is not stopped */
+#define ZEUS_VARIANT_EPOCH_STOP 8   /* the cost is checked at epoch boundaries: the run
+                                       stops at the end of the first epoch whose accumulated cost
+                                       exceeds beta*best, and is charged that epoch's cost */
+#define ZEUS_VARIANT_WINDOWED_BEST 16 /* best = min over the converged runs of the last N = window
+                                       recurrences (needs window >= 2): the threshold follows drift */
 
 /* policies (§6.1 "Baselines"; DESIGN.md R-Q29) */
 #define ZEUS_POLICY_ZEUS 0          /* Alg. 3 pruning + Alg. 1/2 Thompson sampling, Eq. 7 p*, early stop */

@@ -225,6 +225,37 @@ uint32_t replica(uint64_t seed, int64_t trial, int32_t t, int32_t K) {
   return (uint32_t)(((uint64_t)x[t & 3] * (uint64_t)(uint32_t)K) >> 32);
 }
 
+// Draws of retry attempt j >= 1 of recurrence t (R-Q4v): the normal pairs use counter
+// (t, 1 << 24 | j << 16 | k >> 1, trial), the replica counter (t, 3 << 24 | j, trial) word 0.
+// Attempt 0 uses the counters above, so a recurrence without a retry draws what the base
+// replay draws.
+void normal_pair_attempt(uint64_t seed, int64_t trial, int32_t t, int32_t j, int32_t k, double *z0,
+                         double *z1) {
+  if (j == 0) { normal_pair(seed, trial, t, k, z0, z1); return; }
+  const uint32_t ctr[4] = {(uint32_t)t, (1u << 24) | ((uint32_t)j << 16) | (uint32_t)(k >> 1),
+                           (uint32_t)(uint64_t)trial, (uint32_t)((uint64_t)trial >> 32)};
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t x[4];
+  philox(ctr, key, x);
+  const uint32_t a = (k & 1) ? x[2] : x[0], b = (k & 1) ? x[3] : x[1];
+  double u1, v;
+  uniforms(a, b, &u1, &v);
+  const double r = std::sqrt(-2.0 * zlog(u1));
+  double s, c;
+  zsincospi((uint64_t)b << 20, &s, &c);                      // 2 pi v = pi (b 2^20) / 2^51
+  *z0 = r * c;
+  *z1 = r * s;
+}
+uint32_t replica_attempt(uint64_t seed, int64_t trial, int32_t t, int32_t j, int32_t K) {
+  if (j == 0) return replica(seed, trial, t, K);
+  const uint32_t ctr[4] = {(uint32_t)t, (3u << 24) | (uint32_t)j, (uint32_t)(uint64_t)trial,
+                           (uint32_t)((uint64_t)trial >> 32)};
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t x[4];
+  philox(ctr, key, x);
+  return (uint32_t)(((uint64_t)x[0] * (uint64_t)K) >> 32);
+}
+
 // ---------------------------------------------------------------- Observe (Alg. 2)
 // One arm's belief.  Var(C_b) and Sum(C_b) of Alg. 2 are kept as
 // sums shifted by the arm's first observation (NC-6); the window of the N most
@@ -382,7 +413,11 @@ std::string validate(const oracle_trace &tr, const oracle_cell &cell) {
   if (!(cell.prior_var > 0.0)) add("prior variance must be > 0");
   if (!std::isfinite(cell.prior_mean)) add("prior mean not finite");
   if (cell.policy < 0 || cell.policy > 2) add("policy must be 0 (Zeus), 1 (Default) or 2 (Grid Search)");
-  if (cell.ablation < 0 || cell.ablation > 3) add("ablation must be a subset of {1 no pruning, 2 no JIT}");
+  if (cell.ablation < 0 || cell.ablation > 31)
+    add("ablation must be a subset of {1 no pruning, 2 no JIT, 4 retry, 8 epoch stop, 16 windowed best}");
+  if ((cell.ablation & 16) && cell.window < 2) add("windowed best needs window >= 2");
+  if ((cell.ablation & 28) && cell.arrivals) add("variant readings need sequential recurrences");
+  if (cell.ablation != 0 && cell.policy != 0) add("ablations apply to the Zeus policy only");
   if (B >= 1 && P >= 1 && B <= 32 && P <= 64) {
     for (int i = 0; i < B * P; ++i)
       if (!(tr.avg_power_w[i] > 0.0) || !std::isfinite(tr.avg_power_w[i])) { add("average power not positive"); break; }
@@ -574,6 +609,8 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
     complete(j);
   };
 
+  // converged cost of each recurrence (+inf: none), for the windowed best (R-Q5v)
+  std::vector<double> conv_cost((size_t)R, std::numeric_limits<double>::infinity());
   for (int32_t t = 0; t < R; ++t) {
     const int s = (int)(((int64_t)t * S) / R);   // slice of recurrence t (R-Q19)
     if (cell.arrivals) {                           // runs finished by this submission (R-Q31)
@@ -585,6 +622,18 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
       }
       while ((int)pending.size() >= kMaxOutstanding) complete_earliest();
     }
+    // Variant readings of P:L559 (R-Q4v / R-Q1v / R-Q5v; sequential recurrences only):
+    // with `retry`, an early-stopped attempt is followed by another decision in the same
+    // recurrence, Thompson sampling leaving out the arms stopped in it ("stop the job and retry
+    // with another batch size"); the recurrence ends with its first attempt that is not
+    // stopped, or when Thompson sampling has no arm left.
+    const bool retry = (cell.ablation & 4) != 0;
+    const bool epoch_stop = (cell.ablation & 8) != 0;
+    const bool win_best = (cell.ablation & 16) != 0;
+    uint32_t stopped_here = 0;     // arms early-stopped in this recurrence
+    for (int32_t j = 0;; ++j) {
+    if (j > 0 && in_ts && (ts_set & ~stopped_here) == 0) break;   // no arm left to retry
+    const uint32_t eligible = ts_set & ~stopped_here;
     // ---- step 2: decide b_t
     int b;
     bool walk_issue = false;
@@ -603,17 +652,17 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
     } else {
       b = -1;
       for (int a = 0; a < B; ++a)           // arms without a variance estimate first (R-Q6)
-        if ((ts_set & (1u << a)) && (int)arm[a].window.size() < 2) { b = a; break; }
+        if ((eligible & (1u << a)) && (int)arm[a].window.size() < 2) { b = a; break; }
       if (b < 0) {
         // Alg. 1: θ̂_b ~ N(μ̂_b, σ̂_b²) for every b, b* = argmin θ̂_b
         double best_theta = std::numeric_limits<double>::infinity();
         int last_block = -1;
         for (int k = 0; 2 * k < B; ++k) {
-          uint32_t pairmask = (ts_set >> (2 * k)) & 3u;
+          uint32_t pairmask = (eligible >> (2 * k)) & 3u;
           if (!pairmask) continue;
           if ((k >> 1) != last_block) { last_block = k >> 1; cnt.c[8] += 1; }
           double z[2];
-          normal_pair(cell.seed, trial, t, k, &z[0], &z[1]);
+          normal_pair_attempt(cell.seed, trial, t, j, k, &z[0], &z[1]);
           cnt.c[2] += 1;
           for (int h = 0; h < 2; ++h) {
             int a = 2 * k + h;
@@ -639,7 +688,7 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
       epoch_cost(tr, cell, b, p, &c1b, &t1b, &e1b);
     }
     // ---- step 3: replay one recorded run of b
-    const uint32_t r = replica(cell.seed, trial, t, K);
+    const uint32_t r = replica_attempt(cell.seed, trial, t, j, K);
     const int32_t E = tr.epochs_to_target[((size_t)s * B + b) * K + r];
     const int32_t E_run = E > 0 ? E : tr.max_epochs;
     double c0, t0, e0;
@@ -654,11 +703,33 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
     const double C_full = c0 + em1 * c1b;
     const double T_full = t0 + em1 * t1b;
     const double En_full = e0 + em1 * e1b;
-    // ---- step 4: early stop at β·min_t C_t
-    const double thr = cell.beta * best;
+    // ---- step 4: early stop at β·min_t C_t; with `win_best` the minimum runs over
+    // the converged runs of the last N recurrences only (R-Q5v)
+    double best_now = best;
+    if (win_best) {
+      best_now = std::numeric_limits<double>::infinity();
+      for (int32_t u = std::max(0, t - cell.window); u < t; ++u)
+        if (conv_cost[u] < best_now) best_now = conv_cost[u];
+    }
+    const double thr = cell.beta * best_now;
     double C, Tm, En;
     bool stopped = false;
-    if (C_full > thr) {
+    if (C_full > thr && epoch_stop) {
+      // R-Q1v: the cost is checked at epoch boundaries: the run stops at the end of
+      // the first epoch k whose accumulated cost c0 + (k-1) c1 exceeds thr -- unless that is
+      // its last epoch E_run, where it ends anyway (reaching the target, or failing)
+      int32_t k = 1;
+      while (!(c0 + (double)(k - 1) * c1b > thr)) ++k;
+      if (k < E_run) {
+        stopped = true;
+        const double em = (double)(k - 1);
+        C = c0 + em * c1b;
+        Tm = t0 + em * t1b;
+        En = e0 + em * e1b;
+      } else {
+        C = C_full; Tm = T_full; En = En_full;
+      }
+    } else if (C_full > thr) {   // R-Q1: continuous truncation, charged exactly thr
       stopped = true;
       C = thr;
       if (thr <= c0) {
@@ -674,6 +745,7 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
       C = C_full; Tm = T_full; En = En_full;
     }
     const bool converged = (E > 0) && !stopped;
+    if (converged) conv_cost[t] = C;
     cnt.c[0] += 1;
     if (stopped) cnt.c[4] += 1;
     // the run's outcome reaches the optimiser when it completes: immediately in the paper's
@@ -684,7 +756,7 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
 
     // ---- accumulate (Eq. 4, Eqs. 8-9)
     const uint32_t flags = (stopped ? 1u : 0u) | (converged ? 2u : 0u) |
-                           (profiled_now ? 4u : 0u) | (ts_dec ? 8u : 0u);
+                           (profiled_now ? 4u : 0u) | (ts_dec ? 8u : 0u) | (j > 0 ? 16u : 0u);
     res.tot_cost += C;
     res.tot_energy += En;
     res.tot_time += Tm;
@@ -703,10 +775,13 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
       row[5] += (b == T.opt_arm[s] && p == T.pstar[b]) ? 1.0 : 0.0;
       row[6] += ts_dec ? 1.0 : 0.0;
     }
-    if (log) log[t] = (uint32_t)b | ((uint32_t)p << 8) | (flags << 16);
-    if (clog) clog[t] = C;
-    if (elog) elog[t] = En;
-    if (tlog) tlog[t] = Tm;
+    if (log) log[t] = (uint32_t)b | ((uint32_t)p << 8) | (flags << 16);   // the last attempt
+    if (clog) clog[t] = (j > 0 ? clog[t] : 0.0) + C;                      // the recurrence's
+    if (elog) elog[t] = (j > 0 ? elog[t] : 0.0) + En;                     // totals
+    if (tlog) tlog[t] = (j > 0 ? tlog[t] : 0.0) + Tm;
+    if (!(retry && stopped)) break;
+    stopped_here |= 1u << b;
+    }
   }
 }
 

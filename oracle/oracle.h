@@ -48,7 +48,11 @@ typedef struct {
   uint64_t seed;       /* Philox key */
   int32_t policy;      /* 0 Zeus (Alg. 3 + Alg. 1/2), 1 Default (b0, max p), 2 Grid Search
                           with pruning (§6.1) */
-  int32_t ablation;    /* Zeus ablations: bit0 no pruning, bit1 no JIT profiling */
+  int32_t ablation;    /* Zeus ablations: bit0 no pruning, bit1 no JIT profiling;
+                          variant readings of P:L559 (sequential recurrences only):
+                          bit2 retry after an early stop within the recurrence (R-Q4v),
+                          bit3 early stop at the epoch boundary (R-Q1v),
+                          bit4 best over the last N = window recurrences (R-Q5v) */
   const double *arrivals; /* NULL: sequential recurrences; else [R] non-decreasing submit times
                              (s): concurrent submissions (§4.4), Zeus only */
 } oracle_cell;

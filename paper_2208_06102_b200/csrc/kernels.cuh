@@ -1108,6 +1108,11 @@ struct ConcArgs {
   double *st_ring;
   int ring_n;
   int B, S, K, R, max_epochs, charge_profiling, b0, nslot, reg_stride, opt_stride;
+  // the variant kernel only: "no JIT" per-(b, p) costs, and the windowed best's ring
+  const double *A, *Th, *ebar, *opt;   // [B][P], [B][P], [S][B], [cells][S]
+  double *best_ring;                   // [trial][best_n]
+  int P, best_n;
+  double MP;
 };
 
 template <bool LOG>
@@ -1364,6 +1369,316 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
       (unsigned long long)n_sampled * __popc(quads_of(ts_pairs)),
       (unsigned long long)n_sampled * __popc(ts_pairs),
       (unsigned long long)n_sampled * __popc(quads_of(ts_pairs)), 0ull};
+#pragma unroll
+  for (int qq = 0; qq < kCounters; ++qq) {
+    unsigned long long v = ctr[qq];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((tid & 31) == 0 && v) atomicAdd(a.counters + qq, v);
+  }
+}
+
+// ------------------------------------------------------------------ variant readings (f2)
+// The readings of P:L559 that SURVEY §8(f) f2 lists besides the ablations (DESIGN.md R-Q4v,
+// R-Q1v, R-Q5v), for cells with ZEUS_VARIANT_* bits, combinable with the ablations:
+//   retry (4):         after an early stop the recurrence continues with another decision
+//                      (Thompson sampling leaves out the arms stopped in it) until a run is
+//                      not stopped, or no arm is left; attempt j >= 1 draws from its own
+//                      counters (pairs: q | j << 16, replica: (t, 3 << 24 | j, trial) word 0);
+//   epoch stop (8):    the run stops at the end of the first epoch whose accumulated cost
+//                      exceeds thr (unless that epoch is its last) and is charged that cost;
+//   windowed best (16): thr = beta * the minimum converged cost of the last N recurrences.
+// One thread per trial, one pass, Observe before the next attempt, full Thompson draw.
+template <bool LOG>
+__global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int cell = blockIdx.y;
+  const CellParam cp = a.cells[cell];
+  const int tid = threadIdx.x, TPB = blockDim.x;
+  const int64_t j0 = (int64_t)blockIdx.x * TPB;
+  if (j0 >= cp.n || cp.policy != 0 || cp.conc != 2) return;
+  double2 *s_ms = reinterpret_cast<double2 *>(smem);       // [arm][thread] (mu, sigma)
+  const int B = a.B, R = a.R, S = a.S, K = a.K, P = a.P;
+  const ArmConst *arm = a.arms + (size_t)cell * B;
+  const double *regret = a.regret + (size_t)cell * a.reg_stride;
+  const int32_t *optarm = a.opt_arm + (size_t)cell * a.opt_stride;
+  const int64_t jj = j0 + tid;
+  const bool active = jj < cp.n;
+  const int64_t trial = cp.begin + jj;
+  const size_t o = (size_t)(cp.out_off + jj);
+  ArmStat *st = a.st + o * B;
+  const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
+  double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const bool no_prune = cp.ablation & 1, no_jit = cp.ablation & 2, retry = cp.ablation & 4;
+  const bool epoch_stop = cp.ablation & 8, win_best = cp.ablation & 16;
+  const int NB = win_best ? cp.window : 0;
+  double *bring = a.best_ring + o * (size_t)a.best_n;
+  if (active)
+    for (int u = 0; u < NB; ++u) bring[u] = kInf;
+
+  uint32_t profiled = 0, seen = 0, mature = 0;
+  double best = kInf;
+  bool in_ts = false;
+  int round = 1, step = kStart, start = a.b0, cursor = a.b0;
+  const uint32_t all_arms = (B == 32) ? 0xffffffffu : ((1u << B) - 1u);
+  uint32_t cand = all_arms, surv = 0, ts_set = 0;
+  double r1_cost = kInf;
+  int r1_arm = -1;
+  double totC = 0.0, totE = 0.0, totT = 0.0;
+  unsigned long long dig = 0xcbf29ce484222325ull;
+  int nstop = 0, last_b = -1;
+  uint32_t n_dec = 0, n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
+  unsigned long long n_pairs = 0, n_normals = 0, n_blocks = 0;
+
+  int s = 0;
+  U4 rw{0u, 0u, 0u, 0u};
+  for (int t = 0; t < R; ++t) {
+    double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
+    uint32_t cStop = 0, cOpt = 0, cTs = 0;
+    if (S > 1)
+      while ((long long)(s + 1) * R <= (long long)t * S) ++s;
+    if (active) {
+      if ((t & 3) == 0) rw = replica_words(cp.key0, cp.key1, trial, t);
+      double best_now = best;
+      if (win_best) {                                        // R-Q5v: the last N recurrences
+        best_now = kInf;
+        for (int u = 0; u < NB; ++u) best_now = fmin(best_now, bring[u]);
+      }
+      const double thr = cp.beta * best_now;
+      double conv_t = kInf;
+      uint32_t stopped_here = 0u;                            // arms stopped in this recurrence
+      for (int j = 0;; ++j) {
+        if (j > 0 && in_ts && (ts_set & ~stopped_here) == 0u) break;   // nothing left to retry
+        const uint32_t elig = ts_set & ~stopped_here;
+        // ---------------- step 2: decide
+        const bool ts_dec = in_ts;
+        int b;
+        if (!in_ts) {
+          b = (step == kStart) ? start
+            : (step == kDown) ? 31 - __clz(cand & below_mask(cursor))
+                              : __ffs(cand & above_mask(cursor)) - 1;
+          n_prune += 1;
+        } else {
+          const uint32_t unripe = elig & ~mature;
+          if (unripe) {
+            b = __ffs(unripe) - 1;
+            n_forced += 1;
+          } else {
+            double bt = kInf;
+            b = -1;
+            int qcur = -1;
+            U4 xq{0u, 0u, 0u, 0u};
+            for (int k = 0; 2 * k < B; ++k) {
+              const uint32_t two = (elig >> (2 * k)) & 3u;
+              if (!two) continue;
+              if ((k >> 1) != qcur) {
+                qcur = k >> 1;
+                xq = pair_block(cp.key0, cp.key1, trial, t, qcur | (j << 16));
+                n_blocks += 1;
+              }
+              double z0, z1;
+              box_muller((k & 1) ? xq.z : xq.x, (k & 1) ? xq.w : xq.y, z0, z1, a.logtab);
+              n_pairs += 1;
+              n_normals += __popc(two);
+              const double2 m0 = s_ms[(2 * k) * TPB + tid];
+              const double2 m1 = s_ms[(2 * k + 1) * TPB + tid];
+              const double th0 = fma(m0.y, z0, m0.x);
+              const bool take0 = (two & 1u) && (th0 < bt);
+              bt = take0 ? th0 : bt;
+              b = take0 ? 2 * k : b;
+              const double th1 = fma(m1.y, z1, m1.x);
+              const bool take1 = (two & 2u) && (th1 < bt);
+              bt = take1 ? th1 : bt;
+              b = take1 ? 2 * k + 1 : b;
+            }
+            n_sampled += 1;
+          }
+        }
+        // the power limit; "no JIT" tries the limits in ascending order first
+        const bool was_seen = (seen >> b) & 1u;
+        const ArmStat q = st[b];
+        const ArmConst ac = arm[b];
+        int p = ac.pstar;
+        double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;
+        if (no_jit) {
+          const int runs = was_seen ? q.cnt : 0;
+          if (runs < P) {
+            p = runs;
+            const double Ab = __ldg(a.A + (size_t)b * P + p), Thb = __ldg(a.Th + (size_t)b * P + p);
+            c1b = ((cp.eta * Ab) + ((1.0 - cp.eta) * a.MP)) / Thb;
+            t1b = 1.0 / Thb;
+            e1b = Ab / Thb;
+          }
+        }
+        // ---------------- step 3: replay one recorded run
+        const uint32_t rword = j == 0 ? pick_word(rw, t)
+            : philox4x32_10(U4{(uint32_t)t, 0x03000000u | (uint32_t)j, (uint32_t)trial,
+                               (uint32_t)((uint64_t)trial >> 32)}, cp.key0, cp.key1).x;
+        const uint32_t r = __umulhi(rword, (uint32_t)K);
+        const int E = __ldg(a.pool + ((size_t)s * B + b) * K + r);
+        const int Erun = E > 0 ? E : a.max_epochs;
+        double c0, t0, e0;
+        const bool prof_now = !no_jit && a.charge_profiling && !((profiled >> b) & 1u);
+        if (prof_now) { c0 = ac.cP; t0 = ac.tP; e0 = ac.eP; } else { c0 = c1b; t0 = t1b; e0 = e1b; }
+        profiled |= 1u << b;
+        const double em1 = (double)(Erun - 1);
+        const double Cf = c0 + em1 * c1b;
+        // ---------------- step 4: early stop
+        double C, Tm, En;
+        bool stopped = false;
+        if (Cf > thr && epoch_stop) {
+          // first epoch k with c0 + (k-1) c1 > thr: a guess from one division, then the exact
+          // test of the definition (the left side is non-decreasing in k)
+          int k = 1;
+          if (!(c0 > thr)) {
+            const double g = floor((thr - c0) / c1b);
+            k = (g >= (double)Erun) ? Erun : (int)g + 2;
+            if (k < 2) k = 2;
+            while (k > 2 && c0 + (double)(k - 2) * c1b > thr) --k;
+            while (!(c0 + (double)(k - 1) * c1b > thr)) ++k;
+          }
+          if (k < Erun) {
+            stopped = true;
+            const double em = (double)(k - 1);
+            C = c0 + em * c1b;
+            Tm = t0 + em * t1b;
+            En = e0 + em * e1b;
+          } else {
+            C = Cf;
+            Tm = t0 + em1 * t1b;
+            En = e0 + em1 * e1b;
+          }
+        } else if (Cf > thr) {
+          stopped = true;
+          C = thr;
+          if (thr <= c0) {
+            const double phi = thr / c0;
+            Tm = phi * t0;
+            En = phi * e0;
+          } else {
+            const double phi = (thr - c0) / c1b;
+            Tm = t0 + phi * t1b;
+            En = e0 + phi * e1b;
+          }
+        } else {
+          C = Cf;
+          Tm = t0 + em1 * t1b;
+          En = e0 + em1 * e1b;
+        }
+        const bool conv = (E > 0) && !stopped;
+        if (conv) {
+          conv_t = C;
+          if (!(C >= best)) best = C;
+        }
+        // ---------------- Alg. 2 Observe (before the next attempt decides)
+        {
+          const int cnt = was_seen ? q.cnt : 0;
+          double sh, S1, S2;
+          if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
+          else { sh = q.sh; S1 = q.S1; S2 = q.S2; }
+          int n = cnt;
+          if (a.ring_n > 0 && cp.window > 0) {
+            const int N = cp.window;
+            double *slot = &a.st_ring[(o * B + b) * (size_t)a.ring_n + (cnt % N)];
+            if (cnt >= N) {
+              const double dy = *slot - sh;
+              S1 = S1 - dy;
+              S2 = S2 - dy * dy;
+              n = N - 1;
+            }
+            *slot = C;
+          }
+          const double d = C - sh;
+          S1 = S1 + d;
+          S2 = S2 + d * d;
+          n += 1;
+          ArmStat nq;
+          nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
+          st[b] = nq;
+          seen |= 1u << b;
+          if (n >= 2) {
+            s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
+            mature |= 1u << b;
+            n_recomp += 1;
+          }
+        }
+        // ---------------- Alg. 3 bookkeeping
+        if (!in_ts) {
+          if (conv) {
+            surv |= 1u << b;
+            if (round == 1 && (C < r1_cost || (C == r1_cost && b < r1_arm))) { r1_cost = C; r1_arm = b; }
+          }
+          bool end_round = false;
+          if (step == kStart) { step = kDown; cursor = start; }
+          else if (step == kDown) { if (conv) cursor = b; else { step = kUp; cursor = start; } }
+          else { if (conv) cursor = b; else end_round = true; }
+          if (!end_round && step == kDown && (cand & below_mask(cursor)) == 0u) { step = kUp; cursor = start; }
+          if (!end_round && step == kUp && (cand & above_mask(cursor)) == 0u) end_round = true;
+          if (end_round) {
+            if (surv == 0u) surv = 1u << start;
+            if (round == 1) {
+              cand = no_prune ? all_arms : surv;
+              if (r1_arm >= 0) start = r1_arm;
+              surv = 0u;
+              round = 2;
+              step = kStart;
+              cursor = start;
+            } else {
+              in_ts = true;
+              ts_set = no_prune ? all_arms : surv;
+            }
+          }
+        }
+        // ---------------- accumulate (every attempt is a decision)
+        const uint32_t flags = (stopped ? 1u : 0u) | (conv ? 2u : 0u) | (prof_now ? 4u : 0u) |
+                               (ts_dec ? 8u : 0u) | (j > 0 ? 16u : 0u);
+        n_dec += 1;
+        totC += C;
+        totE += En;
+        totT += Tm;
+        nstop += stopped ? 1 : 0;
+        last_b = b;
+        dig = (dig ^ (unsigned long long)(uint32_t)b) * 0x100000001b3ull;
+        dig = (dig ^ (unsigned long long)(uint32_t)p) * 0x100000001b3ull;
+        dig = (dig ^ (unsigned long long)flags) * 0x100000001b3ull;
+        if (LOG) a.log[o * R + t] = (uint32_t)b | ((uint32_t)p << 8) | (flags << 16);
+        vC += C;
+        vE += En;
+        vT += Tm;
+        vReg += (p == ac.pstar) ? __ldg(regret + (size_t)s * B + b)
+                                : __ldg(a.ebar + (size_t)s * B + b) * c1b - __ldg(a.opt + (size_t)cell * S + s);
+        cStop += stopped ? 1u : 0u;
+        cOpt += (b == __ldg(optarm + s) && p == ac.pstar) ? 1u : 0u;
+        cTs += ts_dec ? 1u : 0u;
+        if (!(retry && stopped)) break;
+        stopped_here |= 1u << b;
+      }
+      if (win_best) bring[t % NB] = conv_t;
+    }
+    // sums by the warp reduce-scatter; the counts (up to one per attempt) by REDUX each
+    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, 0);
+    const unsigned k4 = __reduce_add_sync(0xffffffffu, cStop), k5 = __reduce_add_sync(0xffffffffu, cOpt),
+                   k6 = __reduce_add_sync(0xffffffffu, cTs);
+    if ((tid & 31) == 0) {
+      double *row = curves + (size_t)t * kQ;
+      if (k4) atomicAdd(row + 4, (double)k4);
+      if (k5) atomicAdd(row + 5, (double)k5);
+      if (k6) atomicAdd(row + 6, (double)k6);
+    }
+  }
+  if (active) {
+    a.tot_cost[o] = totC;
+    a.tot_energy[o] = totE;
+    a.tot_time[o] = totT;
+    a.digest[o] = dig;
+    a.n_stop[o] = nstop;
+    a.final_arm[o] = last_b;
+  }
+  unsigned long long ctr[kCounters] = {
+      active ? (unsigned long long)n_dec : 0ull, n_sampled, n_pairs, n_normals,
+      (unsigned long long)nstop, n_prune, n_forced, n_recomp, n_blocks,
+      n_pairs, n_blocks, 0ull};
 #pragma unroll
   for (int qq = 0; qq < kCounters; ++qq) {
     unsigned long long v = ctr[qq];

@@ -52,7 +52,8 @@ struct zeus_sim {
   // trace
   int S = 0, K = 0, reg_stride = 0, opt_stride = 0;
   bool loaded = false, ran = false, any_zeus = false, any_baseline = false, any_ablation = false,
-       any_conc = false;
+       any_conc = false, any_variant = false;
+  int best_n = 0;                    // ring of the windowed best (ZEUS_VARIANT_WINDOWED_BEST)
   int nslot = 1, tpb = 128, smem_bytes = 0, tab_bytes = 0, launches = 0, nwin = 1, group_w = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
@@ -61,7 +62,7 @@ struct zeus_sim {
   DevBuf d_A, d_Th, d_pool, d_cells, d_arms, d_regret, d_opt, d_optarm;
   DevBuf d_slots, d_curves, d_tot_cost, d_tot_energy, d_tot_time, d_digest, d_nstop, d_final,
       d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket, d_ebar, d_logtab, d_pareto,
-      d_arrivals;
+      d_arrivals, d_best_ring;
   ~zeus_sim() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -144,8 +145,15 @@ void check_cells(const zeus_cell *cells, int n, Errors &E) {
     if (c.trials < 0) E.add(ZEUS_E_INVALID, "trials < 0" + at);
     if (c.policy < ZEUS_POLICY_ZEUS || c.policy > ZEUS_POLICY_GRID_SEARCH)
       E.add(ZEUS_E_INVALID, "policy must be ZEUS_POLICY_ZEUS, _DEFAULT or _GRID_SEARCH" + at);
-    if (c.ablation < 0 || c.ablation > (ZEUS_ABLATE_PRUNING | ZEUS_ABLATE_JIT))
-      E.add(ZEUS_E_INVALID, "ablation must be a subset of ZEUS_ABLATE_PRUNING | ZEUS_ABLATE_JIT" + at);
+    const int32_t kVariants = ZEUS_VARIANT_RETRY | ZEUS_VARIANT_EPOCH_STOP | ZEUS_VARIANT_WINDOWED_BEST;
+    if (c.ablation < 0 || c.ablation > (ZEUS_ABLATE_PRUNING | ZEUS_ABLATE_JIT | kVariants))
+      E.add(ZEUS_E_INVALID, "ablation must be a subset of the ZEUS_ABLATE_* and ZEUS_VARIANT_* bits" + at);
+    if (c.ablation != 0 && c.policy != ZEUS_POLICY_ZEUS)
+      E.add(ZEUS_E_INVALID, "ablation bits apply to the Zeus policy only" + at);
+    if ((c.ablation & ZEUS_VARIANT_WINDOWED_BEST) && c.window < 2)
+      E.add(ZEUS_E_INVALID, "ZEUS_VARIANT_WINDOWED_BEST needs window >= 2" + at);
+    if (c.arrivals && (c.ablation & kVariants))
+      E.add(ZEUS_E_INVALID, "the ZEUS_VARIANT_* readings need sequential recurrences (no arrivals)" + at);
     if (c.arrivals && (c.policy != ZEUS_POLICY_ZEUS || c.ablation != 0))
       E.add(ZEUS_E_UNSUPPORTED, "arrivals are supported for the Zeus policy without ablations" + at);
   }
@@ -308,9 +316,13 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     p.window = c.window;
     p.policy = c.policy;
     p.ablation = c.ablation;
-    p.conc = c.arrivals != nullptr;
-    s->any_conc |= p.conc != 0;
-    s->any_ablation |= c.ablation != 0 && c.policy == ZEUS_POLICY_ZEUS;
+    // conc: 1 = arrival schedule (concurrent kernel), 2 = variant readings (variant kernel)
+    p.conc = c.arrivals != nullptr ? 1 : (c.ablation & (ZEUS_VARIANT_RETRY | ZEUS_VARIANT_EPOCH_STOP |
+                                                         ZEUS_VARIANT_WINDOWED_BEST)) ? 2 : 0;
+    s->any_conc |= p.conc == 1;
+    s->any_variant |= p.conc == 2;
+    if (p.conc == 2 && (c.ablation & ZEUS_VARIANT_WINDOWED_BEST)) s->best_n = std::max(s->best_n, (int)c.window);
+    s->any_ablation |= c.ablation != 0 && c.policy == ZEUS_POLICY_ZEUS && p.conc == 0;
     s->any_zeus |= c.policy == ZEUS_POLICY_ZEUS;
     s->any_baseline |= c.policy != ZEUS_POLICY_ZEUS;
     p.key0 = (uint32_t)c.seed;
@@ -346,6 +358,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
       (e = s->d_st.alloc(n * s->B * sizeof(zs::ArmStat))) != cudaSuccess ||
       (e = s->d_st_ring.alloc(n * s->B * (size_t)s->wmax * 8)) != cudaSuccess ||
       (e = s->d_carry.alloc(n * sizeof(zs::Carry))) != cudaSuccess ||
+      (e = s->d_best_ring.alloc(n * (size_t)s->best_n * 8)) != cudaSuccess ||
       (e = s->d_perm.alloc(n * 4)) != cudaSuccess ||
       (e = s->d_bucket.alloc((size_t)num_cells * s->nwin * zs::kBuckets * 4)) != cudaSuccess ||
       (e = s->d_logtab.alloc(zs::kLogTab * sizeof(double2))) != cudaSuccess) {
@@ -506,6 +519,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   ZS_CUDA(s, grant_group<8>(s->device));
   ZS_CUDA(s, grant_max_smem((const void *)zs::concurrent_kernel<false>, s->device));
   ZS_CUDA(s, grant_max_smem((const void *)zs::concurrent_kernel<true>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::variant_kernel<false>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::variant_kernel<true>, s->device));
   s->loaded = true;
   return ZEUS_OK;
 }
@@ -552,7 +567,7 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     ZS_CUDA(s, cudaGetLastError());
     s->launches += 1;
   }
-  if (s->max_shard > 0 && s->R > 0 && s->any_conc) {
+  if (s->max_shard > 0 && s->R > 0 && (s->any_conc || s->any_variant)) {
     zs::ConcArgs c{};
     c.cells = s->d_cells.as<zs::CellParam>();
     c.arms = s->d_arms.as<zs::ArmConst>();
@@ -576,12 +591,28 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     c.B = s->B; c.S = s->S; c.K = s->K; c.R = s->R; c.max_epochs = s->max_epochs;
     c.charge_profiling = s->charge_profiling; c.b0 = s->b0; c.nslot = s->nslot;
     c.reg_stride = s->reg_stride; c.opt_stride = s->opt_stride;
+    c.A = s->d_A.as<double>();
+    c.Th = s->d_Th.as<double>();
+    c.ebar = s->d_ebar.as<double>();
+    c.opt = s->d_opt.as<double>();
+    c.best_ring = s->d_best_ring.as<double>();
+    c.P = s->P;
+    c.best_n = s->best_n;
+    c.MP = s->MP;
     const size_t smem = (size_t)128 * (((s->B + 1) & ~1) * 16);
     const dim3 grid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
-    if (s->log_mode) zs::concurrent_kernel<true><<<grid, 128, smem, st>>>(c);
-    else zs::concurrent_kernel<false><<<grid, 128, smem, st>>>(c);
-    ZS_CUDA(s, cudaGetLastError());
-    s->launches += 1;
+    if (s->any_conc) {
+      if (s->log_mode) zs::concurrent_kernel<true><<<grid, 128, smem, st>>>(c);
+      else zs::concurrent_kernel<false><<<grid, 128, smem, st>>>(c);
+      ZS_CUDA(s, cudaGetLastError());
+      s->launches += 1;
+    }
+    if (s->any_variant) {
+      if (s->log_mode) zs::variant_kernel<true><<<grid, 128, smem, st>>>(c);
+      else zs::variant_kernel<false><<<grid, 128, smem, st>>>(c);
+      ZS_CUDA(s, cudaGetLastError());
+      s->launches += 1;
+    }
   }
   if (s->max_shard > 0 && s->R > 0 && s->any_zeus) {
     zs::ReplayArgs a{};

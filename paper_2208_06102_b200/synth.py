@@ -124,7 +124,8 @@ def make_workload(name: str, seed: int = 0, slices: int = 1, replicas: int = 4,
 POLICIES = {"zeus": 0, "default": 1, "grid_search": 2}   # §6.1 baselines
 
 
-ABLATIONS = {"no_pruning": 1, "no_jit": 2}             # P:L1076-1077 (β = ∞ is "no early stop")
+ABLATIONS = {"no_pruning": 1, "no_jit": 2,            # P:L1076-1077 (β = ∞ is "no early stop")
+             "retry": 4, "epoch_stop": 8, "windowed_best": 16}   # readings of P:L559 (R-Q4v/1v/5v)
 
 
 def cell(eta=0.5, beta=2.0, window=0, seed=1, prior_mean=0.0, prior_var=math.inf,
@@ -194,6 +195,15 @@ def config(name: str, seed: int = 2208, trials: int | None = None) -> list[Job]:
         abl = [cell(seed=seed + 7), cell(seed=seed + 7, beta=math.inf),
                cell(seed=seed + 7, ablation="no_pruning"), cell(seed=seed + 7, ablation="no_jit")]
         return [Job(make_workload(w, seed), abl, 200, trials or 10_000) for w in SIX]
+    if name == "f2v":  # the variant readings of P:L559 (R-Q4v retry, R-Q1v epoch-boundary stop)
+        var = [cell(seed=seed + 9), cell(seed=seed + 9, ablation="retry"),
+               cell(seed=seed + 9, ablation="epoch_stop"), cell(seed=seed + 9, ablation="retry+epoch_stop")]
+        jobs = [Job(make_workload(w, seed), var, 200, trials or 10_000) for w in SIX]
+        # R-Q5v windowed best under drift (§6.4's optimum shift, window N = 10)
+        drift = [cell(window=10, seed=seed + 9), cell(window=10, seed=seed + 9, ablation="windowed_best"),
+                 cell(window=10, seed=seed + 9, ablation="windowed_best+retry+epoch_stop")]
+        jobs.append(Job(make_workload("bert_sa", seed, slices=200, drift=True), drift, 200, trials or 10_000))
+        return jobs
     if name == "f3":   # concurrent submissions (§4.4): sequential, mild, heavy overlap
         jobs = []
         for w in SIX:
@@ -209,4 +219,4 @@ def config(name: str, seed: int = 2208, trials: int | None = None) -> list[Job]:
 
 
 CONFIGS = ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5")
-NEXT = ("f1", "f2", "f3")   # SURVEY §8(f) rows built on the same replay
+NEXT = ("f1", "f2", "f2v", "f3")   # SURVEY §8(f) rows built on the same replay

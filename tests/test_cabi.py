@@ -75,7 +75,7 @@ def _job(zs, **kw):
 
 def test_create_reports_every_violation_without_gpu(zs):
     job, keep = _job(zs, bs=[8, 8, 4], b0=7, pl=[200.0, 100.0], mp=50.0, max_epochs=0)
-    cells = [zs.zeus_cell(1.5, 1.0, 1, 0.0, -1.0, 1, -5, 7, 9, None)]
+    cells = [zs.zeus_cell(1.5, 1.0, 1, 0.0, -1.0, 1, -5, 7, 99, None)]
     opts = zs.zeus_run_opts(C.sizeof(zs.zeus_run_opts), -1, 0, -1, 3, 0)
     with pytest.raises(zs.ZeusError) as e:
         zs.zeus_sim_create(job, cells, opts)
@@ -125,3 +125,19 @@ def test_null_handle_calls(zs):
     assert L.zeus_sim_run(None, None) == 1
     assert L.zeus_sim_load_profile(None, None, None, 1, 1, None) == 1
     L.zeus_sim_destroy(None)
+
+
+def test_variant_validation(zs):
+    """ZEUS_VARIANT_* rules: the windowed best needs a window; variants need sequential
+    recurrences; ablation bits are Zeus-only."""
+    job, keep = _job(zs)
+    arr = np.arange(10, dtype=np.float64)
+    opts = zs.zeus_run_opts(C.sizeof(zs.zeus_run_opts), 10, 0, -1, 0, 0)
+    for cell, frag in (
+            (zs.zeus_cell(0.5, 2.0, 0, 0.0, math.inf, 1, 10, 0, 16, None), "needs window >= 2"),
+            (zs.zeus_cell(0.5, 2.0, 0, 0.0, math.inf, 1, 10, 0, 4, arr.ctypes.data_as(C.POINTER(C.c_double))),
+             "sequential recurrences"),
+            (zs.zeus_cell(0.5, 2.0, 0, 0.0, math.inf, 1, 10, 1, 8, None), "Zeus policy only")):
+        with pytest.raises(zs.ZeusError) as e:
+            zs.zeus_sim_create(job, [cell], opts)
+        assert e.value.status == 1 and frag in str(e.value), str(e.value)

@@ -346,3 +346,18 @@ def test_f3_concurrent_submissions(zs, oracle):
     g = run_gpu(zs, job.workload, [c], job.trials, job.recurrences, log=True)
     compare_cell(oracle, g, job.workload, c, 0, np.arange(job.trials), job.recurrences, job.trials,
                  logs=True)
+
+
+def test_f2v_variant_readings(zs, oracle):
+    """SURVEY §8(f) f2, the variant readings of P:L559 (DESIGN.md R-Q4v retry, R-Q1v epoch-boundary
+    stop, R-Q5v windowed best under drift), each in the same launch as the base cell: every
+    trial and logged decision bit-exact vs the oracle, curves within 1e-9."""
+    jobs = synth.config("f2v", trials=1500)
+    for job in (jobs[0], jobs[3], jobs[6]):
+        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True)
+        decisions = 0
+        for ci, c in enumerate(job.cells):
+            o = compare_cell(oracle, g, job.workload, c, ci, np.arange(job.trials), job.recurrences,
+                             job.trials, logs=True)
+            decisions += o["counters"][0]
+        assert g["counters"][0] == decisions          # retries are decisions

@@ -579,3 +579,134 @@ def test_concurrency_overlap_is_valid_and_deterministic(oracle):
                                rtol=1e-12)
     seq = oracle.replay(w, synth.cell(seed=21), R, range(30))
     assert not np.array_equal(a["digest"], seq["digest"])
+
+
+# ------------------------------------------------------------------ variant readings
+def _variant_cell(ablation, **kw):
+    c = synth.cell(**kw)
+    c["ablation"] = ablation
+    return c
+
+
+@pytest.mark.parametrize("key", ["W1_retry", "W1_epoch"])
+def test_micro_trace_variants(oracle, key):
+    """R-Q4v / R-Q1v on W1, computed by hand: per-recurrence arms, costs,
+    totals, decision and stop counts, and the charged time and energy of epoch-boundary stops."""
+    g, w = _micro(key)
+    exp = g[key]
+    for seed in (1, 2):
+        o = oracle.replay(w, _variant_cell(exp["ablation"], eta=1.0, beta=exp["beta"], seed=seed), 8,
+                          [0], logs=True)
+        log = o["log"][0]
+        assert [int(x & 0xFF) for x in log] == exp["arms"]
+        assert [int(x >> 16) for x in log] == exp["final_flags"]
+        np.testing.assert_allclose(o["cost_log"][0], exp["costs"], rtol=1e-13)
+        assert o["tot_cost"][0] == pytest.approx(exp["total_cost"], rel=1e-13)
+        assert o["counters"][0] == exp["decisions"] and o["counters"][4] == exp["stops"]
+        if "stop_times" in exp:
+            ts = [t for t in range(8) if int(log[t] >> 16) & 1]
+            np.testing.assert_allclose(o["time_log"][0][ts], exp["stop_times"], rtol=1e-13)
+            np.testing.assert_allclose(o["energy_log"][0][ts], exp["stop_energies"], rtol=1e-13)
+
+
+@pytest.mark.parametrize("ablation", [4, 8, 16, 4 | 8 | 16, 1 | 4, 2 | 8])
+def test_variants_act_only_through_the_stop(oracle, ablation):
+    """Every variant reading changes what happens after an early stop, or which threshold
+    stops a run: with beta = inf (no early stop) each is bit-identical to the base
+    replay (same draws: attempt 0 uses the base counters)."""
+    w = synth.make_workload("deepspeech2", 5)
+    kw = dict(beta=math.inf, seed=13, window=10 if ablation & 16 else 0)
+    a = oracle.replay(w, _variant_cell(ablation, **kw), 150, range(40), logs=True)
+    b = oracle.replay(w, _variant_cell(ablation & 3, **kw), 150, range(40), logs=True)
+    for k in ("log", "tot_cost", "digest", "n_stop"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_windowed_best_full_window_is_the_global_best(oracle):
+    """R-Q5v with N >= R recurrences covers every earlier run: identical to the global best."""
+    w = synth.make_workload("bert_sa", 2208, slices=40, drift=True)
+    R = 40
+    a = oracle.replay(w, _variant_cell(16, beta=1.5, seed=5, window=R), R, range(60), logs=True)
+    b = oracle.replay(w, _variant_cell(0, beta=1.5, seed=5, window=R), R, range(60), logs=True)
+    for k in ("log", "tot_cost", "digest", "n_stop"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_windowed_best_threshold(oracle):
+    """R-Q5v from the logs: every run is charged at most beta * min(converged costs of the last
+    N recurrences), a stopped run exactly that (continuous truncation), and the window matters
+    (some charge exceeds beta * the global best)."""
+    w = synth.make_workload("bert_sa", 2208, slices=120, drift=True)
+    R, N, beta = 120, 10, 1.5
+    o = oracle.replay(w, _variant_cell(16, beta=beta, seed=6, window=N), R, range(80), logs=True)
+    above_global = 0
+    for j in range(80):
+        conv = []
+        for t in range(R):
+            f = int(o["log"][j, t]) >> 16
+            C = o["cost_log"][j, t]
+            thr = beta * min([c for u, c in conv if u >= t - N], default=math.inf)
+            gthr = beta * min([c for _, c in conv], default=math.inf)
+            assert C <= thr
+            if f & 1:
+                assert C == thr and not (f & 2)
+            above_global += C > gthr
+            if f & 2:
+                conv.append((t, C))
+    assert above_global > 0
+
+
+def test_epoch_boundary_stop(oracle):
+    """R-Q1v from the logs: a stopped run ends at the first epoch boundary whose accumulated
+    cost exceeds thr = beta * best: C > thr >= C - c1(b) (cost per epoch at p*), and C minus the
+    first epoch is a whole number of epochs; runs are never stopped in their last epoch."""
+    for name in ("deepspeech2", "bert_qa", "resnet18"):
+        w = synth.make_workload(name, 9)
+        beta = 1.3
+        cel = _variant_cell(8, beta=beta, seed=7)
+        st = oracle.step1(w, cel)
+        o = oracle.replay(w, cel, 100, range(40), logs=True)
+        n_stopped = 0
+        for j in range(40):
+            best = math.inf
+            for t in range(100):
+                x = int(o["log"][j, t])
+                b, f, C = x & 0xFF, x >> 16, o["cost_log"][j, t]
+                thr = beta * best
+                if f & 1:
+                    n_stopped += 1
+                    c1 = st["c1"][b]
+                    c0 = st["c_prof"][b] if f & 4 else c1
+                    assert C > thr >= C - c1 or (C == c0 and c0 > thr)
+                    k = (C - c0) / c1
+                    assert abs(k - round(k)) < 1e-9
+                if f & 2:
+                    best = min(best, C)
+        assert n_stopped > 0
+
+
+def test_retry_recurrences(oracle):
+    """R-Q4v: every retry follows a stop (decisions - R <= stops), a recurrence only ends on a
+    stop when Thompson sampling has run out of arms, and without any stop the replay is the
+    base replay's."""
+    w = synth.make_workload("shufflenet_v2", 3)
+    R, n = 150, 40
+    o = oracle.replay(w, _variant_cell(4, beta=1.3, seed=11), R, range(n), logs=True)
+    base = oracle.replay(w, _variant_cell(0, beta=1.3, seed=11), R, range(n), logs=True)
+    assert o["counters"][0] > R * n                     # some recurrences retried
+    assert o["counters"][0] - R * n <= o["counters"][4]
+    for j in range(n):
+        for t in range(R):
+            f = int(o["log"][j, t]) >> 16
+            if f & 1:                                    # ended on a stop: TS with no arm left
+                assert f & 8
+    same = o["n_stop"] == 0
+    assert np.array_equal(o["digest"][same], base["digest"][same])
+
+
+def test_variant_validation(oracle):
+    w = synth.make_workload("bert_qa", 0)
+    assert "windowed best needs window" in oracle.validate(w, _variant_cell(16))[1]
+    assert "sequential" in oracle.validate(w, _variant_cell(4, arrivals=np.arange(10.0)))[1]
+    assert "subset" in oracle.validate(w, _variant_cell(32))[1]
+    assert oracle.validate(w, _variant_cell(4 | 8 | 16, window=5))[0] == 0

@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--trials", type=int, default=None, help="trials per cell per GPU (default: the config's)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--layout", type=int, default=0)
+    ap.add_argument("--graph", type=int, default=1, choices=(0, 1),
+                    help="1: each handle's run is one CUDA-graph launch (zeus_run_opts.graph)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -201,6 +203,7 @@ def workload_config(args, jobs, world):
             "slices": int(w["pool"].shape[0]), "replicas": int(w["pool"].shape[2]),
             "eta": job.cells[0]["eta"], "beta": job.cells[0]["beta"], "window": job.cells[0]["window"],
             "l2": "flushed between timed steps (256 MiB memset); inputs are KB-sized tables staged to smem",
+            "cuda_graph": bool(args.graph),
             "parallelism": f"trials sharded over {world} GPU(s), NCCL all-reduce of curves"}
 
 
@@ -243,7 +246,7 @@ def main():
     for jb in jobs:                                  # one handle and one stream per job
         total, begin, end = shard_range(jb.trials, world, rank, args.scaling)
         sm = Simulation(jb.workload, jb.cells, total, jb.recurrences, shard=(begin, end),
-                        device=local, layout=args.layout).load_profile()
+                        device=local, layout=args.layout, graph=bool(args.graph)).load_profile()
         sims.append(sm)
         streams.append(torch.cuda.Stream(device=dev))
         curves.append(torch.zeros((sm.ncells, sm.R, 7), dtype=torch.float64, device=dev))

@@ -130,6 +130,12 @@ typedef struct {
                                           stage with trials regrouped by survivor count;
                                         3 one pass, a lane group of W = 2/4/8 lanes per trial
                                           (the draw split across lanes, shuffle argmin) */
+  int32_t graph;                     /* 0: zeus_sim_run enqueues its kernels one by one;
+                                        1: the first run captures them into a CUDA graph (on an
+                                          internal stream) and every run launches that graph on
+                                          the caller's stream -- one launch instead of 5-10 for
+                                          launch-bound configurations; same results.
+                                          zeus_sim_load_profile discards the graph. */
 } zeus_run_opts;
 
 /* Outputs.  Every pointer is caller-owned and may be NULL (skipped); each

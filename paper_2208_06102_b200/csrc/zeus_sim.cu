@@ -26,6 +26,7 @@ struct DevBuf {
   size_t bytes = 0;
   ~DevBuf() { if (p) cudaFree(p); }
   cudaError_t alloc(size_t n) {
+    if (p && n == bytes) return cudaSuccess;   // same size: keep the allocation (and its address)
     if (p) { cudaFree(p); p = nullptr; }
     bytes = n;
     if (n == 0) return cudaSuccess;
@@ -54,6 +55,23 @@ struct zeus_sim {
   bool loaded = false, ran = false, any_zeus = false, any_baseline = false, any_ablation = false,
        any_conc = false, any_variant = false;
   int best_n = 0;                    // ring of the windowed best (ZEUS_VARIANT_WINDOWED_BEST)
+  // CUDA graph of one run's launches (zeus_run_opts.graph), captured on cap_stream
+  int use_graph = 0, graph_launches = 0;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  std::vector<uintptr_t> launch_signature() const {
+    return {(uintptr_t)d_A.p, (uintptr_t)d_Th.p, (uintptr_t)d_pool.p, (uintptr_t)d_arms.p,
+            (uintptr_t)d_regret.p, (uintptr_t)d_opt.p, (uintptr_t)d_optarm.p, (uintptr_t)d_ebar.p,
+            (uintptr_t)S, (uintptr_t)K, (uintptr_t)reg_stride, (uintptr_t)opt_stride, (uintptr_t)tpb,
+            (uintptr_t)smem_bytes, (uintptr_t)tab_bytes, (uintptr_t)group_w, (uintptr_t)loaded};
+  }
+  void drop_graph() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (graph) cudaGraphDestroy(graph);
+    graph_exec = nullptr;
+    graph = nullptr;
+  }
   int nslot = 1, tpb = 128, smem_bytes = 0, tab_bytes = 0, launches = 0, nwin = 1, group_w = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
@@ -64,6 +82,8 @@ struct zeus_sim {
       d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket, d_ebar, d_logtab, d_pareto,
       d_arrivals, d_best_ring;
   ~zeus_sim() {
+    drop_graph();
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (ev2) cudaEventDestroy(ev2);
@@ -265,6 +285,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     if (opts->shard_end >= 0 && opts->shard_end < opts->shard_begin) E.add(ZEUS_E_INVALID, "shard_end < shard_begin");
     if (opts->log_mode != 0 && opts->log_mode != 1) E.add(ZEUS_E_INVALID, "log_mode must be 0 or 1");
     if (opts->layout < 0 || opts->layout > 3) E.add(ZEUS_E_INVALID, "layout must be 0, 1, 2 or 3");
+    if (opts->graph != 0 && opts->graph != 1) E.add(ZEUS_E_INVALID, "graph must be 0 or 1");
   }
   if (E.code != ZEUS_OK) return fail(nullptr, E.code, E.s);
 
@@ -291,6 +312,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
   s->R = opts->recurrences > 0 ? opts->recurrences : 2 * s->B * s->P;
   s->log_mode = opts->log_mode;
   s->layout = opts->layout;
+  s->use_graph = opts->graph;
   {                                      // arrival schedules: finite, non-decreasing (R-Q31)
     Errors EA;
     for (int i = 0; i < num_cells; ++i) {
@@ -399,6 +421,7 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
                                   int32_t K, const int32_t *pool) {
   if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
   s->err.clear();
+  const std::vector<uintptr_t> sig0 = s->launch_signature();
   Errors E;
   const int B = s->B, P = s->P;
   if (!A) E.add(ZEUS_E_INVALID, "avg_power_w is NULL");
@@ -521,17 +544,14 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   ZS_CUDA(s, grant_max_smem((const void *)zs::concurrent_kernel<true>, s->device));
   ZS_CUDA(s, grant_max_smem((const void *)zs::variant_kernel<false>, s->device));
   ZS_CUDA(s, grant_max_smem((const void *)zs::variant_kernel<true>, s->device));
+  // a captured run binds buffer addresses and launch shapes: keep it only if none changed
+  if (s->launch_signature() != sig0) s->drop_graph();
   s->loaded = true;
   return ZEUS_OK;
 }
 
-zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
-  if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
-  s->err.clear();
-  if (!s->loaded) return fail(s, ZEUS_E_STATE, "zeus_sim_run before zeus_sim_load_profile");
-  ZS_CUDA(s, cudaSetDevice(s->device));
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  s->stream = st;
+// Enqueues one run's memsets, events and kernels on st (a1-a7 and the f-row kernels).
+static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st) {
   const int nc = (int)s->cells.size();
   ZS_CUDA(s, cudaMemsetAsync(s->d_slots.p, 0, s->d_slots.bytes, st));
   ZS_CUDA(s, cudaMemsetAsync(s->d_counters.p, 0, s->d_counters.bytes, st));
@@ -688,6 +708,35 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
       s->d_slots.as<double>(), s->d_curves.as<double>(), nc, s->nslot, s->R);
   ZS_CUDA(s, cudaGetLastError());
   ZS_CUDA(s, cudaEventRecord(s->ev2, st));
+  return ZEUS_OK;
+}
+
+zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
+  if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
+  s->err.clear();
+  if (!s->loaded) return fail(s, ZEUS_E_STATE, "zeus_sim_run before zeus_sim_load_profile");
+  ZS_CUDA(s, cudaSetDevice(s->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  s->stream = st;
+  if (!s->use_graph) {
+    const zeus_status rc = enqueue_run(s, st);
+    if (rc != ZEUS_OK) return rc;
+  } else {
+    if (!s->graph_exec) {                   // capture once; the legacy stream cannot capture
+      if (!s->cap_stream) ZS_CUDA(s, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+      ZS_CUDA(s, cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
+      const zeus_status rc = enqueue_run(s, s->cap_stream);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(s->cap_stream, &g);
+      if (rc != ZEUS_OK) { if (g) cudaGraphDestroy(g); return rc; }
+      ZS_CUDA(s, ec);
+      s->graph = g;
+      ZS_CUDA(s, cudaGraphInstantiate(&s->graph_exec, s->graph, 0));
+      s->graph_launches = s->launches;
+    }
+    ZS_CUDA(s, cudaGraphLaunch(s->graph_exec, st));
+    s->launches = s->graph_launches;
+  }
   s->ran = true;
   return ZEUS_OK;
 }

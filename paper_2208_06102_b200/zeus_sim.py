@@ -51,7 +51,7 @@ class zeus_cell(C.Structure):
 class zeus_run_opts(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("recurrences", C.c_int32),
                 ("shard_begin", C.c_int64), ("shard_end", C.c_int64), ("log_mode", C.c_int32),
-                ("layout", C.c_int32)]
+                ("layout", C.c_int32), ("graph", C.c_int32)]
 
 
 class zeus_results(C.Structure):
@@ -149,7 +149,7 @@ class Simulation:
     """
 
     def __init__(self, workload, cells, trials, recurrences=0, shard=(0, -1), log=False,
-                 device=0, layout=0):
+                 device=0, layout=0, graph=False):
         self.w = workload
         bs = np.ascontiguousarray(workload["batch_sizes"], dtype=np.int32)
         pl = np.ascontiguousarray(workload["power_limits"], dtype=np.float64)
@@ -171,7 +171,7 @@ class Simulation:
                                 int(c.get("seed", 0)), int(trials), int(c.get("policy", 0)),
                                 int(c.get("ablation", 0)), ptr))
         opts = zeus_run_opts(C.sizeof(zeus_run_opts), int(recurrences), int(shard[0]),
-                             int(shard[1]), 1 if log else 0, int(layout))
+                             int(shard[1]), 1 if log else 0, int(layout), 1 if graph else 0)
         self.h = zeus_sim_create(job, cs, opts, device)
         R, n, nc, B, S = (C.c_int32(), C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32())
         lib().zeus_sim_shape(self.h, C.byref(R), C.byref(n), C.byref(nc), C.byref(B), None)

@@ -361,3 +361,25 @@ def test_f2v_variant_readings(zs, oracle):
                              job.trials, logs=True)
             decisions += o["counters"][0]
         assert g["counters"][0] == decisions          # retries are decisions
+
+
+def test_cuda_graph_runs_identical(zs):
+    """zeus_run_opts.graph: the captured run, replayed, gives the bits of the direct launches;
+    reloading the same-shaped trace keeps the graph valid, a new shape recaptures it."""
+    want = ["digest", "tot_cost", "final_arm", "curves", "counters"]
+    for name, trials in (("cfg1", 300), ("cfg4_38", 400), ("cfg5", 600)):
+        (job,) = synth.config(name, trials=trials)
+        direct = zs.Simulation(job.workload, job.cells, job.trials, job.recurrences).load_profile()
+        ref = direct.run().results(want=want)
+        direct.close()
+        g = zs.Simulation(job.workload, job.cells, job.trials, job.recurrences, graph=True).load_profile()
+        for rep in range(3):
+            if rep == 2:
+                g.load_profile()                     # same trace again: same buffers, same graph
+            out = g.run().results(want=want)
+            for k in want:
+                if k == "curves":
+                    np.testing.assert_allclose(out[k], ref[k], rtol=1e-12)
+                else:
+                    assert np.array_equal(out[k], ref[k]), (name, rep, k)
+        g.close()

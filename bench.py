@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--trials", type=int, default=None, help="trials per cell per GPU (default: the config's)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--layout", type=int, default=0)
-    ap.add_argument("--graph", type=int, default=1, choices=(0, 1),
+    ap.add_argument("--graph", type=int, default=0, choices=(0, 1),
                     help="1: each handle's run is one CUDA-graph launch (zeus_run_opts.graph)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")

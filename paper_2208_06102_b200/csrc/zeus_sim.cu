@@ -551,14 +551,18 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
 }
 
 // Enqueues one run's memsets, events and kernels on st (a1-a7 and the f-row kernels).
-static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st) {
+static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
   const int nc = (int)s->cells.size();
+  // the timing events: inside a capture they must be external event nodes to be recorded
+  auto record = [&](cudaEvent_t ev) {
+    return capturing ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal) : cudaEventRecord(ev, st);
+  };
   ZS_CUDA(s, cudaMemsetAsync(s->d_slots.p, 0, s->d_slots.bytes, st));
   ZS_CUDA(s, cudaMemsetAsync(s->d_counters.p, 0, s->d_counters.bytes, st));
-  ZS_CUDA(s, cudaEventRecord(s->ev0, st));
+  ZS_CUDA(s, record(s->ev0));
   launch_step1(s, st);                        // a1: Eq. 7 argmin + per-arm constants
   ZS_CUDA(s, cudaGetLastError());
-  ZS_CUDA(s, cudaEventRecord(s->ev3, st));
+  ZS_CUDA(s, record(s->ev3));
   s->launches = 2;                            // step 1 + curve reduction
   if (s->max_shard > 0 && s->R > 0 && s->any_baseline) {
     zs::BaselineArgs b{};
@@ -703,11 +707,11 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st) {
       ZS_CUDA(s, cudaGetLastError());
     }
   }
-  ZS_CUDA(s, cudaEventRecord(s->ev1, st));
+  ZS_CUDA(s, record(s->ev1));
   zs::curve_reduce_kernel<<<std::max(1, std::min(1184, (int)((nc * (size_t)s->R * zs::kQ + 255) / 256))), 256, 0, st>>>(
       s->d_slots.as<double>(), s->d_curves.as<double>(), nc, s->nslot, s->R);
   ZS_CUDA(s, cudaGetLastError());
-  ZS_CUDA(s, cudaEventRecord(s->ev2, st));
+  ZS_CUDA(s, record(s->ev2));
   return ZEUS_OK;
 }
 
@@ -719,13 +723,13 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   s->stream = st;
   if (!s->use_graph) {
-    const zeus_status rc = enqueue_run(s, st);
+    const zeus_status rc = enqueue_run(s, st, false);
     if (rc != ZEUS_OK) return rc;
   } else {
     if (!s->graph_exec) {                   // capture once; the legacy stream cannot capture
       if (!s->cap_stream) ZS_CUDA(s, cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
       ZS_CUDA(s, cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal));
-      const zeus_status rc = enqueue_run(s, s->cap_stream);
+      const zeus_status rc = enqueue_run(s, s->cap_stream, true);
       cudaGraph_t g = nullptr;
       const cudaError_t ec = cudaStreamEndCapture(s->cap_stream, &g);
       if (rc != ZEUS_OK) { if (g) cudaGraphDestroy(g); return rc; }

@@ -404,14 +404,15 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   int nstop = 0, last_b = -1;
   // event counters (u32 per trial; the pair/normal counts follow from n_sampled
   // because the survivor set is fixed during Thompson sampling)
+  // (phase B counts from zero and adds phase A's carried counts at the end; every draw of
+  // this kernel past phase A is screened, so the screened draws are n_sampled here)
   uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
-  uint32_t n_resid = 0, n_redraw = 0, n_scr = 0;            // bound screen: residual pairs, redrawn blocks, draws
+  uint32_t n_resid = 0;                                     // bound screen: residual pairs
   if (PHASE == 2 && active) {                               // resume from phase A
     const Carry c = a.carry[o];
     best = c.best; totC = c.totC; totE = c.totE; totT = c.totT; dig = c.dig;
     profiled = c.profiled; seen = c.seen; mature = c.mature; ts_set = c.ts_set;
     nstop = c.nstop; last_b = c.last_b;
-    n_sampled = c.n_sampled; n_prune = c.n_prune; n_forced = c.n_forced; n_recomp = c.n_recomp;
     for (int k = 0; 2 * k < B; ++k)
       if ((ts_set >> (2 * k)) & 3u) ts_pairs |= 1u << k;
     for (int b = 0; b < B; ++b) {                           // posterior of every arm with n >= 2,
@@ -527,8 +528,8 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
               b = take1 ? 2 * k + 1 : b;
             };
             n_resid += nres;
-            n_scr += 1;
-            n_redraw += nres > kResSlots ? nres - kResSlots : 0;
+            if (nres > kResSlots)                            // rare: straight to the counter
+              atomicAdd(a.counters + 10, (unsigned long long)(nres - kResSlots));
             for (int i = 0; i < nres && i < kResSlots; ++i) {
               const uint4 e = s_res[i * TPB + tid];
               double z0, z1;
@@ -749,11 +750,15 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   }
   // work this launch evaluated: with the bound screen, phase B transforms the leader pair and
   // the residual pairs only (phase A's draws, carried in n_sampled, transform every pair)
+  const unsigned long long screened = (unsigned long long)n_sampled * (__popc(ts_pairs) - 1);
+  if (PHASE == 2 && active) {
+    const Carry c = a.carry[o];
+    n_sampled += c.n_sampled; n_prune += c.n_prune; n_forced += c.n_forced; n_recomp += c.n_recomp;
+  }
   const unsigned long long pairs_all = (unsigned long long)n_sampled * __popc(ts_pairs);
   const unsigned long long blocks_all = (unsigned long long)n_sampled * __popc(quads_of(ts_pairs));
-  const unsigned long long screened = (unsigned long long)n_scr * (__popc(ts_pairs) - 1);
   const unsigned long long bm_done = pairs_all - screened + n_resid;
-  const unsigned long long blocks_done = blocks_all + n_redraw;
+  const unsigned long long blocks_done = blocks_all;
   unsigned long long ctr[kCounters] = {
       active ? (unsigned long long)R : 0ull, n_sampled, pairs_all,
       (unsigned long long)n_sampled * __popc(ts_set),

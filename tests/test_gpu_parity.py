@@ -383,3 +383,20 @@ def test_cuda_graph_runs_identical(zs):
                 else:
                     assert np.array_equal(out[k], ref[k]), (name, rep, k)
         g.close()
+
+
+def test_bound_screen_every_path(zs, oracle):
+    """a trace whose posteriors stay wide (32 arms, few recurrences, large beta)
+    drives the bound screen through all of its paths -- screened-out pairs, parked residuals
+    and redrawn ones past the two slots (counter [10] above [8]) -- bit-exact vs the oracle."""
+    rng = np.random.default_rng(77)
+    w = _random_trace(rng, 32, 4, 1, 4, fail=0.05)
+    cells = [synth.cell(eta=0.5, beta=50.0, seed=int(rng.integers(2**63)), prior_mean=0.0,
+                        prior_var=math.inf)]
+    trials, R = 400, 90
+    for layout in (1, 2):
+        g = run_gpu(zs, w, cells, trials, R, log=True, layout=layout)
+        c = g["counters"]
+        assert c[9] < c[2]                       # pairs screened out
+        assert c[10] > c[8]                      # a third residual redrew its block
+        compare_cell(oracle, g, w, cells[0], 0, np.arange(trials), R, trials, logs=True)

@@ -26,6 +26,9 @@
 #ifndef ZS_BOUND_SKIP
 #define ZS_BOUND_SKIP 1
 #endif
+#ifndef ZS_QCACHE
+#define ZS_QCACHE 1
+#endif
 
 namespace zs {
 
@@ -427,6 +430,12 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const int t_end = PHASE == 1 ? a.t_split : R;
   int s = 0;                                                // slice of t = floor(t*S/R) (R-Q19)
   U4 rw{0u, 0u, 0u, 0u};
+#if ZS_QCACHE
+  // the Observe record of the last arm observed, kept in registers: Thompson sampling mostly
+  // repeats its arm, and then the decision needs no load of the record (same values)
+  ArmStat qc{0.0, 0.0, 0.0, 0, 0};
+  int qc_b = -1;
+#endif
   for (int t = t_begin; t < t_end; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0;
@@ -593,7 +602,11 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       // Observe statistics of arm b: issue the load now, consume after the curves.  In the
       // Thompson phase every survivor was run (and observed, and profiled) during pruning.
       was_seen = (ZS_SLIM_B && PHASE == 2 && !ABL && !WINDOWED) ? true : ((seen >> b) & 1u);
+#if ZS_QCACHE
+      if (PHASE == 2 && b == qc_b) q = qc; else q = st[b];
+#else
       q = st[b];
+#endif
       const ArmConst ac = arm[b];
       // the power limit accompanying b and its per-epoch cost/time/energy
       int p = ac.pstar;
@@ -719,6 +732,10 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
         ArmStat nq;
         nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
         st[b] = nq;
+#if ZS_QCACHE
+        qc = nq;
+        qc_b = b;
+#endif
         seen |= 1u << b;
         if (n >= 2) {
           s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);

@@ -8,6 +8,8 @@ from paper_2208_06102_b200 import build as B  # noqa: E402
 
 VARIANTS = {
     "u1": ([], []),
+    "qc": (["ZS_QCACHE=1"], []),
+    "noqc": (["ZS_QCACHE=0"], []),
     "sall": (["ZS_SCREEN_ALL=1"], []),
     "lred": (["ZS_LANE_RED=1"], []),
     "clk": (["ZS_REGION_CLOCKS=1"], []),
@@ -55,6 +57,8 @@ VARIANTS = {
     "u1_r80": (["ZS_MAXNREG=80"], []),
     "u1_r88": (["ZS_MAXNREG=88"], []),
     "u1_r72": (["ZS_MAXNREG=72"], []),
+    "u1_r64": (["ZS_MAXNREG=64"], []),
+    "u1_r56": (["ZS_MAXNREG=56"], []),
     "u2_r80": (["ZS_PAIR_UNROLL=2", "ZS_MAXNREG=80"], []),
 }
 

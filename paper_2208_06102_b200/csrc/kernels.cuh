@@ -288,17 +288,21 @@ enum : int { kStart = 0, kDown = 1, kUp = 2 };
 // radius word a: u1 = (a+1) 2^-32 > 2^-(clz(a)+1), so r^2 = -2 log u1 < 2 ln2 (clz(a)+1), and
 // sqrt(x) lies below its tangents at x = 2 ln2 and x = 6 ln2 (sqrt is concave).  The constants
 // carry a 2^-29 margin, far above the rounding of the computed r, cos and sin.
+ZS_C(kRubSlope0, 0.5887050123542859);     // tangent of sqrt(2 ln2 x) at x = 1: slope = intercept
+ZS_C(kRubSlope1, 0.3398889973560289);     // tangent at x = 3
+ZS_C(kRubIcpt1, 1.0196669920680868);
 __device__ __forceinline__ double radius_bound(uint32_t a) {
   const double cc = (double)(__clz(a) + 1);
-  return fmin(__fma_ru(cc, 0.5887050123542859, 0.5887050123542859),
-              __fma_ru(cc, 0.3398889973560289, 1.0196669920680868));
+  return fmin(__fma_ru(cc, kRubSlope0, kRubSlope0), __fma_ru(cc, kRubSlope1, kRubIcpt1));
 }
 // Can an arm of this pair (bits `two`: arms 2k, 2k+1 in the survivor set) still beat the best
 // sample bt?  theta = fma(sigma, z, mu) >= RD(mu - sigma rub) for |z| <= rub, and rounding is
 // monotone, so RD(mu - sigma rub) > bt proves theta > bt: the arm can neither win nor tie.
+// Branch-free: both bounds are evaluated (a non-survivor's slot may hold anything; its bit masks it).
 __device__ __forceinline__ bool screen_keep(uint32_t two, double rub, double2 m0, double2 m1, double bt) {
-  return ((two & 1u) && !(__fma_rd(-m0.y, rub, m0.x) > bt)) ||
-         ((two & 2u) && !(__fma_rd(-m1.y, rub, m1.x) > bt));
+  const bool out0 = __fma_rd(-m0.y, rub, m0.x) > bt;
+  const bool out1 = __fma_rd(-m1.y, rub, m1.x) > bt;
+  return ((two & 1u) && !out0) | ((two & 2u) && !out1);
 }
 constexpr int kResSlots = 2;   // residual pairs whose words are parked in shared memory
 

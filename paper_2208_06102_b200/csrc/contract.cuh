@@ -72,6 +72,22 @@ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
   return c;
 }
 
+// The 20 round keys of one Philox key, precomputed on the host and passed in the kernel
+// parameters: the rounds then read them as constant-bank operands (LOP3 R, R, c[][], R)
+// instead of recomputing k + r W with a uniform add per round.
+struct RoundKeys { uint32_t k0[10], k1[10]; };
+
+__device__ __forceinline__ U4 philox4x32_10(U4 c, const RoundKeys &rk) {
+  constexpr uint32_t kMul0 = 0xD2511F53u, kMul1 = 0xCD9E8D57u;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(kMul0, c.x), lo0 = kMul0 * c.x;
+    const uint32_t hi1 = __umulhi(kMul1, c.z), lo1 = kMul1 * c.z;
+    c = U4{hi1 ^ c.y ^ rk.k0[r], lo1, hi0 ^ c.w ^ rk.k1[r], lo0};
+  }
+  return c;
+}
+
 // ------------------------------------------------------------ zlog
 // fdlibm __ieee754_log for positive normal x, one formula for every f (the
 // shortcut branches folded in), polynomial halves by explicit fma (NC-3).
@@ -183,6 +199,10 @@ __device__ __forceinline__ U4 pair_block(uint32_t key0, uint32_t key1, int64_t t
   return philox4x32_10(U4{(uint32_t)t, 0x01000000u | (uint32_t)q, (uint32_t)trial,
                           (uint32_t)((uint64_t)trial >> 32)}, key0, key1);
 }
+__device__ __forceinline__ U4 pair_block(const RoundKeys &rk, int64_t trial, int t, int q) {
+  return philox4x32_10(U4{(uint32_t)t, 0x01000000u | (uint32_t)q, (uint32_t)trial,
+                          (uint32_t)((uint64_t)trial >> 32)}, rk);
+}
 
 // Box-Muller from two 32-bit words: u1 = (a + 1) 2^-32 in (0,1], v = b 2^-32 in [0,1);
 // z0 = r cos(2 pi v), z1 = r sin(2 pi v), r = sqrt(-2 log u1) (NC-3).
@@ -219,6 +239,10 @@ __global__ void log_table_kernel(double2 *tab) {
 __device__ __forceinline__ U4 replica_words(uint32_t key0, uint32_t key1, int64_t trial, int t) {
   return philox4x32_10(U4{(uint32_t)t >> 2, 0x02000000u, (uint32_t)trial,
                           (uint32_t)((uint64_t)trial >> 32)}, key0, key1);
+}
+__device__ __forceinline__ U4 replica_words(const RoundKeys &rk, int64_t trial, int t) {
+  return philox4x32_10(U4{(uint32_t)t >> 2, 0x02000000u, (uint32_t)trial,
+                          (uint32_t)((uint64_t)trial >> 32)}, rk);
 }
 __device__ __forceinline__ uint32_t pick_word(const U4 &w, int t) {
   const int q = t & 3;

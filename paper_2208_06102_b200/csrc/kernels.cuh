@@ -170,6 +170,9 @@ struct ReplayArgs {
   const double *A, *Th, *ebar, *opt;
   int P;
   double MP;
+  // RK launches (one cell, grid.y = 1): the cell's Philox round keys, read by the rounds as
+  // constant-bank operands instead of being recomputed as k + r W in every block
+  RoundKeys rk;
 };
 
 constexpr int kBuckets = 34;      // 2 x popcount of the survivor-pair mask + parity of its lowest pair
@@ -349,12 +352,21 @@ __device__ __forceinline__ uint32_t above_mask(int c) { return c >= 31 ? 0u : ~(
 #else
 #define ZS_REPLAY_BOUNDS __launch_bounds__(128)
 #endif
-template <bool WINDOWED, bool LOG, int PHASE, bool ABL>
+template <bool WINDOWED, bool LOG, int PHASE, bool ABL, bool RK>
 __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
   const int cell = blockIdx.y;
   const CellParam cp = a.cells[cell];
+  // Philox blocks of this cell (NC-3); RK launches take the round keys from the parameters
+  auto pair_block_c = [&](int64_t tr, int tt, int q) -> U4 {
+    if constexpr (RK) return pair_block(a.rk, tr, tt, q);
+    else return pair_block(cp.key0, cp.key1, tr, tt, q);
+  };
+  auto replica_words_c = [&](int64_t tr, int tt) -> U4 {
+    if constexpr (RK) return replica_words(a.rk, tr, tt);
+    else return replica_words(cp.key0, cp.key1, tr, tt);
+  };
   const int tid = threadIdx.x, TPB = blockDim.x;
   const int64_t j0 = (int64_t)blockIdx.x * TPB;
   if (j0 >= cp.n || cp.policy != 0 || cp.conc) return;    // past the shard / another kernel's cell
@@ -454,7 +466,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     if (active) {
       // step 3's replica words: one Philox block per four recurrences (NC-3), refreshed when
       // t enters a new block of four; warp-uniform because all lanes share t
-      if ((t & 3) == 0 || t == t_begin) rw = replica_words(cp.key0, cp.key1, trial, t);
+      if ((t & 3) == 0 || t == t_begin) rw = replica_words_c(trial, t);
       // ---------------- step 2: decide b_t
       const bool ts_dec = in_ts;
       if (PHASE != 2 && !in_ts) {
@@ -497,7 +509,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             uint4 *s_res = reinterpret_cast<uint4 *>(smem + a.tab_bytes + (size_t)((B + 1) & ~1) * 16 * TPB);
             const int lead = (last_b >= 0 && ((ts_set >> last_b) & 1u)) ? last_b : __ffs(ts_set) - 1;
             const int kl = lead >> 1, ql = kl >> 1;
-            const U4 xl = pair_block(cp.key0, cp.key1, trial, t, ql);
+            const U4 xl = pair_block_c(trial, t, ql);
             {
               double z0, z1;
               box_muller((kl & 1) ? xl.z : xl.x, (kl & 1) ? xl.w : xl.y, z0, z1, logtab);
@@ -520,7 +532,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             while (qm) {
               const int qd = __ffs(qm) - 1;
               qm &= qm - 1u;
-              const U4 xq = pair_block(cp.key0, cp.key1, trial, t, qd);
+              const U4 xq = pair_block_c(trial, t, qd);
               const uint32_t need = (ts_pairs >> (2 * qd)) & 3u;
               if (need & 1u)
                 screen(2 * qd, xq.x, xq.y, s_ms[(4 * qd) * TPB + tid], s_ms[(4 * qd + 1) * TPB + tid]);
@@ -552,7 +564,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             while (res) {
               const int k = __ffs(res) - 1;
               res &= res - 1u;
-              const U4 xq = pair_block(cp.key0, cp.key1, trial, t, k >> 1);
+              const U4 xq = pair_block_c(trial, t, k >> 1);
               double z0, z1;
               box_muller((k & 1) ? xq.z : xq.x, (k & 1) ? xq.w : xq.y, z0, z1, logtab);
               consider_tie(k, z0, z1);
@@ -569,7 +581,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             while (qm) {
               const int qd = __ffs(qm) - 1;
               qm &= qm - 1u;
-              const U4 xq = pair_block(cp.key0, cp.key1, trial, t, qd);
+              const U4 xq = pair_block_c(trial, t, qd);
               const uint32_t need = (ts_pairs >> (2 * qd)) & 3u;
               if (need == 3u) {
                 double za0, za1, zb0, zb1;
@@ -594,7 +606,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             pm &= pm - 1u;
             if ((k >> 1) != qcur) {
               qcur = k >> 1;
-              xq = pair_block(cp.key0, cp.key1, trial, t, qcur);
+              xq = pair_block_c(trial, t, qcur);
             }
             double z0, z1;
             box_muller((k & 1) ? xq.z : xq.x, (k & 1) ? xq.w : xq.y, z0, z1, logtab);

@@ -179,15 +179,19 @@ void check_cells(const zeus_cell *cells, int n, Errors &E) {
   }
 }
 
-// replay_kernel<WINDOWED, LOG, PHASE> by runtime flags
+// replay_kernel<WINDOWED, LOG, PHASE, ABLATIONS, RK> by runtime flags
 typedef void (*ReplayFn)(zs::ReplayArgs);
-template <bool W, bool L, bool A>
+template <bool W, bool L, bool A, bool RK = false>
 constexpr ReplayFn pick(int phase) {
-  return phase == 0 ? zs::replay_kernel<W, L, 0, A> : phase == 1 ? zs::replay_kernel<W, L, 1, A>
-                                                                 : zs::replay_kernel<W, L, 2, A>;
+  return phase == 0 ? zs::replay_kernel<W, L, 0, A, RK> : phase == 1 ? zs::replay_kernel<W, L, 1, A, RK>
+                                                                     : zs::replay_kernel<W, L, 2, A, RK>;
 }
-// replay_kernel<WINDOWED, LOG, PHASE, ABLATIONS> by runtime flags
-ReplayFn replay_fn(bool windowed, bool log, int phase, bool abl = false) {
+// rk: a one-cell launch whose round keys travel in the parameters (no ablation path)
+ReplayFn replay_fn(bool windowed, bool log, int phase, bool abl = false, bool rk = false) {
+  if (rk && !abl) {
+    if (windowed) return log ? pick<true, true, false, true>(phase) : pick<true, false, false, true>(phase);
+    return log ? pick<false, true, false, true>(phase) : pick<false, false, false, true>(phase);
+  }
   if (abl) {
     if (windowed) return log ? pick<true, true, true>(phase) : pick<true, false, true>(phase);
     return log ? pick<false, true, true>(phase) : pick<false, false, true>(phase);
@@ -499,7 +503,7 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
     const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
     if (bytes > 227 * 1024) continue;
     int blocks = 0;
-    const void *fn = (const void *)replay_fn(wmax > 0, false, two_phase ? 2 : 0, s->any_ablation);
+    const void *fn = (const void *)replay_fn(wmax > 0, false, two_phase ? 2 : 0, s->any_ablation, s->cells.size() == 1);
     int granted = 0;
     ZS_CUDA(s, grant_max_smem(fn, s->device, &granted));
     if ((int)bytes > granted) continue;
@@ -535,8 +539,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   for (int w = 0; w < 2; ++w)
     for (int l = 0; l < 2; ++l)
       for (int ph = 0; ph < 3; ++ph)
-        for (int ab = 0; ab < 2; ++ab)
-          ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph, ab), s->device));
+        for (int ab = 0; ab < 3; ++ab)            // ab == 2: the RK kernels
+          ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph, ab == 1, ab == 2), s->device));
   ZS_CUDA(s, grant_group<2>(s->device));
   ZS_CUDA(s, grant_group<4>(s->device));
   ZS_CUDA(s, grant_group<8>(s->device));
@@ -678,6 +682,20 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     a.opt = s->d_opt.as<double>();
     a.P = s->P;
     a.MP = s->MP;
+    // one-cell launches carry the cell's Philox round keys in the kernel parameters (RK kernels)
+    const bool rk = nc == 1;
+    if (rk) {
+      uint32_t k0 = s->cpar[0].key0, k1 = s->cpar[0].key1;
+      for (int r = 0; r < 10; ++r) {
+        a.rk.k0[r] = k0;
+        a.rk.k1[r] = k1;
+        k0 += 0x9E3779B9u;                   // Philox4x32 key schedule (Weyl constants)
+        k1 += 0xBB67AE85u;
+      }
+    }
+    auto replay_launch = [&](int phase) {
+      replay_fn(windowed, s->log_mode, phase, s->any_ablation, rk)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+    };
     // auto: two phases except for windowed launches, where the one-pass kernel measured
     // faster (CFG4 1.45e10 vs 1.30e10 decisions/s); explicit layouts are honoured
     const bool two_phase = (s->layout == 2 || (s->layout == 0 && !windowed)) && a.t_split < s->R;
@@ -689,13 +707,13 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
       ZS_CUDA(s, cudaGetLastError());
       s->launches += 1;
     } else if (!two_phase) {
-      replay_fn(windowed, s->log_mode, 0, s->any_ablation)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+      replay_launch(0);
       ZS_CUDA(s, cudaGetLastError());
       s->launches += 1;
     } else {
       s->launches += 4;
       ZS_CUDA(s, cudaMemsetAsync(s->d_bucket.p, 0, s->d_bucket.bytes, st));
-      replay_fn(windowed, s->log_mode, 1, s->any_ablation)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+      replay_launch(1);
       ZS_CUDA(s, cudaGetLastError());
       zs::bucket_scan_kernel<<<(unsigned)((nc * (int64_t)s->nwin + 127) / 128), 128, 0, st>>>(a.bucket, nc, s->nwin);
       ZS_CUDA(s, cudaGetLastError());
@@ -703,7 +721,7 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
       zs::bucket_scatter_kernel<<<dim3(std::max(1u, sx), (unsigned)nc), 256, 0, st>>>(
           a.cells, a.carry, a.bucket, a.perm, nc, s->B, s->nwin);
       ZS_CUDA(s, cudaGetLastError());
-      replay_fn(windowed, s->log_mode, 2, s->any_ablation)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+      replay_launch(2);
       ZS_CUDA(s, cudaGetLastError());
     }
   }

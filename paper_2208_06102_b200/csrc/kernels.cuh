@@ -26,6 +26,9 @@
 #ifndef ZS_BOUND_SKIP
 #define ZS_BOUND_SKIP 1
 #endif
+#ifndef ZS_WRITE_BACK
+#define ZS_WRITE_BACK 1
+#endif
 #ifndef ZS_QCACHE
 #define ZS_QCACHE 1
 #endif
@@ -747,7 +750,17 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
         n += 1;
         ArmStat nq;
         nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
+#if ZS_QCACHE && ZS_WRITE_BACK
+        // Thompson phase: the record stays in registers while the trial keeps its arm and is
+        // written back when the trial moves to another arm (and at the end of the launch)
+        if (PHASE == 2) {
+          if (b != qc_b && qc_b >= 0) st[qc_b] = qc;
+        } else {
+          st[b] = nq;
+        }
+#else
         st[b] = nq;
+#endif
 #if ZS_QCACHE
         qc = nq;
         qc_b = b;
@@ -773,6 +786,9 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     }
     return;
   }
+#if ZS_QCACHE && ZS_WRITE_BACK
+  if (PHASE == 2 && active && qc_b >= 0) st[qc_b] = qc;
+#endif
   if (active) {
     a.tot_cost[o] = totC;
     a.tot_energy[o] = totE;

@@ -10,6 +10,8 @@ VARIANTS = {
     "u1": ([], []),
     "qc": (["ZS_QCACHE=1"], []),
     "noqc": (["ZS_QCACHE=0"], []),
+    "wb": (["ZS_WRITE_BACK=1"], []),
+    "nowb": (["ZS_WRITE_BACK=0"], []),
     "sall": (["ZS_SCREEN_ALL=1"], []),
     "lred": (["ZS_LANE_RED=1"], []),
     "clk": (["ZS_REGION_CLOCKS=1"], []),

@@ -245,8 +245,8 @@ __device__ __forceinline__ U4 replica_words(const RoundKeys &rk, int64_t trial, 
                           (uint32_t)((uint64_t)trial >> 32)}, rk);
 }
 __device__ __forceinline__ uint32_t pick_word(const U4 &w, int t) {
-  const int q = t & 3;
-  return q == 0 ? w.x : q == 1 ? w.y : q == 2 ? w.z : w.w;
+  const uint32_t lo = (t & 1) ? w.y : w.x, hi = (t & 1) ? w.w : w.z;   // selects, no branch
+  return (t & 2) ? hi : lo;
 }
 
 }  // namespace zs

@@ -29,6 +29,9 @@
 #ifndef ZS_WRITE_BACK
 #define ZS_WRITE_BACK 1
 #endif
+#ifndef ZS_DIET
+#define ZS_DIET 1
+#endif
 #ifndef ZS_QCACHE
 #define ZS_QCACHE 1
 #endif
@@ -253,11 +256,21 @@ __device__ __forceinline__ void curve_accumulate(double *curves, int t, int lane
   kq += __shfl_xor_sync(0xffffffffu, kq, 1);
   vPacked = (int)__reduce_add_sync(0xffffffffu, (unsigned)vPacked);   // REDUX
   double *row = curves + (size_t)t * kQ;
+#if ZS_DIET
+  // predicated reductions, no branch: lanes 0/8/16/24 add the sums, lanes 0/8/16 the counts
+  const int cntq = (vPacked >> (lane & 24)) & 0xff;       // lane 0: stops, 8: optimal, 16: TS
+  const int p0 = (lane & 7) == 0, p1 = p0 && lane < 24 && cntq;
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p red.global.add.f64 [%0], %1;\n}"
+               :: "l"(row + (lane >> 3)), "d"(kq), "r"(p0) : "memory");
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p red.global.add.f64 [%0], %1;\n}"
+               :: "l"(row + 4 + (lane >> 3)), "d"((double)cntq), "r"(p1) : "memory");
+#else
   if ((lane & 7) == 0) {
     atomicAdd(row + (lane >> 3), kq);
     const int cntq = (vPacked >> (lane & 24)) & 0xff;     // lane 0: stops, 8: optimal, 16: TS
     if (lane < 24 && cntq) atomicAdd(row + 4 + (lane >> 3), (double)cntq);
   }
+#endif
 }
 
 // 1-D bulk copy global -> shared through the TMA unit, completion on an mbarrier.
@@ -297,10 +310,21 @@ enum : int { kStart = 0, kDown = 1, kUp = 2 };
 ZS_C(kRubSlope0, 0.5887050123542859);     // tangent of sqrt(2 ln2 x) at x = 1: slope = intercept
 ZS_C(kRubSlope1, 0.3398889973560289);     // tangent at x = 3
 ZS_C(kRubIcpt1, 1.0196669920680868);
+#if !ZS_DIET
 __device__ __forceinline__ double radius_bound(uint32_t a) {
   const double cc = (double)(__clz(a) + 1);
   return fmin(__fma_ru(cc, kRubSlope0, kRubSlope0), __fma_ru(cc, kRubSlope1, kRubIcpt1));
 }
+#else
+// The same two tangents with their coefficients rounded up to 20-bit mantissas (larger, so still
+// upper bounds), which DFMA takes as immediates; the tangent at clz(a) = 0 is the constant
+// 2 x 0x1.2d6acp-1, and for clz(a) >= 1 the second tangent is the smaller of the two.
+__device__ __forceinline__ double radius_bound(uint32_t a) {
+  const double cc = (double)(__clz(a) + 1);
+  const double l2 = __fma_ru(cc, 0x1.5c0bep-2, 0x1.0508fp+0);
+  return ((int)a < 0) ? 0x1.2d6acp+0 : l2;
+}
+#endif
 // Can an arm of this pair (bits `two`: arms 2k, 2k+1 in the survivor set) still beat the best
 // sample bt?  theta = fma(sigma, z, mu) >= RD(mu - sigma rub) for |z| <= rub, and rounding is
 // monotone, so RD(mu - sigma rub) > bt proves theta > bt: the arm can neither win nor tie.
@@ -622,7 +646,19 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       // Thompson phase every survivor was run (and observed, and profiled) during pruning.
       was_seen = (ZS_SLIM_B && PHASE == 2 && !ABL && !WINDOWED) ? true : ((seen >> b) & 1u);
 #if ZS_QCACHE
+#if ZS_DIET && ZS_WRITE_BACK
+      if (PHASE == 2) {                                     // the trial moves to another arm:
+        if (b != qc_b) {                                    // write the cached record back and
+          if (qc_b >= 0) st[qc_b] = qc;                     // load the new arm's in its place
+          qc = st[b];
+          qc_b = b;
+        }
+      } else {
+        q = st[b];
+      }
+#else
       if (PHASE == 2 && b == qc_b) q = qc; else q = st[b];
+#endif
 #else
       q = st[b];
 #endif
@@ -728,10 +764,15 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     if (active) {
       // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
       {
-        const int cnt = was_seen ? q.cnt : 0;
+#if ZS_DIET && ZS_WRITE_BACK
+        const ArmStat &qr = (PHASE == 2) ? qc : q;          // the record in place (see above)
+#else
+        const ArmStat &qr = q;
+#endif
+        const int cnt = was_seen ? qr.cnt : 0;
         double sh, S1, S2;
         if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
-        else { sh = q.sh; S1 = q.S1; S2 = q.S2; }
+        else { sh = qr.sh; S1 = qr.S1; S2 = qr.S2; }
         int n = cnt;
         if (WINDOWED && cp.window > 0) {
           const int N = cp.window;
@@ -754,7 +795,9 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
         // Thompson phase: the record stays in registers while the trial keeps its arm and is
         // written back when the trial moves to another arm (and at the end of the launch)
         if (PHASE == 2) {
+#if !ZS_DIET
           if (b != qc_b && qc_b >= 0) st[qc_b] = qc;
+#endif
         } else {
           st[b] = nq;
         }
@@ -766,7 +809,11 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
         qc_b = b;
 #endif
         seen |= 1u << b;
+#if ZS_DIET
+        if ((PHASE == 2 && !ABL) || n >= 2) {               // every Thompson-phase arm was run in pruning
+#else
         if (n >= 2) {
+#endif
           s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
           mature |= 1u << b;
           n_recomp += 1;

@@ -11,6 +11,8 @@ VARIANTS = {
     "qc": (["ZS_QCACHE=1"], []),
     "noqc": (["ZS_QCACHE=0"], []),
     "wb": (["ZS_WRITE_BACK=1"], []),
+    "diet": (["ZS_DIET=1"], []),
+    "nodiet": (["ZS_DIET=0"], []),
     "nowb": (["ZS_WRITE_BACK=0"], []),
     "sall": (["ZS_SCREEN_ALL=1"], []),
     "lred": (["ZS_LANE_RED=1"], []),

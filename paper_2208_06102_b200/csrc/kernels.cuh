@@ -668,7 +668,11 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;
       const bool no_jit = ABL && (cp.ablation & 2);
       if (no_jit) {               // ablation "no JIT profiling": the first P runs of
+#if ZS_DIET && ZS_WRITE_BACK
+        const int runs = was_seen ? ((PHASE == 2) ? qc.cnt : q.cnt) : 0;   // b try the limits
+#else
         const int runs = was_seen ? q.cnt : 0;   // b try the limits in ascending order
+#endif
         if (runs < a.P) {
           p = runs;
           const double Ab = __ldg(a.A + (size_t)b * a.P + p), Thb = __ldg(a.Th + (size_t)b * a.P + p);

@@ -400,3 +400,23 @@ def test_bound_screen_every_path(zs, oracle):
         assert c[9] < c[2]                       # pairs screened out
         assert c[10] > c[8]                      # a third residual redrew its block
         compare_cell(oracle, g, w, cells[0], 0, np.arange(trials), R, trials, logs=True)
+
+
+def test_round_key_kernels_match_multicell_launch(zs):
+    """a one-cell launch runs the RK kernels (Philox round keys in the kernel
+    parameters), a multi-cell launch the kernels that derive them from the key; the same cell
+    in both gives the same bits, in both schedules (phase A/B and one pass)."""
+    want = ["digest", "tot_cost", "tot_energy", "tot_time", "final_arm", "n_stop"]
+    (job,) = synth.config("cfg5", trials=3000)
+    other = synth.cell(eta=0.3, beta=3.0, seed=99)
+    for layout in (1, 2):
+        one = zs.Simulation(job.workload, job.cells, job.trials, 300, layout=layout).load_profile()
+        a = one.run().results(want=want)
+        one.close()
+        two = zs.Simulation(job.workload, [job.cells[0], other], job.trials, 300,
+                            layout=layout).load_profile()
+        b = two.run().results(want=want)
+        two.close()
+        for k in want:
+            assert np.array_equal(np.asarray(a[k]).reshape(-1)[:job.trials],
+                                  np.asarray(b[k]).reshape(-1)[:job.trials]), (layout, k)

@@ -32,6 +32,9 @@
 #ifndef ZS_DIET
 #define ZS_DIET 1
 #endif
+#ifndef ZS_ONEPASS_CACHE
+#define ZS_ONEPASS_CACHE 1
+#endif
 #ifndef ZS_QCACHE
 #define ZS_QCACHE 1
 #endif
@@ -487,6 +490,9 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     int b = 0;
     bool was_seen = false;
     ArmStat q;
+#if ZS_ONEPASS_CACHE
+    double y_old = 0.0;
+#endif
     double C = 0.0;
     if (S > 1)                                              // no 64-bit division per decision
       while ((long long)(s + 1) * R <= (long long)t * S) ++s;
@@ -647,15 +653,22 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       was_seen = (ZS_SLIM_B && PHASE == 2 && !ABL && !WINDOWED) ? true : ((seen >> b) & 1u);
 #if ZS_QCACHE
 #if ZS_DIET && ZS_WRITE_BACK
-      if (PHASE == 2) {                                     // the trial moves to another arm:
+      if (PHASE == 2 || ZS_ONEPASS_CACHE) {                 // the trial moves to another arm:
         if (b != qc_b) {                                    // write the cached record back and
-          if (qc_b >= 0) st[qc_b] = qc;                     // load the new arm's in its place
-          qc = st[b];
+          if (PHASE == 2 && qc_b >= 0) st[qc_b] = qc;       // load the new arm's in its place
+          qc = st[b];                                       // (phases 0/1 write through)
           qc_b = b;
         }
       } else {
         q = st[b];
       }
+#if ZS_ONEPASS_CACHE
+      // the windowed Observe's evicted cost, loaded as soon as the decision is known
+      if (WINDOWED && cp.window > 0) {
+        const int cnt0 = was_seen ? qc.cnt : 0;
+        if (cnt0 >= cp.window) y_old = a.st_ring[(o * B + b) * (size_t)a.ring_n + (cnt0 % cp.window)];
+      }
+#endif
 #else
       if (PHASE == 2 && b == qc_b) q = qc; else q = st[b];
 #endif
@@ -669,7 +682,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       const bool no_jit = ABL && (cp.ablation & 2);
       if (no_jit) {               // ablation "no JIT profiling": the first P runs of
 #if ZS_DIET && ZS_WRITE_BACK
-        const int runs = was_seen ? ((PHASE == 2) ? qc.cnt : q.cnt) : 0;   // b try the limits
+        const int runs = was_seen ? ((PHASE == 2 || ZS_ONEPASS_CACHE) ? qc.cnt : q.cnt) : 0;
 #else
         const int runs = was_seen ? q.cnt : 0;   // b try the limits in ascending order
 #endif
@@ -769,7 +782,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
       {
 #if ZS_DIET && ZS_WRITE_BACK
-        const ArmStat &qr = (PHASE == 2) ? qc : q;          // the record in place (see above)
+        const ArmStat &qr = (PHASE == 2 || ZS_ONEPASS_CACHE) ? qc : q;   // the record in place
 #else
         const ArmStat &qr = q;
 #endif
@@ -782,7 +795,11 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
           const int N = cp.window;
           double *slot = &a.st_ring[(o * B + b) * (size_t)a.ring_n + (cnt % N)];
           if (cnt >= N) {
+#if ZS_ONEPASS_CACHE
+            const double dy = y_old - sh;
+#else
             const double dy = *slot - sh;
+#endif
             S1 = S1 - dy;
             S2 = S2 - dy * dy;
             n = N - 1;

@@ -13,6 +13,8 @@ VARIANTS = {
     "wb": (["ZS_WRITE_BACK=1"], []),
     "diet": (["ZS_DIET=1"], []),
     "nodiet": (["ZS_DIET=0"], []),
+    "opc": (["ZS_ONEPASS_CACHE=1"], []),
+    "noopc": (["ZS_ONEPASS_CACHE=0"], []),
     "nowb": (["ZS_WRITE_BACK=0"], []),
     "sall": (["ZS_SCREEN_ALL=1"], []),
     "lred": (["ZS_LANE_RED=1"], []),

@@ -35,6 +35,9 @@
 #ifndef ZS_ONEPASS_CACHE
 #define ZS_ONEPASS_CACHE 1
 #endif
+#ifndef ZS_KERNEL_CACHE
+#define ZS_KERNEL_CACHE 1
+#endif
 #ifndef ZS_QCACHE
 #define ZS_QCACHE 1
 #endif
@@ -962,6 +965,10 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
   uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
   int s = 0;
   U4 rw{0u, 0u, 0u, 0u};
+#if ZS_KERNEL_CACHE
+  ArmStat qc{0.0, 0.0, 0.0, 0, 0};                     // the last arm's record (read cache)
+  int qc_b = -1;
+#endif
   for (int t = 0; t < R; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0;
@@ -1028,7 +1035,11 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
     double C = 0.0;
     if (active) {
       was_seen = (seen >> b) & 1u;
+#if ZS_KERNEL_CACHE
+      if (b == qc_b) q = qc; else q = st[b];
+#else
       q = st[b];
+#endif
       const ArmConst ac = arm[b];
       const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
       const int E = pool[((size_t)s * B + b) * K + r];
@@ -1131,10 +1142,14 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
       S1 = S1 + d;
       S2 = S2 + d * d;
       n += 1;
-      if (leader) {
+      {
         ArmStat nq;
         nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
-        st[b] = nq;
+        if (leader) st[b] = nq;
+#if ZS_KERNEL_CACHE
+        qc = nq;                                            // every lane of the group keeps it
+        qc_b = b;
+#endif
       }
       seen |= 1u << b;
       if (n >= 2) {
@@ -1279,6 +1294,10 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
   uint32_t q_flags[kMaxOutstanding];                         // bit0 converged, bit1 walk
   int nq = 0;
 
+#if ZS_KERNEL_CACHE
+  ArmStat qc{0.0, 0.0, 0.0, 0, 0};                     // the last arm's record (read cache)
+  int qc_b = -1;
+#endif
   // a run's outcome reaching the optimiser
   auto complete = [&](int i) {
     const int b = q_b[i];
@@ -1287,7 +1306,12 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
     if (conv && !(C >= best)) { best = C; best_arm = b; }
     {                                                        // Alg. 2 Observe (NC-6)
       const bool was_seen = (seen >> b) & 1u;
+#if ZS_KERNEL_CACHE
+      ArmStat q;
+      if (b == qc_b) q = qc; else q = st[b];
+#else
       const ArmStat q = st[b];
+#endif
       const int cnt = was_seen ? q.cnt : 0;
       double sh, S1, S2;
       if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
@@ -1311,6 +1335,10 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
       ArmStat nq_;
       nq_.sh = sh; nq_.S1 = S1; nq_.S2 = S2; nq_.cnt = cnt + 1; nq_.pad = 0;
       st[b] = nq_;
+#if ZS_KERNEL_CACHE
+      qc = nq_;
+      qc_b = b;
+#endif
       seen |= 1u << b;
       if (n >= 2) {
         s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
@@ -1555,6 +1583,10 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
 
   int s = 0;
   U4 rw{0u, 0u, 0u, 0u};
+#if ZS_KERNEL_CACHE
+  ArmStat qc{0.0, 0.0, 0.0, 0, 0};                     // the last arm's record (read cache)
+  int qc_b = -1;
+#endif
   for (int t = 0; t < R; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     uint32_t cStop = 0, cOpt = 0, cTs = 0;
@@ -1619,7 +1651,12 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
         }
         // the power limit; "no JIT" tries the limits in ascending order first
         const bool was_seen = (seen >> b) & 1u;
+#if ZS_KERNEL_CACHE
+        ArmStat q;
+        if (b == qc_b) q = qc; else q = st[b];
+#else
         const ArmStat q = st[b];
+#endif
         const ArmConst ac = arm[b];
         int p = ac.pstar;
         double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;
@@ -1718,6 +1755,10 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
           ArmStat nq;
           nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
           st[b] = nq;
+#if ZS_KERNEL_CACHE
+          qc = nq;
+          qc_b = b;
+#endif
           seen |= 1u << b;
           if (n >= 2) {
             s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);

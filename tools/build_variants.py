@@ -15,6 +15,7 @@ VARIANTS = {
     "nodiet": (["ZS_DIET=0"], []),
     "opc": (["ZS_ONEPASS_CACHE=1"], []),
     "noopc": (["ZS_ONEPASS_CACHE=0"], []),
+    "kc": (["ZS_KERNEL_CACHE=1"], []),
     "nowb": (["ZS_WRITE_BACK=0"], []),
     "sall": (["ZS_SCREEN_ALL=1"], []),
     "lred": (["ZS_LANE_RED=1"], []),

@@ -1030,6 +1030,7 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
       bb = take ? ob : bb;
     }
     if (sampled) b = bb;
+    __syncwarp();                                            // the draw's reads before lane 0's stores
     bool was_seen = false;
     ArmStat q;
     double C = 0.0;

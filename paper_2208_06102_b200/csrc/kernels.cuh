@@ -26,21 +26,6 @@
 #ifndef ZS_BOUND_SKIP
 #define ZS_BOUND_SKIP 1
 #endif
-#ifndef ZS_WRITE_BACK
-#define ZS_WRITE_BACK 1
-#endif
-#ifndef ZS_DIET
-#define ZS_DIET 1
-#endif
-#ifndef ZS_ONEPASS_CACHE
-#define ZS_ONEPASS_CACHE 1
-#endif
-#ifndef ZS_KERNEL_CACHE
-#define ZS_KERNEL_CACHE 1
-#endif
-#ifndef ZS_QCACHE
-#define ZS_QCACHE 1
-#endif
 
 namespace zs {
 
@@ -262,7 +247,6 @@ __device__ __forceinline__ void curve_accumulate(double *curves, int t, int lane
   kq += __shfl_xor_sync(0xffffffffu, kq, 1);
   vPacked = (int)__reduce_add_sync(0xffffffffu, (unsigned)vPacked);   // REDUX
   double *row = curves + (size_t)t * kQ;
-#if ZS_DIET
   // predicated reductions, no branch: lanes 0/8/16/24 add the sums, lanes 0/8/16 the counts
   const int cntq = (vPacked >> (lane & 24)) & 0xff;       // lane 0: stops, 8: optimal, 16: TS
   const int p0 = (lane & 7) == 0, p1 = p0 && lane < 24 && cntq;
@@ -270,13 +254,6 @@ __device__ __forceinline__ void curve_accumulate(double *curves, int t, int lane
                :: "l"(row + (lane >> 3)), "d"(kq), "r"(p0) : "memory");
   asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p red.global.add.f64 [%0], %1;\n}"
                :: "l"(row + 4 + (lane >> 3)), "d"((double)cntq), "r"(p1) : "memory");
-#else
-  if ((lane & 7) == 0) {
-    atomicAdd(row + (lane >> 3), kq);
-    const int cntq = (vPacked >> (lane & 24)) & 0xff;     // lane 0: stops, 8: optimal, 16: TS
-    if (lane < 24 && cntq) atomicAdd(row + 4 + (lane >> 3), (double)cntq);
-  }
-#endif
 }
 
 // 1-D bulk copy global -> shared through the TMA unit, completion on an mbarrier.
@@ -316,12 +293,6 @@ enum : int { kStart = 0, kDown = 1, kUp = 2 };
 ZS_C(kRubSlope0, 0.5887050123542859);     // tangent of sqrt(2 ln2 x) at x = 1: slope = intercept
 ZS_C(kRubSlope1, 0.3398889973560289);     // tangent at x = 3
 ZS_C(kRubIcpt1, 1.0196669920680868);
-#if !ZS_DIET
-__device__ __forceinline__ double radius_bound(uint32_t a) {
-  const double cc = (double)(__clz(a) + 1);
-  return fmin(__fma_ru(cc, kRubSlope0, kRubSlope0), __fma_ru(cc, kRubSlope1, kRubIcpt1));
-}
-#else
 // The same two tangents with their coefficients rounded up to 20-bit mantissas (larger, so still
 // upper bounds), which DFMA takes as immediates; the tangent at clz(a) = 0 is the constant
 // 2 x 0x1.2d6acp-1, and for clz(a) >= 1 the second tangent is the smaller of the two.
@@ -330,7 +301,6 @@ __device__ __forceinline__ double radius_bound(uint32_t a) {
   const double l2 = __fma_ru(cc, 0x1.5c0bep-2, 0x1.0508fp+0);
   return ((int)a < 0) ? 0x1.2d6acp+0 : l2;
 }
-#endif
 // Can an arm of this pair (bits `two`: arms 2k, 2k+1 in the survivor set) still beat the best
 // sample bt?  theta = fma(sigma, z, mu) >= RD(mu - sigma rub) for |z| <= rub, and rounding is
 // monotone, so RD(mu - sigma rub) > bt proves theta > bt: the arm can neither win nor tie.
@@ -479,12 +449,10 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const int t_end = PHASE == 1 ? a.t_split : R;
   int s = 0;                                                // slice of t = floor(t*S/R) (R-Q19)
   U4 rw{0u, 0u, 0u, 0u};
-#if ZS_QCACHE
   // the Observe record of the last arm observed, kept in registers: Thompson sampling mostly
   // repeats its arm, and then the decision needs no load of the record (same values)
   ArmStat qc{0.0, 0.0, 0.0, 0, 0};
   int qc_b = -1;
-#endif
   for (int t = t_begin; t < t_end; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0;
@@ -492,10 +460,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     // the latency of the arm-state load hides behind the shuffles
     int b = 0;
     bool was_seen = false;
-    ArmStat q;
-#if ZS_ONEPASS_CACHE
-    double y_old = 0.0;
-#endif
+    double y_old = 0.0;                                     // windowed: the cost leaving the window
     double C = 0.0;
     if (S > 1)                                              // no 64-bit division per decision
       while ((long long)(s + 1) * R <= (long long)t * S) ++s;
@@ -651,44 +616,28 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
           n_sampled += 1;
         }
       }
-      // Observe statistics of arm b: issue the load now, consume after the curves.  In the
-      // Thompson phase every survivor was run (and observed, and profiled) during pruning.
+      // Observe statistics of arm b: the last observed arm's record lives in
+      // registers (qc); when the trial moves to another arm the Thompson phase writes it back
+      // (phases 0/1 write through) and loads the new arm's in its place, to be consumed after the
+      // curves.  In the Thompson phase every survivor was run (and observed) during pruning.
       was_seen = (ZS_SLIM_B && PHASE == 2 && !ABL && !WINDOWED) ? true : ((seen >> b) & 1u);
-#if ZS_QCACHE
-#if ZS_DIET && ZS_WRITE_BACK
-      if (PHASE == 2 || ZS_ONEPASS_CACHE) {                 // the trial moves to another arm:
-        if (b != qc_b) {                                    // write the cached record back and
-          if (PHASE == 2 && qc_b >= 0) st[qc_b] = qc;       // load the new arm's in its place
-          qc = st[b];                                       // (phases 0/1 write through)
-          qc_b = b;
-        }
-      } else {
-        q = st[b];
+      if (b != qc_b) {
+        if (PHASE == 2 && qc_b >= 0) st[qc_b] = qc;
+        qc = st[b];
+        qc_b = b;
       }
-#if ZS_ONEPASS_CACHE
       // the windowed Observe's evicted cost, loaded as soon as the decision is known
       if (WINDOWED && cp.window > 0) {
         const int cnt0 = was_seen ? qc.cnt : 0;
         if (cnt0 >= cp.window) y_old = a.st_ring[(o * B + b) * (size_t)a.ring_n + (cnt0 % cp.window)];
       }
-#endif
-#else
-      if (PHASE == 2 && b == qc_b) q = qc; else q = st[b];
-#endif
-#else
-      q = st[b];
-#endif
       const ArmConst ac = arm[b];
       // the power limit accompanying b and its per-epoch cost/time/energy
       int p = ac.pstar;
       double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;
       const bool no_jit = ABL && (cp.ablation & 2);
       if (no_jit) {               // ablation "no JIT profiling": the first P runs of
-#if ZS_DIET && ZS_WRITE_BACK
-        const int runs = was_seen ? ((PHASE == 2 || ZS_ONEPASS_CACHE) ? qc.cnt : q.cnt) : 0;
-#else
-        const int runs = was_seen ? q.cnt : 0;   // b try the limits in ascending order
-#endif
+        const int runs = was_seen ? qc.cnt : 0;            // b try the limits in ascending order
         if (runs < a.P) {
           p = runs;
           const double Ab = __ldg(a.A + (size_t)b * a.P + p), Thb = __ldg(a.Th + (size_t)b * a.P + p);
@@ -784,11 +733,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     if (active) {
       // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
       {
-#if ZS_DIET && ZS_WRITE_BACK
-        const ArmStat &qr = (PHASE == 2 || ZS_ONEPASS_CACHE) ? qc : q;   // the record in place
-#else
-        const ArmStat &qr = q;
-#endif
+        const ArmStat &qr = qc;                             // the record (see the decision)
         const int cnt = was_seen ? qr.cnt : 0;
         double sh, S1, S2;
         if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
@@ -798,11 +743,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
           const int N = cp.window;
           double *slot = &a.st_ring[(o * B + b) * (size_t)a.ring_n + (cnt % N)];
           if (cnt >= N) {
-#if ZS_ONEPASS_CACHE
             const double dy = y_old - sh;
-#else
-            const double dy = *slot - sh;
-#endif
             S1 = S1 - dy;
             S2 = S2 - dy * dy;
             n = N - 1;
@@ -815,29 +756,13 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
         n += 1;
         ArmStat nq;
         nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
-#if ZS_QCACHE && ZS_WRITE_BACK
-        // Thompson phase: the record stays in registers while the trial keeps its arm and is
-        // written back when the trial moves to another arm (and at the end of the launch)
-        if (PHASE == 2) {
-#if !ZS_DIET
-          if (b != qc_b && qc_b >= 0) st[qc_b] = qc;
-#endif
-        } else {
-          st[b] = nq;
-        }
-#else
-        st[b] = nq;
-#endif
-#if ZS_QCACHE
+        // the Thompson phase writes the record back when the trial moves to another arm (and
+        // at the end of the launch); phases 0/1 write through
+        if (PHASE != 2) st[b] = nq;
         qc = nq;
         qc_b = b;
-#endif
         seen |= 1u << b;
-#if ZS_DIET
         if ((PHASE == 2 && !ABL) || n >= 2) {               // every Thompson-phase arm was run in pruning
-#else
-        if (n >= 2) {
-#endif
           s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
           mature |= 1u << b;
           n_recomp += 1;
@@ -857,9 +782,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     }
     return;
   }
-#if ZS_QCACHE && ZS_WRITE_BACK
   if (PHASE == 2 && active && qc_b >= 0) st[qc_b] = qc;
-#endif
   if (active) {
     a.tot_cost[o] = totC;
     a.tot_energy[o] = totE;
@@ -965,10 +888,8 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
   uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
   int s = 0;
   U4 rw{0u, 0u, 0u, 0u};
-#if ZS_KERNEL_CACHE
   ArmStat qc{0.0, 0.0, 0.0, 0, 0};                     // the last arm's record (read cache)
   int qc_b = -1;
-#endif
   for (int t = 0; t < R; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0;
@@ -1036,11 +957,7 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
     double C = 0.0;
     if (active) {
       was_seen = (seen >> b) & 1u;
-#if ZS_KERNEL_CACHE
       if (b == qc_b) q = qc; else q = st[b];
-#else
-      q = st[b];
-#endif
       const ArmConst ac = arm[b];
       const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
       const int E = pool[((size_t)s * B + b) * K + r];
@@ -1147,10 +1064,8 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
         ArmStat nq;
         nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
         if (leader) st[b] = nq;
-#if ZS_KERNEL_CACHE
         qc = nq;                                            // every lane of the group keeps it
         qc_b = b;
-#endif
       }
       seen |= 1u << b;
       if (n >= 2) {
@@ -1295,10 +1210,8 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
   uint32_t q_flags[kMaxOutstanding];                         // bit0 converged, bit1 walk
   int nq = 0;
 
-#if ZS_KERNEL_CACHE
   ArmStat qc{0.0, 0.0, 0.0, 0, 0};                     // the last arm's record (read cache)
   int qc_b = -1;
-#endif
   // a run's outcome reaching the optimiser
   auto complete = [&](int i) {
     const int b = q_b[i];
@@ -1307,12 +1220,8 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
     if (conv && !(C >= best)) { best = C; best_arm = b; }
     {                                                        // Alg. 2 Observe (NC-6)
       const bool was_seen = (seen >> b) & 1u;
-#if ZS_KERNEL_CACHE
       ArmStat q;
       if (b == qc_b) q = qc; else q = st[b];
-#else
-      const ArmStat q = st[b];
-#endif
       const int cnt = was_seen ? q.cnt : 0;
       double sh, S1, S2;
       if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
@@ -1336,10 +1245,8 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
       ArmStat nq_;
       nq_.sh = sh; nq_.S1 = S1; nq_.S2 = S2; nq_.cnt = cnt + 1; nq_.pad = 0;
       st[b] = nq_;
-#if ZS_KERNEL_CACHE
       qc = nq_;
       qc_b = b;
-#endif
       seen |= 1u << b;
       if (n >= 2) {
         s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
@@ -1584,10 +1491,8 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
 
   int s = 0;
   U4 rw{0u, 0u, 0u, 0u};
-#if ZS_KERNEL_CACHE
   ArmStat qc{0.0, 0.0, 0.0, 0, 0};                     // the last arm's record (read cache)
   int qc_b = -1;
-#endif
   for (int t = 0; t < R; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     uint32_t cStop = 0, cOpt = 0, cTs = 0;
@@ -1652,12 +1557,8 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
         }
         // the power limit; "no JIT" tries the limits in ascending order first
         const bool was_seen = (seen >> b) & 1u;
-#if ZS_KERNEL_CACHE
         ArmStat q;
         if (b == qc_b) q = qc; else q = st[b];
-#else
-        const ArmStat q = st[b];
-#endif
         const ArmConst ac = arm[b];
         int p = ac.pstar;
         double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;
@@ -1756,10 +1657,8 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
           ArmStat nq;
           nq.sh = sh; nq.S1 = S1; nq.S2 = S2; nq.cnt = cnt + 1; nq.pad = 0;
           st[b] = nq;
-#if ZS_KERNEL_CACHE
           qc = nq;
           qc_b = b;
-#endif
           seen |= 1u << b;
           if (n >= 2) {
             s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);

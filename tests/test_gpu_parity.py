@@ -420,3 +420,22 @@ def test_round_key_kernels_match_multicell_launch(zs):
         for k in want:
             assert np.array_equal(np.asarray(a[k]).reshape(-1)[:job.trials],
                                   np.asarray(b[k]).reshape(-1)[:job.trials]), (layout, k)
+
+
+@pytest.mark.parametrize("B,P,S,K,window,beta,trials,R", [
+    (32, 8, 1, 4, 0, 2.0, 200, 100),      # 32 arms: 16 pairs, 8 quads, three-residual redraws
+    (17, 5, 2, 3, 4, 2.0, 150, 60),       # odd arm count, window, two slices
+    (6, 7, 40, 4, 10, 2.0, 300, 40),      # drift-shaped: one slice per recurrence, window N = 10
+    (3, 4, 1, 2, 0, math.inf, 130, 30),   # two pairs, no early stop
+])
+@pytest.mark.parametrize("layout", [1, 2])
+def test_random_traces_one_cell(zs, oracle, B, P, S, K, window, beta, trials, R, layout):
+    """One-cell launches run the RK kernels (round keys in the parameters, the
+    record cache with write-back in the Thompson phase); edge shapes in both schedules,
+    every decision bit-exact vs the oracle."""
+    rng = np.random.default_rng(B * 7919 + S)
+    w = _random_trace(rng, B, P, S, K)
+    cell = synth.cell(eta=0.6, beta=beta, window=window, seed=int(rng.integers(2**63)))
+    g = run_gpu(zs, w, [cell], trials, R, log=True, layout=layout)
+    compare_step1(oracle, g, w, [cell])
+    compare_cell(oracle, g, w, cell, 0, np.arange(trials), R, trials, logs=True)

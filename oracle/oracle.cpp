@@ -256,6 +256,37 @@ uint32_t replica_attempt(uint64_t seed, int64_t trial, int32_t t, int32_t j, int
   return (uint32_t)(((uint64_t)x[0] * (uint64_t)K) >> 32);
 }
 
+// ---------------------------------------------------------------- Predict (Alg. 1)
+struct Counters { int64_t c[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}; };
+
+// Alg. 1: for every batch size b of the set, sample θ̂_b ~ N(μ̂_b, σ̂_b²) and
+// return argmin_b θ̂_b (strict <, ascending b: ties go to the smaller index, NC-4).  The
+// normal of arm b at recurrence t (attempt j) is one half of the Box-Muller pair k = b >> 1
+// (NC-3); θ̂_b = fma(σ̂_b, z, μ̂_b).  `set` is a bitmask of arms; returns -1 for an empty set.
+int thompson_argmin(uint64_t seed, int64_t trial, int32_t t, int32_t j, int B, uint32_t set,
+                    const double *mu, const double *sigma, Counters &cnt) {
+  int b = -1;
+  double best_theta = std::numeric_limits<double>::infinity();
+  int last_block = -1;
+  for (int k = 0; 2 * k < B; ++k) {
+    uint32_t pairmask = (set >> (2 * k)) & 3u;
+    if (!pairmask) continue;
+    if ((k >> 1) != last_block) { last_block = k >> 1; cnt.c[8] += 1; }
+    double z[2];
+    normal_pair_attempt(seed, trial, t, j, k, &z[0], &z[1]);
+    cnt.c[2] += 1;
+    for (int h = 0; h < 2; ++h) {
+      int a = 2 * k + h;
+      if (!(pairmask & (1u << h))) continue;
+      double theta = std::fma(sigma[a], z[h], mu[a]);
+      cnt.c[3] += 1;
+      if (theta < best_theta) { best_theta = theta; b = a; }
+    }
+  }
+  cnt.c[1] += 1;
+  return b;
+}
+
 // ---------------------------------------------------------------- Observe (Alg. 2)
 // One arm's belief.  Var(C_b) and Sum(C_b) of Alg. 2 are kept as
 // sums shifted by the arm's first observation (NC-6); the window of the N most
@@ -459,8 +490,6 @@ struct TrialResult {
   int32_t n_stop = 0, final_arm = -1;
 };
 
-struct Counters { int64_t c[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}; };
-
 // Per-epoch cost, time and energy of configuration (b, p) -- the quantity inside the
 // min of Eq. 7, in the NC-2 operation order.
 void epoch_cost(const oracle_trace &tr, const oracle_cell &cell, int b, int p, double *c,
@@ -543,6 +572,7 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
   const int B = tr.num_batch_sizes, S = tr.num_slices, K = tr.replicas;
   const Prior pr = make_prior(cell.prior_mean, cell.prior_var);
   std::vector<Arm> arm(B);
+  std::vector<double> mu(B), sigma(B);                      // the posteriors Predict reads
   double best = std::numeric_limits<double>::infinity();   // min_t C_t
 
   // Alg. 3 state
@@ -654,25 +684,8 @@ void run_trial(const oracle_trace &tr, const oracle_cell &cell, const Tables &T,
       for (int a = 0; a < B; ++a)           // arms without a variance estimate first (R-Q6)
         if ((eligible & (1u << a)) && (int)arm[a].window.size() < 2) { b = a; break; }
       if (b < 0) {
-        // Alg. 1: θ̂_b ~ N(μ̂_b, σ̂_b²) for every b, b* = argmin θ̂_b
-        double best_theta = std::numeric_limits<double>::infinity();
-        int last_block = -1;
-        for (int k = 0; 2 * k < B; ++k) {
-          uint32_t pairmask = (eligible >> (2 * k)) & 3u;
-          if (!pairmask) continue;
-          if ((k >> 1) != last_block) { last_block = k >> 1; cnt.c[8] += 1; }
-          double z[2];
-          normal_pair_attempt(cell.seed, trial, t, j, k, &z[0], &z[1]);
-          cnt.c[2] += 1;
-          for (int h = 0; h < 2; ++h) {
-            int a = 2 * k + h;
-            if (!(pairmask & (1u << h))) continue;
-            double theta = std::fma(arm[a].sigma, z[h], arm[a].mu);
-            cnt.c[3] += 1;
-            if (theta < best_theta) { best_theta = theta; b = a; }
-          }
-        }
-        cnt.c[1] += 1;
+        for (int a = 0; a < B; ++a) { mu[a] = arm[a].mu; sigma[a] = arm[a].sigma; }
+        b = thompson_argmin(cell.seed, trial, t, j, B, eligible, mu.data(), sigma.data(), cnt);
       } else {
         cnt.c[6] += 1;
       }
@@ -926,6 +939,12 @@ void oracle_normal_pair(uint64_t seed, int64_t trial, int32_t t, int32_t k, doub
 }
 uint32_t oracle_replica(uint64_t seed, int64_t trial, int32_t t, int32_t K) {
   return replica(seed, trial, t, K);
+}
+int32_t oracle_thompson_argmin(uint64_t seed, int64_t trial, int32_t t, int32_t B, uint32_t set,
+                               const double *mu, const double *sigma) {
+  if (B < 1 || B > 32) return -1;
+  Counters cnt;
+  return thompson_argmin(seed, trial, t, 0, B, set, mu, sigma, cnt);
 }
 int oracle_posterior(const double *xs, int32_t n, int32_t window, double prior_mean,
                      double prior_var, double *mu, double *sigma, double *s2, double *var) {

@@ -94,6 +94,10 @@ void oracle_zsincospi(uint64_t m52, double *s, double *c);
 void oracle_uniforms(uint32_t a, uint32_t b, double *u1, double *v);
 void oracle_normal_pair(uint64_t seed, int64_t trial, int32_t t, int32_t k, double *z0, double *z1);
 uint32_t oracle_replica(uint64_t seed, int64_t trial, int32_t t, int32_t K);
+/* Alg. 1 Predict over the arms in bitmask `set` with posteriors (mu, sigma)[B]: the arm the
+ * replay of (seed, trial) picks at recurrence t; -1 for an empty set */
+int32_t oracle_thompson_argmin(uint64_t seed, int64_t trial, int32_t t, int32_t B, uint32_t set,
+                               const double *mu, const double *sigma);
 int oracle_posterior(const double *xs, int32_t n, int32_t window, double prior_mean,
                      double prior_var, double *mu, double *sigma, double *s2, double *var);
 int32_t oracle_hardware_threads(void);

@@ -115,6 +115,9 @@ def lib():
                                          C.POINTER(C.c_double), C.POINTER(C.c_double)]
         L.oracle_replica.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32]
         L.oracle_replica.restype = C.c_uint32
+        L.oracle_thompson_argmin.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_uint32,
+                                             C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.oracle_thompson_argmin.restype = C.c_int32
         L.oracle_posterior.argtypes = [C.POINTER(C.c_double), C.c_int32, C.c_int32, C.c_double,
                                        C.c_double] + [C.POINTER(C.c_double)] * 4
         L.oracle_hardware_threads.restype = C.c_int32
@@ -246,6 +249,16 @@ def normal_pair(seed, trial, t, k):
 
 def replica(seed, trial, t, K):
     return lib().oracle_replica(int(seed), int(trial), int(t), int(K))
+
+
+def thompson_argmin(seed, trial, t, mu, sigma, arms=None):
+    """Alg. 1 Predict as the replay runs it: the arm picked among ``arms`` (default: all)."""
+    mu = np.ascontiguousarray(mu, np.float64)
+    sigma = np.ascontiguousarray(sigma, np.float64)
+    B = len(mu)
+    mask = sum(1 << a for a in (range(B) if arms is None else arms))
+    return int(lib().oracle_thompson_argmin(int(seed), int(trial), int(t), B, mask,
+                                            _p(mu, C.c_double), _p(sigma, C.c_double)))
 
 
 def posterior(xs, window=0, prior_mean=0.0, prior_var=np.inf):

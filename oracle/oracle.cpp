@@ -957,6 +957,26 @@ int oracle_posterior(const double *xs, int32_t n, int32_t window, double prior_m
   *sigma = a.sigma;
   return 0;
 }
+// Batches of the primitives for the large-sample pins (tests/test_sampler_scale.py).
+void oracle_zlog_batch(const double *x, double *y, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) y[i] = zlog(x[i]);
+}
+void oracle_zsincospi_batch(const uint64_t *m, double *s, double *c, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) zsincospi(m[i], s + i, c + i);
+}
+// out[2j], out[2j+1] = the Box-Muller pair k of trial trial0 + j at recurrence t
+void oracle_normal_batch(uint64_t seed, int64_t trial0, int64_t n, int32_t t, int32_t k,
+                         int32_t threads, double *out) {
+  if (threads < 1) threads = 1;
+  auto work = [&](int w) {
+    for (int64_t j = w; j < n; j += threads)
+      normal_pair(seed, trial0 + j, t, k, out + 2 * j, out + 2 * j + 1);
+  };
+  std::vector<std::thread> pool;
+  for (int w = 1; w < threads; ++w) pool.emplace_back(work, w);
+  work(0);
+  for (auto &th : pool) th.join();
+}
 int32_t oracle_hardware_threads(void) {
   unsigned h = std::thread::hardware_concurrency();
   return h == 0 ? 1 : (int32_t)h;

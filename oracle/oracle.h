@@ -101,6 +101,11 @@ int32_t oracle_thompson_argmin(uint64_t seed, int64_t trial, int32_t t, int32_t 
 int oracle_posterior(const double *xs, int32_t n, int32_t window, double prior_mean,
                      double prior_var, double *mu, double *sigma, double *s2, double *var);
 int32_t oracle_hardware_threads(void);
+/* batches of the primitives (large-sample pins) */
+void oracle_zlog_batch(const double *x, double *y, int64_t n);
+void oracle_zsincospi_batch(const uint64_t *m, double *s, double *c, int64_t n);
+void oracle_normal_batch(uint64_t seed, int64_t trial0, int64_t n, int32_t t, int32_t k,
+                         int32_t threads, double *out);
 
 #ifdef __cplusplus
 }

@@ -121,6 +121,11 @@ def lib():
         L.oracle_posterior.argtypes = [C.POINTER(C.c_double), C.c_int32, C.c_int32, C.c_double,
                                        C.c_double] + [C.POINTER(C.c_double)] * 4
         L.oracle_hardware_threads.restype = C.c_int32
+        L.oracle_zlog_batch.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64]
+        L.oracle_zsincospi_batch.argtypes = [C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                             C.POINTER(C.c_double), C.c_int64]
+        L.oracle_normal_batch.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int32, C.c_int32,
+                                          C.c_int32, C.POINTER(C.c_double)]
         L.oracle_pareto.argtypes = [C.POINTER(Trace), C.c_int32, C.POINTER(C.c_uint8)]
         _lib = L
     return _lib
@@ -279,6 +284,28 @@ def pareto(w, s=0):
     if lib().oracle_pareto(C.byref(h.tr), int(s), _p(m, C.c_uint8)) != 0:
         raise ValueError("bad slice")
     return m
+
+
+def zlog_batch(x):
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.empty_like(x)
+    lib().oracle_zlog_batch(_p(x, C.c_double), _p(y, C.c_double), len(x))
+    return y
+
+
+def zsincospi_batch(m):
+    m = np.ascontiguousarray(m, np.uint64)
+    s, c = np.empty(len(m)), np.empty(len(m))
+    lib().oracle_zsincospi_batch(_p(m, C.c_uint64), _p(s, C.c_double), _p(c, C.c_double), len(m))
+    return s, c
+
+
+def normal_batch(seed, trial0, n, t, k, threads=1):
+    """[n][2]: the Box-Muller pair k of trials trial0 .. trial0+n-1 at recurrence t (NC-3)."""
+    out = np.empty((n, 2))
+    lib().oracle_normal_batch(int(seed), int(trial0), int(n), int(t), int(k), int(threads),
+                              _p(out, C.c_double))
+    return out
 
 
 def hardware_threads():

@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dump", default=None,
+                    help="directory: each rank writes rank<r>.npz (shard, per-trial digests and "
+                         "costs, curves) after the timed steps (multi-rank parity tests)")
     return ap.parse_args()
 
 
@@ -119,26 +122,74 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ work model
-def work_per_launch(counters, _unused=None):
-    """Algorithmic lane-instructions of one launch: the work the replay evaluated x per-primitive
-    sm_100a SASS costs of the contract (tools/work_model.json):
-      per Box-Muller transform evaluated      bm
-      per Philox block evaluated              philox (a block feeds two pairs, NC-3)
-      per survivor pair bound-screened        screen
-      per normal used in a transformed pair   theta = fma + argmin step
-      per decision                            the serial contract work (lookup, charge, early
-                                              stop, Observe and posterior, totals, digest, curve
-                                              contributions) + a quarter replica Philox block +
-                                              this decision's share of the warp curve reduction
-    Transforms the bound screen proved unnecessary are not counted (counters [9..11])."""
-    wm = json.load(open(os.path.join(ROOT, "tools", "work_model.json")))
+PIPES = ("fp64", "alu", "fma", "total")
+# lanes per clock per SM of each pipe (B200: 4 SMSPs; DESIGN.md §8 derives them from the guides and
+# tools/peaks.cu): the FP64 unit, the alu pipe (LOP3/IADD3/SHF/SEL/ISETP), the fma pipe (IMAD*),
+# and issue (one warp-instruction per SMSP per clock)
+PIPE_LANES = {"fp64": 64, "alu": 64, "fma": 64, "total": ISSUE_LANES_PER_CLK_SM}
+
+
+def _work_model():
+    return json.load(open(os.path.join(ROOT, "tools", "work_model.json")))
+
+
+def method_work(counters):
+    """the algorithmic lane-instructions of the METHOD's events, by pipe.  Alg. 1
+    samples every survivor, so every survivor pair is one Box-Muller transform
+    (counter [2]), every quad with a survivor one Philox block ([8]), every normal used one
+    θ = fma + argmin step ([3]); every decision ([0]) does the serial contract work (lookup,
+    charge, early stop, Observe + posterior, totals, digest, curve contributions), a quarter of
+    a replica Philox block and its share of the warp curve reduction.  Costs per primitive:
+    sm_100a SASS of the contract functions (tools/work_model.json).  The counters are the
+    oracle-checked event counts, so W does not depend on what the kernel skipped."""
+    wm = _work_model()
+    c = [int(x) for x in counters]
+    dec, pairs, normals, blocks = c[0], c[2], c[3], c[8]
+    return {k: pairs * wm["bm"][k] + blocks * wm["philox"][k] + normals * wm["theta"][k]
+            + dec * (wm["serial"][k] + wm["philox"][k] / 4.0 + wm["curves"][k]) for k in PIPES}
+
+
+def evaluated_work(counters):
+    """The work this kernel evaluated: only the Box-Muller transforms the bound screen could not
+    rule out ([9]), the Philox blocks drawn ([10]) and the pairs screened ([11])."""
+    wm = _work_model()
     c = [int(x) for x in counters]
     dec, pairs, normals = c[0], c[2], c[3]
     bm_done, blocks_done, screened = c[9], c[10], c[11]
     used = normals * bm_done / max(1, pairs)
-    per_dec = {k: wm["serial"][k] + wm["philox"][k] / 4.0 + wm["curves"][k] for k in ("fp64", "total")}
     return {k: bm_done * wm["bm"][k] + blocks_done * wm["philox"][k] + screened * wm["screen"][k]
-            + used * wm["theta"][k] + dec * per_dec[k] for k in ("fp64", "total")}
+            + used * wm["theta"][k] + dec * (wm["serial"][k] + wm["philox"][k] / 4.0 + wm["curves"][k])
+            for k in PIPES}
+
+
+def roofline_of(counters, launch_s, clock_hz, dram_bytes, single):
+    """t_bound = max over {FP64 unit, alu pipe, fma pipe, issue, HBM} of work / peak (SURVEY
+    §8(d)); frac = t_bound / t_measured.  `achieved` / `peak` are those of the binding resource."""
+    W = method_work(counters)
+    E = evaluated_work(counters)
+    peaks = {k: PIPE_LANES[k] * SM_COUNT * clock_hz for k in PIPES}
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9 \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6.65e12
+    t_pipe = {k: W[k] / peaks[k] for k in PIPES}
+    t_hbm = (dram_bytes or 0.0) / hbm
+    bind = max(t_pipe, key=t_pipe.get)
+    dec = max(1, int(counters[0]))
+    name = {"total": "issue", "alu": "alu pipe", "fma": "fma pipe", "fp64": "FP64 unit"}
+    return {"bound": "alu", "binding": name[bind],
+            "achieved": W[bind] / launch_s / 1e12, "peak": peaks[bind] / 1e12, "unit": "T lane-inst/s",
+            "frac": t_pipe[bind] / launch_s, "traffic": None,
+            "kernel": "replay (phase A + regroup + phase B kernels)" if single else "whole step",
+            "launch_ms": launch_s * 1e3,
+            "method_work_per_decision": {k: W[k] / dec for k in PIPES},
+            "pipes": {name[k]: {"achieved": W[k] / launch_s / 1e12, "peak": peaks[k] / 1e12,
+                                "frac": t_pipe[k] / launch_s} for k in PIPES},
+            "hbm": {"bytes": dram_bytes, "t_bound_ms": 1e3 * t_hbm},
+            "evaluated": {"work_per_decision": E["total"] / dec,
+                          "achieved": E["total"] / launch_s / 1e12,
+                          "frac_of_issue": E["total"] / launch_s / peaks["total"]},
+            "peak_basis": f"lanes/clk/SM: FP64 64, alu 64, fma 64, issue {ISSUE_LANES_PER_CLK_SM} "
+                          f"(tools/peaks.cu, DESIGN.md §8) x {SM_COUNT} SMs x median SM clock under "
+                          f"load {clock_hz / 1e6:.0f} MHz"}
 
 
 # ------------------------------------------------------------------ reference arm (oracle)
@@ -236,13 +287,16 @@ def main():
     from paper_2208_06102_b200 import build
     from paper_2208_06102_b200.zeus_sim import Simulation
 
-    build.build()
+    if local == 0:                                   # one builder per node; the others wait
+        build.build()
+    if dist:
+        dist.barrier()
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     jobs = synth.config(args.config, trials=args.trials)
     job = jobs[0]
-    sims, streams, curves = [], [], []
+    sims, streams, curves, fixed = [], [], [], []
     for jb in jobs:                                  # one handle and one stream per job
         total, begin, end = shard_range(jb.trials, world, rank, args.scaling)
         sm = Simulation(jb.workload, jb.cells, total, jb.recurrences, shard=(begin, end),
@@ -250,6 +304,7 @@ def main():
         sims.append(sm)
         streams.append(torch.cuda.Stream(device=dev))
         curves.append(torch.zeros((sm.ncells, sm.R, 7), dtype=torch.float64, device=dev))
+        fixed.append(torch.zeros((sm.ncells, sm.R, 7, 3), dtype=torch.int64, device=dev))
     main = torch.cuda.Stream(device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     launches = []
@@ -262,10 +317,12 @@ def main():
         for sm, st, cv in zip(sims, streams, curves):
             st.wait_event(start)
             sm.run(st)
-        for sm, st, cv in zip(sims, streams, curves):
+        for sm, st, cv, fx in zip(sims, streams, curves, fixed):
             with torch.cuda.stream(st):
-                r = sm.results(want=["counters"], out={"curves": cv})
-                reduce_curves(cv)
+                r = sm.results(want=["counters"], out={"curves": cv, "curves_fixed": fx})
+                if dist:                             # a8: exact all-reduce, then one rounding
+                    reduce_curves(fx)
+                    sm.curves_from_fixed(fx, cv)
             outs.append(r)
             main.wait_stream(st)
         launches.append(sum(r["kernel_launches"] for r in outs))
@@ -330,41 +387,48 @@ def main():
         for sm, st, (A_h, Th_h, pool_h, host_out) in zip(sims, streams, staged):
             Z.zeus_sim_load_profile(sm.h, A_h, Th_h, pool_h.shape[0], pool_h.shape[2], pool_h)
             sm.run(st)
-        for sm, (A_h, Th_h, pool_h, host_out) in zip(sims, staged):
-            sm.results(want=[], out=host_out)
+        for sm, fx, cv, (A_h, Th_h, pool_h, host_out) in zip(sims, fixed, curves, staged):
             if dist:
-                cur_h = torch.from_numpy(host_out["curves"])
-                cur_h.copy_(reduce_curves(cur_h.to(dev)).cpu())
+                sm.results(want=[], out=dict(host_out, curves=None, curves_fixed=fx))
+                reduce_curves(fx)
+                sm.curves_from_fixed(fx, cv)
+                torch.from_numpy(host_out["curves"]).copy_(cv.cpu())
+            else:
+                sm.results(want=[], out=host_out)
     torch.cuda.synchronize()
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = dec_per_step * e2e_steps / float(e2e_s[0])
 
-    # ---- roofline of the dominant kernel group (the replay): algorithmic lane-instructions /
-    # its CUDA-event duration on the launching stream (whole step for multi-job configs)
-    work = work_per_launch(counters, None)
+    # ---- roofline of the dominant kernel group (the replay): the method's work
+    # over the replay's CUDA-event duration on its launching stream (whole step for multi-job
+    # configs); traffic from the committed ncu capture of this build (profiles/replay_traffic.json)
     launch_s = replay_total / args.steps / 1e3
     clock_hz = (clocks["sm_mhz"] or 1965.0) * 1e6
-    peak_issue = ISSUE_LANES_PER_CLK_SM * SM_COUNT * clock_hz
-    peak_fp64 = FP64_LANES_PER_CLK_SM * SM_COUNT * clock_hz
-    ach_issue, ach_fp64 = work["total"] / launch_s, work["fp64"] / launch_s
+    roofline = roofline_of(counters, launch_s, clock_hz, None, single)
     prof = os.path.join(ROOT, "profiles", "replay_traffic.json")
-    traffic = None
-    if os.path.exists(prof):
+    if os.path.exists(prof) and args.config == "cfg5":
         tr = json.load(open(prof))
-        traffic = tr["dram_bytes_per_decision"] * dec_per_step / world
-    roofline = {"bound": "alu", "achieved": ach_issue / 1e12, "peak": peak_issue / 1e12,
-                "unit": "T lane-inst/s", "frac": ach_issue / peak_issue, "traffic": traffic,
-                "kernel": "replay (phase A + regroup + phase B kernels)" if single else "whole step",
-                "launch_ms": launch_s * 1e3,
-                "work_per_decision": work["total"] / max(1, int(counters[0])),
-                "peak_basis": f"issue: {ISSUE_LANES_PER_CLK_SM} lanes/clk/SM x {SM_COUNT} SMs x "
-                              f"median SM clock under load {clock_hz / 1e6:.0f} MHz",
-                "fp64": {"achieved": ach_fp64 / 1e12, "peak": peak_fp64 / 1e12,
-                         "frac": ach_fp64 / peak_fp64,
-                         "peak_basis": f"{FP64_LANES_PER_CLK_SM} FP64 lanes/clk/SM (measured "
-                                       "1.82e13 DFMA lane/s at 1965 MHz, tools/peaks.cu)"}}
+        roofline["traffic"] = tr["dram_bytes_per_decision"] * dec_per_step / world
+        roofline["traffic_source"] = tr.get("source")
+        roofline["hbm"] = {"bytes": roofline["traffic"],
+                           "t_bound_ms": 1e3 * roofline["traffic"] / (json.load(open(os.path.join(
+                               ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9)
+                           if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else None}
+    if os.path.exists(os.path.join(ROOT, "profiles", "replay_executed.json")) and args.config == "cfg5":
+        ex = json.load(open(os.path.join(ROOT, "profiles", "replay_executed.json")))
+        roofline["executed"] = ex
+
+    if args.dump:                                    # per-rank outputs for the parity tests
+        os.makedirs(args.dump, exist_ok=True)
+        for i, (jb, sm) in enumerate(zip(jobs, sims)):
+            total, begin, end = shard_range(jb.trials, world, rank, args.scaling)
+            o = sm.results(want=["digest", "tot_cost", "n_stop", "final_arm"])
+            np.savez(os.path.join(args.dump, f"rank{rank}_job{i}.npz"), begin=begin, end=end,
+                     total=total, digest=o["digest"], tot_cost=o["tot_cost"], n_stop=o["n_stop"],
+                     final_arm=o["final_arm"], curves=curves[i].cpu().numpy(),
+                     curves_fixed=fixed[i].cpu().numpy())
 
     line = None
     if rank == 0:

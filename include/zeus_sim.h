@@ -24,8 +24,17 @@
  *  - Ownership: input arrays are read (and copied) before the call returns;
  *    the handle owns all device memory until zeus_sim_destroy; results are
  *    written only into caller-owned buffers.
- *  - Async: zeus_sim_run enqueues work on the caller's CUDA stream and
- *    returns; zeus_sim_results synchronises that stream first.
+ *  - Async, stream-ordered: every handle has a STREAM -- the cudaStream_t of its
+ *    last zeus_sim_run, or an internal non-blocking stream before the first run.
+ *    zeus_sim_load_profile enqueues its copies on it (after any run still in
+ *    flight there) and returns; zeus_sim_run enqueues on the caller's stream,
+ *    first making it wait for the last load, and that stream becomes the
+ *    handle's; zeus_sim_results enqueues its copies on the handle's stream and
+ *    synchronises that stream only.  No call launches work on the legacy
+ *    default stream unless the caller passes it, and no call synchronises the
+ *    device (zeus_sim_destroy and reallocations excepted: cudaFree does).
+ *    A stream passed to zeus_sim_run must stay valid until the handle has run
+ *    on another stream or is destroyed.
  *  - Threading: a handle belongs to one thread at a time; distinct handles
  *    may run concurrently on different streams or devices.
  *  - Sharding: RNG counters use the GLOBAL trial index (NC-3), so per-trial
@@ -147,8 +156,15 @@ typedef struct {
      q = 0 cost, 1 energy (J), 2 time (s), 3 pseudo-regret Ebar(b_t)c1(b_t) - opt
      (Eq. 9 with Epochs read as the trace mean, R-Q12), 4 early stops, 5 decisions
      equal to the known optimum, 6 decisions taken by Thompson sampling.
-     Counts are exact in fp64 (< 2^53), so the array can be all-reduced as is. */
+     Each value is the EXACT sum of the per-trial values quantised to 2^-F (F =
+     curve_scale_bits, chosen from an upper bound of one run's cost so that
+     |v 2^F| < 2^60), rounded once to fp64: the same bits whatever the trial
+     order, launch layout or sharding.  Counts are exact. */
   double *curves;
+  /* the same sums before rounding, [cells][R][7][3] int64 limbs: value = (l0 + l1 2^26 +
+     l2 2^52) 2^-F (counts: l0).  Integer sums, so ranks all-reduce THESE (exactly) and
+     convert with zeus_sim_curves_from_fixed to get world-size-invariant curves. */
+  int64_t *curves_fixed;
   /* per trial [cells][shard] */
   double *tot_cost, *tot_energy, *tot_time;   /* summed in recurrence order (NC-8) */
   uint64_t *digest;                           /* FNV-1a-64 over (b_t, p_t, flags) (NC-9) */
@@ -180,6 +196,7 @@ typedef struct {
      step 1 (Eq. 7) kernel, replay kernel, curve-reduction kernel */
   float step1_ms, replay_ms, reduce_ms;
   int32_t kernel_launches;           /* kernels the last zeus_sim_run launched */
+  int32_t curve_scale_bits;          /* F of curves_fixed (set by every successful call) */
 } zeus_results;
 
 /* Validates job, cells and opts (every violated invariant is reported),
@@ -193,8 +210,16 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
  *   epochs_to_target host [S][B][K] (S slices, K replicas); <= 0 = the run never
  *                   reaches the target (R-Q16); every value <= max_epochs;
  *                   every slice needs one converged replica on some arm.
- * Copies them to the device and computes step 1 for every cell (Eq. 7 argmin,
- * per-epoch and profiling constants, known optimum).  Synchronous. */
+ * The arrays are copied into a pinned staging buffer before the call returns
+ * (the caller may reuse them at once), then to the device asynchronously on the
+ * handle's stream, after any run still in flight there.  Same-shaped reloads
+ * (same S and K) reuse every device buffer, so a captured CUDA graph stays
+ * valid; a new shape first waits for the handle's stream, then reallocates.
+ * Step 1 (Eq. 7 argmin, per-epoch and profiling constants, known optimum) is
+ * computed by the next zeus_sim_run, or by zeus_sim_results when it asks for
+ * the step-1 tables before any run; the Pareto masks only when asked for.
+ * On any failure the handle is left unloaded (zeus_sim_run then fails with
+ * ZEUS_E_STATE) until a load succeeds. */
 zeus_status zeus_sim_load_profile(zeus_sim *sim, const double *avg_power_w,
                                   const double *throughput_eps, int32_t num_slices,
                                   int32_t replicas, const int32_t *epochs_to_target);
@@ -204,8 +229,16 @@ zeus_status zeus_sim_load_profile(zeus_sim *sim, const double *avg_power_w,
  * (cell, shard trial) for R recurrences, and the curve reduction. */
 zeus_status zeus_sim_run(zeus_sim *sim, void *cuda_stream);
 
-/* Synchronises the run's stream and copies the requested outputs. */
+/* Validates the request (ZEUS_E_STATE for replay outputs before any run, or a
+ * log without log_mode; nothing is copied then), enqueues the copies on the
+ * handle's stream, synchronises that stream, and returns. */
 zeus_status zeus_sim_results(zeus_sim *sim, zeus_results *out);
+
+/* curves [cells][R][7] (device) from fixed-point sums curves_fixed [cells][R][7][3] (device),
+ * e.g. after an all-reduce (SUM) of every rank's curves_fixed: carries the limbs and rounds
+ * once, exactly as zeus_sim_results does, so N ranks get the bits of one.  Runs on the
+ * handle's stream and synchronises it.  ZEUS_E_INVALID for NULL or host pointers. */
+zeus_status zeus_sim_curves_from_fixed(zeus_sim *sim, const int64_t *curves_fixed, double *curves);
 
 /* Frees the handle and its device memory; NULL is a no-op. */
 void zeus_sim_destroy(zeus_sim *sim);

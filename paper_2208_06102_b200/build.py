@@ -31,11 +31,13 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     srcs = sources()
     if not force and os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(f) for f in srcs):
         return out
-    cmd = [NVCC, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-o", out,
-           os.path.join(HERE, "csrc", "zeus_sim.cu"), "-lcudart"]
+    tmp = f"{out}.tmp{os.getpid()}"                 # written aside, then renamed into place, so a
+    cmd = [NVCC, *FLAGS, *extra, *[f"-D{d}" for d in defines], "-o", tmp,   # concurrent loader
+           os.path.join(HERE, "csrc", "zeus_sim.cu"), "-lcudart"]          # never sees half a file
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+    os.replace(tmp, out)
     with open(out + ".ptxas.log", "w") as f:
         f.write(r.stderr)
     if verbose:

@@ -141,7 +141,8 @@ struct ReplayArgs {
   const double *regret;           // [cells][reg_stride]
   const int32_t *opt_arm;         // [cells][opt_stride]
   const int32_t *pool;            // [S][B][K], allocation padded to 16 B
-  double *curve_slots;            // [cells][nslot][R][kQ]
+  long long *curve_slots;         // [cells][nslot][R][kQ][kLimbs] fixed point (curve_accumulate)
+  double curve_scale;             // 2^F of the fixed point
   double *tot_cost, *tot_energy, *tot_time;
   unsigned long long *digest;
   int32_t *n_stop, *final_arm;
@@ -158,6 +159,12 @@ struct ReplayArgs {
   // stage, <= 2B recurrences), phase B the Thompson-sampling rest with trials
   // regrouped so the lanes of a warp draw the same number of normal pairs
   int t_split;
+  // Counted curves (no ablation): a run that is not early-stopped is fully determined by its
+  // class (Thompson decision?, paid the profiling epoch?), b and replica at recurrence t, so its
+  // curve values are counted, not summed: hist[cell][R][nhslot][4][B][K] (u32), folded into the
+  // exact fixed-point sums by curve_hist_fold_kernel after the replay
+  uint32_t *hist;
+  int nhslot;
   struct Carry *carry;            // [stride] per-trial scalar state between phases
   int32_t *perm;                  // [stride] phase-B lane -> trial (within each cell's block)
   int32_t *bucket;                // [cells][nwin][kBuckets] histogram, then running offsets
@@ -230,30 +237,47 @@ __device__ __forceinline__ int warp_sum(int v) {
   return v;
 }
 
-// Warp partial of the curves at recurrence t: a reduce-scatter leaves the warp total of
-// fp64 quantity (lane >> 3) in lanes 0, 8, 16, 24 (12 shuffles instead of 40, one REDUX for the packed counts), then one
-// 4-lane atomic for the sums and one 3-lane atomic for the counts (packed 8 bits each:
-// stops | optimal << 8 | Thompson << 16).  All 32 lanes must call it.
-__device__ __forceinline__ void curve_accumulate(double *curves, int t, int lane, double vC,
-                                                 double vE, double vT, double vReg, int vPacked) {
-  const bool h = lane & 16, g = lane & 8;
-  double k0 = h ? vT : vC, k1 = h ? vReg : vE;
-  k0 += __shfl_xor_sync(0xffffffffu, h ? vC : vT, 16);
-  k1 += __shfl_xor_sync(0xffffffffu, h ? vE : vReg, 16);
-  double kq = g ? k1 : k0;
-  kq += __shfl_xor_sync(0xffffffffu, g ? k0 : k1, 8);
-  kq += __shfl_xor_sync(0xffffffffu, kq, 4);
-  kq += __shfl_xor_sync(0xffffffffu, kq, 2);
-  kq += __shfl_xor_sync(0xffffffffu, kq, 1);
-  vPacked = (int)__reduce_add_sync(0xffffffffu, (unsigned)vPacked);   // REDUX
-  double *row = curves + (size_t)t * kQ;
-  // predicated reductions, no branch: lanes 0/8/16/24 add the sums, lanes 0/8/16 the counts
-  const int cntq = (vPacked >> (lane & 24)) & 0xff;       // lane 0: stops, 8: optimal, 16: TS
-  const int p0 = (lane & 7) == 0, p1 = p0 && lane < 24 && cntq;
-  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p red.global.add.f64 [%0], %1;\n}"
-               :: "l"(row + (lane >> 3)), "d"(kq), "r"(p0) : "memory");
-  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p red.global.add.f64 [%0], %1;\n}"
-               :: "l"(row + 4 + (lane >> 3)), "d"((double)cntq), "r"(p1) : "memory");
+// Curves in exact fixed point (bitwise the same whatever the world size, the
+// layout or the order of the atomics).  A trial's value v of quantity q at recurrence t becomes
+// the integer Q = RN(v 2^F) (|Q| < 2^61; F is chosen on the host from an upper bound of v, so
+// the quantisation is < 2^-F absolute), split into limbs Q = l0 + l1 2^26 + l2 2^52 with
+// 0 <= l0, l1 < 2^26.  Every limb is summed over the warp by one REDUX (32 lanes x 2^26 < 2^31,
+// exact) and added to a 64-bit slot counter by one red.global.add.u64 (exact); integer sums do
+// not depend on order, so neither do the curves.  curve_reduce_kernel adds the slots, carries
+// the limbs and rounds once to fp64.  Counts (stops | optimal << 8 | Thompson << 16, packed
+// 8 bits each) are summed by one REDUX and added to limb 0.  All 32 lanes must call it.
+constexpr int kLimbs = 3, kLimbBits = 26;
+constexpr int kRow = kQ * kLimbs;   // int64 per (slot, recurrence)
+__device__ __forceinline__ void red_add_u64(long long *p, unsigned long long v, bool pred) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p red.global.add.u64 [%0], %1;\n}"
+               :: "l"(p), "l"(v), "r"((int)pred) : "memory");
+}
+__device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
+  asm volatile("red.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void curve_accumulate(long long *curves, int t, int lane, double vC,
+                                                 double vE, double vT, double vReg, int vPacked,
+                                                 double scale) {
+  long long *row = curves + (size_t)t * kRow;
+  const bool l0 = lane == 0;
+  const double v[4] = {vC, vE, vT, vReg};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const long long Q = __double2ll_rn(v[q] * scale);
+    const unsigned a0 = (unsigned)Q & 0x3ffffffu;
+    const unsigned a1 = (unsigned)(Q >> kLimbBits) & 0x3ffffffu;
+    const int a2 = (int)(Q >> (2 * kLimbBits));
+    const unsigned s0 = __reduce_add_sync(0xffffffffu, a0);
+    const unsigned s1 = __reduce_add_sync(0xffffffffu, a1);
+    const int s2 = __reduce_add_sync(0xffffffffu, a2);
+    red_add_u64(row + q * kLimbs, s0, l0 && s0);
+    red_add_u64(row + q * kLimbs + 1, s1, l0 && s1);
+    red_add_u64(row + q * kLimbs + 2, (unsigned long long)(long long)s2, l0 && s2);
+  }
+  const unsigned pk = __reduce_add_sync(0xffffffffu, (unsigned)vPacked);   // REDUX
+  red_add_u64(row + 4 * kLimbs, pk & 0xffu, l0 && (pk & 0xffu));
+  red_add_u64(row + 5 * kLimbs, (pk >> 8) & 0xffu, l0 && ((pk >> 8) & 0xffu));
+  red_add_u64(row + 6 * kLimbs, (pk >> 16) & 0xffu, l0 && ((pk >> 16) & 0xffu));
 }
 
 // 1-D bulk copy global -> shared through the TMA unit, completion on an mbarrier.
@@ -410,7 +434,10 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const size_t o = (size_t)(cp.out_off + jj);              // this trial's row in the outputs/state
   ArmStat *st = a.st + o * B;
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
-  double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
+  long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
+  constexpr bool kHist = !ABL;                              // counted curves (see ReplayArgs::hist)
+  const int HB = 4 * B * K;                                 // bins per (cell, t, slot)
+  uint32_t *hist = a.hist + ((size_t)cell * R * a.nhslot + (warp_global % a.nhslot)) * (size_t)HB;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
 
   uint32_t profiled = 0, seen = 0, mature = 0;              // bit a: profiled / observed / n_a >= 2
@@ -461,6 +488,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     int b = 0;
     bool was_seen = false;
     double y_old = 0.0;                                     // windowed: the cost leaving the window
+    int hkey = -1;                                          // (b, replica) of a counted run
     double C = 0.0;
     if (S > 1)                                              // no 64-bit division per decision
       while ((long long)(s + 1) * R <= (long long)t * S) ++s;
@@ -653,6 +681,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       double c0, t0, e0;
       const bool prof_now = !(ZS_SLIM_B && PHASE == 2 && !ABL && !WINDOWED) && !no_jit && a.charge_profiling &&
                             !((profiled >> b) & 1u);
+      if (kHist) hkey = ((ts_dec ? 2 : 0) + (prof_now ? 1 : 0)) * B * K + b * K + (int)r;
       if (prof_now) { c0 = ac.cP; t0 = ac.tP; e0 = ac.eP; } else { c0 = c1b; t0 = t1b; e0 = e1b; }
       profiled |= 1u << b;
       const double em1 = (double)(Erun - 1);
@@ -729,7 +758,17 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       vPacked = (stopped ? 1 : 0) | ((b == optarm[s] && p == ac.pstar) ? (1 << 8) : 0) |
                 (ts_dec ? (1 << 16) : 0);
     }
-    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked);
+    if constexpr (kHist) {
+      // a run that is not stopped is counted in its (b, replica) bin (one predicated RED); the
+      // rare stopped runs (charged the continuous threshold) take the fixed-point sums
+      const bool special = active && (vPacked & 1);
+      if (active && !special) red_add_u32(hist + (size_t)t * a.nhslot * HB + hkey, 1u);
+      if (__any_sync(0xffffffffu, special))
+        curve_accumulate(curves, t, tid & 31, special ? vC : 0.0, special ? vE : 0.0, special ? vT : 0.0,
+                         special ? vReg : 0.0, special ? vPacked : 0, a.curve_scale);
+    } else {
+      curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked, a.curve_scale);
+    }
     if (active) {
       // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
       {
@@ -871,7 +910,9 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
   const size_t o = (size_t)(cp.out_off + (active ? jj : 0));
   ArmStat *st = a.st + o * B;
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
-  double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
+  long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
+  const int HB = 4 * B * K;                                 // counted curves (ReplayArgs::hist)
+  uint32_t *hist = a.hist + ((size_t)cell * R * a.nhslot + (warp_global % a.nhslot)) * (size_t)HB;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
 
   uint32_t profiled = 0, seen = 0, mature = 0;
@@ -952,6 +993,7 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
     }
     if (sampled) b = bb;
     __syncwarp();                                            // the draw's reads before lane 0's stores
+    int hkey = -1;
     bool was_seen = false;
     ArmStat q;
     double C = 0.0;
@@ -965,6 +1007,7 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
       double c0, t0, e0;
       const bool prof_now = a.charge_profiling && !((profiled >> b) & 1u);
       if (prof_now) { c0 = ac.cP; t0 = ac.tP; e0 = ac.eP; } else { c0 = ac.c1; t0 = ac.t1; e0 = ac.e1; }
+      hkey = ((ts_dec ? 2 : 0) + (prof_now ? 1 : 0)) * B * K + b * K + (int)r;
       profiled |= 1u << b;
       const double em1 = (double)(Erun - 1);
       const double Cf = c0 + em1 * ac.c1;
@@ -1037,7 +1080,14 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
         vPacked = (stopped ? 1 : 0) | ((b == optarm[s]) ? (1 << 8) : 0) | (ts_dec ? (1 << 16) : 0);
       }
     }
-    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked);
+    {                                                        // counted curves (ReplayArgs::hist)
+      const bool counted = active && leader && !(vPacked & 1);
+      const bool special = active && leader && (vPacked & 1);
+      if (counted) red_add_u32(hist + (size_t)t * a.nhslot * HB + hkey, 1u);
+      if (__any_sync(0xffffffffu, special))
+        curve_accumulate(curves, t, tid & 31, special ? vC : 0.0, special ? vE : 0.0, special ? vT : 0.0,
+                         special ? vReg : 0.0, special ? vPacked : 0, a.curve_scale);
+    }
     if (active) {                                            // Alg. 2 Observe (NC-6)
       const int cnt = was_seen ? q.cnt : 0;
       double sh, S1, S2;
@@ -1151,7 +1201,8 @@ struct ConcArgs {
   const int32_t *pool;            // [S][B][K]
   const double2 *logtab;
   const double *arrivals;         // [cells][R] (cells with conc = 1)
-  double *curve_slots;
+  long long *curve_slots;         // [cells][nslot][R][kQ][kLimbs] fixed point (curve_accumulate)
+  double curve_scale;             // 2^F of the fixed point
   double *tot_cost, *tot_energy, *tot_time;
   unsigned long long *digest;
   int32_t *n_stop, *final_arm;
@@ -1188,7 +1239,7 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
   const size_t o = (size_t)(cp.out_off + jj);
   ArmStat *st = a.st + o * B;
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
-  double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
+  long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
 
   uint32_t profiled = 0, seen = 0, mature = 0;
@@ -1410,7 +1461,7 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
       vReg = __ldg(regret + (size_t)s * B + b);
       vPacked = (stopped ? 1 : 0) | ((b == __ldg(optarm + s)) ? (1 << 8) : 0) | (ts_dec ? (1 << 16) : 0);
     }
-    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked);
+    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked, a.curve_scale);
   }
   if (active) {
     a.tot_cost[o] = totC;
@@ -1466,7 +1517,7 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
   const size_t o = (size_t)(cp.out_off + jj);
   ArmStat *st = a.st + o * B;
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
-  double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
+  long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const bool no_prune = cp.ablation & 1, no_jit = cp.ablation & 2, retry = cp.ablation & 4;
   const bool epoch_stop = cp.ablation & 8, win_best = cp.ablation & 16;
@@ -1719,15 +1770,15 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
       }
       if (win_best) bring[t % NB] = conv_t;
     }
-    // sums by the warp reduce-scatter; the counts (up to one per attempt) by REDUX each
-    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, 0);
+    // sums in fixed point by REDUX; the counts (up to one per attempt) by REDUX each
+    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, 0, a.curve_scale);
     const unsigned k4 = __reduce_add_sync(0xffffffffu, cStop), k5 = __reduce_add_sync(0xffffffffu, cOpt),
                    k6 = __reduce_add_sync(0xffffffffu, cTs);
-    if ((tid & 31) == 0) {
-      double *row = curves + (size_t)t * kQ;
-      if (k4) atomicAdd(row + 4, (double)k4);
-      if (k5) atomicAdd(row + 5, (double)k5);
-      if (k6) atomicAdd(row + 6, (double)k6);
+    if ((tid & 31) == 0) {                  // counts live in limb 0 of their quantity
+      long long *row = curves + (size_t)t * kRow;
+      if (k4) atomicAdd(reinterpret_cast<unsigned long long *>(row + 4 * kLimbs), (unsigned long long)k4);
+      if (k5) atomicAdd(reinterpret_cast<unsigned long long *>(row + 5 * kLimbs), (unsigned long long)k5);
+      if (k6) atomicAdd(reinterpret_cast<unsigned long long *>(row + 6 * kLimbs), (unsigned long long)k6);
     }
   }
   if (active) {
@@ -1764,7 +1815,8 @@ struct BaselineArgs {
   const double *ebar;             // [S][B]
   const double *opt;              // [cells][S]
   const int32_t *opt_arm;         // [cells][opt_stride]
-  double *curve_slots;            // [cells][nslot][R][kQ]
+  long long *curve_slots;         // [cells][nslot][R][kQ][kLimbs] fixed point (curve_accumulate)
+  double curve_scale;             // 2^F of the fixed point
   double *tot_cost, *tot_energy, *tot_time;
   unsigned long long *digest;
   int32_t *n_stop, *final_arm;
@@ -1787,7 +1839,7 @@ __global__ void __launch_bounds__(128) baseline_kernel(BaselineArgs a) {
   const size_t o = (size_t)(cp.out_off + jj);
   const int B = a.B, P = a.P, S = a.S, K = a.K, R = a.R;
   const int warp_global = blockIdx.x * (blockDim.x >> 5) + (tid >> 5);
-  double *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kQ;
+  long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
   const ArmConst *arms = a.arms + (size_t)cell * B;
   bool exploring = cp.policy == 2;
   U4 rw{0u, 0u, 0u, 0u};
@@ -1838,7 +1890,7 @@ __global__ void __launch_bounds__(128) baseline_kernel(BaselineArgs a) {
       vReg = __ldg(a.ebar + (size_t)s * B + b) * c - __ldg(a.opt + (size_t)cell * S + s);
       vPacked = (b == __ldg(a.opt_arm + (size_t)cell * a.opt_stride + s) && p == arms[b].pstar) ? (1 << 8) : 0;
     }
-    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked);
+    curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked, a.curve_scale);
   }
   if (active) {
     a.tot_cost[o] = totC;
@@ -1887,17 +1939,88 @@ __global__ void pareto_kernel(const double *A, const double *Th, const double *e
   }
 }
 
-// curves[cell][t][q] = sum over slots in slot order
-__global__ void curve_reduce_kernel(const double *slots, double *curves, int ncells, int nslot,
-                                    int R) {
+// The exact curve sums: fixed[cell][t][q][limb] = the slots' integer sums (any order), then
+// carried into 26-bit limbs and rounded once to fp64: curves = RN(l2 2^52 + (l1 2^26 + l0)) 2^-F.
+__device__ __forceinline__ double fixed_to_double(long long l0, long long l1, long long l2,
+                                                  double inv_scale) {
+  l1 += l0 >> kLimbBits;                    // arithmetic shifts: floor, so the low limbs end in
+  l0 &= (1ll << kLimbBits) - 1;             // [0, 2^26) and the sign lives in l2
+  l2 += l1 >> kLimbBits;
+  l1 &= (1ll << kLimbBits) - 1;
+  const double lo = (double)(l1 * (1ll << kLimbBits) + l0);    // < 2^52: exact
+  return ((double)l2 * 0x1p52 + lo) * inv_scale;               // |l2| < 2^53: one rounding
+}
+
+// The counted runs (ReplayArgs::hist) into the fixed-point sums.  One thread per (cell, t, bin);
+// bin = (class, b, replica r), class = 2 ts + prof.  The n runs of a bin were each charged what
+// the replay computes for a run that is not stopped -- C = c0 + (E_run - 1) c1 with c0 = c_prof
+// when it paid the profiling epoch and c1 otherwise (NC-5), the same for T and energy, the
+// pseudo-regret of b -- so n RN(v 2^F) is added to slot 0 as an exact integer (three limbs, by
+// 64-bit integer atomics), and n to the optimal (b = opt arm) and Thompson counts.  Runs after
+// the replay kernels; the sums are then exactly those of run-by-run accumulation.
+__global__ void curve_hist_fold_kernel(const uint32_t *hist, long long *slots, const ArmConst *arms,
+                                       const double *regret, const int32_t *opt_arm,
+                                       const int32_t *pool, int ncells, int nslot, int nhslot, int R,
+                                       int B, int S, int K, int max_epochs, int reg_stride,
+                                       int opt_stride, double scale) {
+  const int HB = 4 * B * K;
+  const long long total = (long long)ncells * R * HB;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int bin = (int)(i % HB);
+    const long long ct = i / HB;                             // cell * R + t
+    const int cell = (int)(ct / R), t = (int)(ct % R);
+    long long n = 0;
+    for (int k = 0; k < nhslot; ++k) n += hist[((size_t)ct * nhslot + k) * HB + bin];
+    if (n == 0) continue;
+    const int cls = bin / (B * K), b = (bin / K) % B, r = bin % K;
+    const int s = (int)(((long long)t * S) / R);
+    const ArmConst ac = arms[(size_t)cell * B + b];
+    const bool prof = cls & 1;
+    const double c0 = prof ? ac.cP : ac.c1, t0 = prof ? ac.tP : ac.t1, e0 = prof ? ac.eP : ac.e1;
+    const int E = pool[((size_t)s * B + b) * K + r];
+    const int Erun = E > 0 ? E : max_epochs;
+    const double em1 = (double)(Erun - 1);
+    const double v[4] = {c0 + em1 * ac.c1, e0 + em1 * ac.e1, t0 + em1 * ac.t1,
+                         regret[(size_t)cell * reg_stride + (size_t)s * B + b]};
+    unsigned long long *row = reinterpret_cast<unsigned long long *>(slots + ((size_t)cell * nslot * R + t) * kRow);
+    for (int q = 0; q < 4; ++q) {
+      const __int128 T = (__int128)n * (__int128)__double2ll_rn(v[q] * scale);
+      atomicAdd(row + q * kLimbs + 0, (unsigned long long)(long long)(T & ((1 << kLimbBits) - 1)));
+      atomicAdd(row + q * kLimbs + 1, (unsigned long long)(long long)((T >> kLimbBits) & ((1 << kLimbBits) - 1)));
+      atomicAdd(row + q * kLimbs + 2, (unsigned long long)(long long)(T >> (2 * kLimbBits)));
+    }
+    if (b == opt_arm[(size_t)cell * opt_stride + s]) atomicAdd(row + 5 * kLimbs, (unsigned long long)n);
+    if (cls & 2) atomicAdd(row + 6 * kLimbs, (unsigned long long)n);
+  }
+}
+
+__global__ void curve_reduce_kernel(const long long *slots, long long *fixed, double *curves,
+                                    int ncells, int nslot, int R, double inv_scale) {
   const long long total = (long long)ncells * R * kQ;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     const long long cell = i / ((long long)R * kQ);
     const long long rq = i % ((long long)R * kQ);
-    double s = 0.0;
-    for (int k = 0; k < nslot; ++k) s += slots[((size_t)cell * nslot + k) * (size_t)R * kQ + rq];
-    curves[i] = s;
+    long long l[kLimbs] = {0, 0, 0};
+    for (int k = 0; k < nslot; ++k)
+#pragma unroll
+      for (int m = 0; m < kLimbs; ++m)
+        l[m] += slots[((size_t)cell * nslot + k) * (size_t)R * kRow + rq * kLimbs + m];
+#pragma unroll
+    for (int m = 0; m < kLimbs; ++m) fixed[i * kLimbs + m] = l[m];
+    const bool count = rq % kQ >= 4;       // counts are plain integers in limb 0
+    curves[i] = count ? (double)l[0] : fixed_to_double(l[0], l[1], l[2], inv_scale);
+  }
+}
+
+// curves from (all-reduced) fixed-point sums [n][kQ][kLimbs] -- the same rounding as above
+__global__ void curves_from_fixed_kernel(const long long *fixed, double *curves, long long n,
+                                         double inv_scale) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n * kQ;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long *l = fixed + i * kLimbs;
+    curves[i] = (i % kQ >= 4) ? (double)l[0] : fixed_to_double(l[0], l[1], l[2], inv_scale);
   }
 }
 

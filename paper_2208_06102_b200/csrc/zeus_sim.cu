@@ -73,16 +73,33 @@ struct zeus_sim {
     graph = nullptr;
   }
   int nslot = 1, tpb = 128, smem_bytes = 0, tab_bytes = 0, launches = 0, nwin = 1, group_w = 0;
-  cudaStream_t stream = nullptr;
+  // The handle's stream: where load_profile and results enqueue their work -- the stream of the
+  // last zeus_sim_run, or `own` (an internal non-blocking stream) before the first run.  No call
+  // launches on the legacy stream or synchronises the device (include/zeus_sim.h, "Async").
+  cudaStream_t stream = nullptr, own = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  cudaEvent_t ev_loaded = nullptr;   // the last load's copies, on the stream they were enqueued on
+  cudaEvent_t ev_staged = nullptr;   // the pinned staging buffer is free again
+  bool staged_pending = false;
+  void *h_stage = nullptr;           // pinned host copy of the traces (the caller's arrays are read
+  size_t h_stage_bytes = 0;          // before load_profile returns; the DMA reads this copy)
+  bool tables_valid = false;         // step-1 tables of the loaded traces are on the device
+  bool pareto_valid = false;         // the Pareto masks of the loaded traces are on the device
   std::string err;
   // device memory
   DevBuf d_A, d_Th, d_pool, d_cells, d_arms, d_regret, d_opt, d_optarm;
-  DevBuf d_slots, d_curves, d_tot_cost, d_tot_energy, d_tot_time, d_digest, d_nstop, d_final,
+  int curve_bits = 0;                // F of the curves' fixed point (curve_accumulate)
+  DevBuf d_hist;                     // counted runs per (cell, t, slot, class, b, replica)
+  int nhslot = 1;
+  DevBuf d_slots, d_fixed, d_curves, d_tot_cost, d_tot_energy, d_tot_time, d_digest, d_nstop, d_final,
       d_log, d_counters, d_st, d_st_ring, d_carry, d_perm, d_bucket, d_ebar, d_logtab, d_pareto,
       d_arrivals, d_best_ring;
   ~zeus_sim() {
     drop_graph();
+    if (own) { cudaStreamSynchronize(own); cudaStreamDestroy(own); }
+    if (h_stage) cudaFreeHost(h_stage);
+    if (ev_loaded) cudaEventDestroy(ev_loaded);
+    if (ev_staged) cudaEventDestroy(ev_staged);
     if (cap_stream) cudaStreamDestroy(cap_stream);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -365,14 +382,15 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
   s->shard_total = off;
   s->nwin = (int)std::max<int64_t>(1, (s->max_shard + zs::kRegroupWindow - 1) / zs::kRegroupWindow);
   // curve slots: spread the per-warp atomics over up to 64 copies, bounded to 64 MB
-  const size_t curve_bytes = (size_t)num_cells * s->R * zs::kQ * sizeof(double);
+  const size_t curve_bytes = (size_t)num_cells * s->R * zs::kRow * sizeof(long long);
   s->nslot = (int)std::max<size_t>(1, std::min<size_t>(64, (64ull << 20) / std::max<size_t>(1, curve_bytes)));
 
   const size_t n = (size_t)s->shard_total;
   cudaError_t e = cudaSuccess;
   if ((e = s->d_cells.alloc(sizeof(zs::CellParam) * num_cells)) != cudaSuccess ||
       (e = s->d_slots.alloc(curve_bytes * s->nslot)) != cudaSuccess ||
-      (e = s->d_curves.alloc(curve_bytes)) != cudaSuccess ||
+      (e = s->d_fixed.alloc(curve_bytes)) != cudaSuccess ||
+      (e = s->d_curves.alloc((size_t)num_cells * s->R * zs::kQ * sizeof(double))) != cudaSuccess ||
       (e = s->d_tot_cost.alloc(n * 8)) != cudaSuccess ||
       (e = s->d_tot_energy.alloc(n * 8)) != cudaSuccess ||
       (e = s->d_tot_time.alloc(n * 8)) != cudaSuccess ||
@@ -392,10 +410,13 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     delete s;
     return fail(nullptr, e == cudaErrorMemoryAllocation ? ZEUS_E_NOMEM : ZEUS_E_CUDA, m);
   }
-  if ((e = cudaMemcpy(s->d_cells.p, s->cpar.data(), sizeof(zs::CellParam) * num_cells,
-                      cudaMemcpyHostToDevice)) != cudaSuccess ||
+  if ((e = cudaStreamCreateWithFlags(&s->own, cudaStreamNonBlocking)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(s->d_cells.p, s->cpar.data(), sizeof(zs::CellParam) * num_cells,
+                           cudaMemcpyHostToDevice, s->own)) != cudaSuccess ||
       (e = cudaEventCreate(&s->ev0)) != cudaSuccess || (e = cudaEventCreate(&s->ev1)) != cudaSuccess ||
-      (e = cudaEventCreate(&s->ev2)) != cudaSuccess || (e = cudaEventCreate(&s->ev3)) != cudaSuccess) {
+      (e = cudaEventCreate(&s->ev2)) != cudaSuccess || (e = cudaEventCreate(&s->ev3)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&s->ev_loaded, cudaEventDisableTiming)) != cudaSuccess ||
+      (e = cudaEventCreateWithFlags(&s->ev_staged, cudaEventDisableTiming)) != cudaSuccess) {
     std::string m = std::string("create: ") + cudaGetErrorString(e);
     delete s;
     return fail(nullptr, ZEUS_E_CUDA, m);
@@ -405,18 +426,22 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     for (int i = 0; i < num_cells; ++i)
       if (cells[i].arrivals) std::memcpy(&arr[(size_t)i * s->R], cells[i].arrivals, (size_t)s->R * 8);
     if ((e = s->d_arrivals.alloc(arr.size() * 8)) != cudaSuccess ||
-        (e = cudaMemcpy(s->d_arrivals.p, arr.data(), arr.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        (e = cudaMemcpyAsync(s->d_arrivals.p, arr.data(), arr.size() * 8, cudaMemcpyHostToDevice,
+                             s->own)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s->own)) != cudaSuccess) {
       std::string m = std::string("arrivals: ") + cudaGetErrorString(e);
       delete s;
       return fail(nullptr, ZEUS_E_CUDA, m);
     }
   }
-  zs::log_table_kernel<<<1, 128>>>(s->d_logtab.as<double2>());   // the sampler's log table
-  if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaDeviceSynchronize()) != cudaSuccess) {
+  zs::log_table_kernel<<<1, 128, 0, s->own>>>(s->d_logtab.as<double2>());   // the sampler's log table
+  // the handle's own stream only (never the device): the pageable copies above read `cpar`
+  if ((e = cudaGetLastError()) != cudaSuccess || (e = cudaStreamSynchronize(s->own)) != cudaSuccess) {
     std::string m = std::string("log table: ") + cudaGetErrorString(e);
     delete s;
     return fail(nullptr, ZEUS_E_CUDA, m);
   }
+  s->stream = s->own;
   *out = s;
   return ZEUS_OK;
 }
@@ -461,32 +486,82 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   }
   if (E.code != ZEUS_OK) return fail(s, E.code, E.s);
   ZS_CUDA(s, cudaSetDevice(s->device));
-  s->S = S;
-  s->K = K;
-  s->reg_stride = (int)align_up((size_t)S * B, 2);
-  s->opt_stride = (int)align_up((size_t)S, 4);
+  // From here the handle is in flux: it is "loaded" again only when every buffer, copy and launch
+  // shape below is consistent (a failure midway leaves it unloaded, so zeus_sim_run refuses it).
+  s->loaded = false;
+  s->tables_valid = false;
+  s->pareto_valid = false;
+  cudaStream_t st = s->stream;
   const int nc = (int)s->cells.size();
-  ZS_CUDA(s, s->d_A.alloc((size_t)B * P * 8));
-  ZS_CUDA(s, s->d_Th.alloc((size_t)B * P * 8));
-  ZS_CUDA(s, s->d_pool.alloc(align_up((size_t)S * B * K * 4, 16)));
-  ZS_CUDA(s, s->d_arms.alloc((size_t)nc * B * sizeof(zs::ArmConst)));
-  ZS_CUDA(s, s->d_regret.alloc((size_t)nc * s->reg_stride * 8));
-  ZS_CUDA(s, s->d_opt.alloc((size_t)nc * S * 8));
-  ZS_CUDA(s, s->d_optarm.alloc((size_t)nc * s->opt_stride * 4));
-  ZS_CUDA(s, s->d_ebar.alloc((size_t)S * B * 8));
-  ZS_CUDA(s, cudaMemset(s->d_pool.p, 0, s->d_pool.bytes));
-  ZS_CUDA(s, cudaMemset(s->d_regret.p, 0, s->d_regret.bytes));
-  ZS_CUDA(s, cudaMemset(s->d_optarm.p, 0, s->d_optarm.bytes));
-  ZS_CUDA(s, cudaMemcpy(s->d_A.p, A, (size_t)B * P * 8, cudaMemcpyHostToDevice));
-  ZS_CUDA(s, cudaMemcpy(s->d_Th.p, Th, (size_t)B * P * 8, cudaMemcpyHostToDevice));
-  ZS_CUDA(s, cudaMemcpy(s->d_pool.p, pool, (size_t)S * B * K * 4, cudaMemcpyHostToDevice));
-  launch_step1(s, nullptr);
-  ZS_CUDA(s, cudaGetLastError());
-  ZS_CUDA(s, s->d_pareto.alloc((size_t)S * B * P));
-  zs::pareto_kernel<<<S, 256>>>(s->d_A.as<double>(), s->d_Th.as<double>(), s->d_ebar.as<double>(),
-                                s->d_pool.as<int32_t>(), s->d_pareto.as<uint8_t>(), B, P, K);
-  ZS_CUDA(s, cudaGetLastError());
-  ZS_CUDA(s, cudaDeviceSynchronize());
+  const size_t b_A = (size_t)B * P * 8, b_pool = (size_t)S * B * K * 4;
+  const int reg_stride = (int)align_up((size_t)S * B, 2), opt_stride = (int)align_up((size_t)S, 4);
+  const bool same_shape = s->d_A.p && s->S == S && s->K == K;
+  if (!same_shape) {
+    // reallocation frees buffers a run still in flight may read: wait for the handle's stream
+    // (cudaFree would otherwise synchronise the whole device)
+    ZS_CUDA(s, cudaStreamSynchronize(st));
+    s->drop_graph();
+    s->S = S;
+    s->K = K;
+    s->reg_stride = reg_stride;
+    s->opt_stride = opt_stride;
+    ZS_CUDA(s, s->d_A.alloc(b_A));
+    ZS_CUDA(s, s->d_Th.alloc(b_A));
+    ZS_CUDA(s, s->d_pool.alloc(align_up(b_pool, 16)));
+    ZS_CUDA(s, s->d_arms.alloc((size_t)nc * B * sizeof(zs::ArmConst)));
+    ZS_CUDA(s, s->d_regret.alloc((size_t)nc * s->reg_stride * 8));
+    ZS_CUDA(s, s->d_opt.alloc((size_t)nc * S * 8));
+    ZS_CUDA(s, s->d_optarm.alloc((size_t)nc * s->opt_stride * 4));
+    ZS_CUDA(s, s->d_ebar.alloc((size_t)S * B * 8));
+    ZS_CUDA(s, s->d_pareto.alloc((size_t)S * B * P));
+    // counted curves: [cells][R][nhslot][4][B][K] u32, up to 16 slot copies within 64 MB
+    const size_t per_slot = (size_t)nc * s->R * 4 * B * K * 4;
+    s->nhslot = (int)std::max<size_t>(1, std::min<size_t>(16, (64ull << 20) / std::max<size_t>(1, per_slot)));
+    ZS_CUDA(s, s->d_hist.alloc(per_slot * s->nhslot));
+  }
+  // Stage the caller's arrays in pinned memory (read before this call returns), then copy them
+  // to the device on the handle's stream: ordered after any run still in flight there, so that
+  // run finishes with the old tables.  The staging buffer is reused once its last copy is done.
+  const size_t stage = 2 * b_A + b_pool;
+  if (s->staged_pending) { ZS_CUDA(s, cudaEventSynchronize(s->ev_staged)); s->staged_pending = false; }
+  if (s->h_stage_bytes < stage) {
+    if (s->h_stage) ZS_CUDA(s, cudaFreeHost(s->h_stage));
+    s->h_stage = nullptr;
+    s->h_stage_bytes = 0;
+    ZS_CUDA(s, cudaMallocHost(&s->h_stage, stage));
+    s->h_stage_bytes = stage;
+  }
+  unsigned char *hs = static_cast<unsigned char *>(s->h_stage);
+  std::memcpy(hs, A, b_A);
+  std::memcpy(hs + b_A, Th, b_A);
+  std::memcpy(hs + 2 * b_A, pool, b_pool);
+  if (align_up(b_pool, 16) > b_pool)        // the bulk copies read the pool padded to 16 B
+    ZS_CUDA(s, cudaMemsetAsync(static_cast<unsigned char *>(s->d_pool.p) + b_pool, 0,
+                               align_up(b_pool, 16) - b_pool, st));
+  if (!same_shape) {
+    ZS_CUDA(s, cudaMemsetAsync(s->d_regret.p, 0, s->d_regret.bytes, st));
+    ZS_CUDA(s, cudaMemsetAsync(s->d_optarm.p, 0, s->d_optarm.bytes, st));
+  }
+  ZS_CUDA(s, cudaMemcpyAsync(s->d_A.p, hs, b_A, cudaMemcpyHostToDevice, st));
+  ZS_CUDA(s, cudaMemcpyAsync(s->d_Th.p, hs + b_A, b_A, cudaMemcpyHostToDevice, st));
+  ZS_CUDA(s, cudaMemcpyAsync(s->d_pool.p, hs + 2 * b_A, b_pool, cudaMemcpyHostToDevice, st));
+  ZS_CUDA(s, cudaEventRecord(s->ev_staged, st));
+  s->staged_pending = true;
+  {
+    // F of the curves' fixed point: every per-trial value of a recurrence (cost, energy, time,
+    // pseudo-regret) is at most mult * max_epochs * max_{b,p} max(MAXPOWER, 1) / Th(b,p) (A <=
+    // MAXPOWER, so cost and energy per epoch are below MAXPOWER / Th; mult = B when retries can
+    // charge several runs to one recurrence); with V < 2^e, F = 60 - e keeps |v 2^F| < 2^60.
+    double vmax = 0.0;
+    for (int i = 0; i < B * P; ++i) vmax = std::max(vmax, std::max(s->MP, 1.0) / Th[i]);
+    bool retry = false;
+    for (const auto &c : s->cells) retry |= (c.ablation & ZEUS_VARIANT_RETRY) != 0;
+    vmax *= (double)s->max_epochs * (retry ? B : 1);
+    int e = 0;
+    std::frexp(vmax, &e);                   // vmax < 2^e
+    s->curve_bits = std::max(-1000, std::min(1000, 60 - e));
+  }
+  ZS_CUDA(s, cudaEventRecord(s->ev_loaded, st));
 
   // launch shape of the replay: the block size (32/64/128 trials) that keeps the
   // most warps resident given the shared-memory footprint per trial
@@ -549,8 +624,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   ZS_CUDA(s, grant_max_smem((const void *)zs::variant_kernel<false>, s->device));
   ZS_CUDA(s, grant_max_smem((const void *)zs::variant_kernel<true>, s->device));
   // a captured run binds buffer addresses and launch shapes: keep it only if none changed
-  if (s->launch_signature() != sig0) s->drop_graph();
   s->loaded = true;
+  if (s->launch_signature() != sig0) s->drop_graph();
   return ZEUS_OK;
 }
 
@@ -563,6 +638,7 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
   };
   ZS_CUDA(s, cudaMemsetAsync(s->d_slots.p, 0, s->d_slots.bytes, st));
   ZS_CUDA(s, cudaMemsetAsync(s->d_counters.p, 0, s->d_counters.bytes, st));
+  if (s->any_zeus && !s->any_ablation) ZS_CUDA(s, cudaMemsetAsync(s->d_hist.p, 0, s->d_hist.bytes, st));
   ZS_CUDA(s, record(s->ev0));
   launch_step1(s, st);                        // a1: Eq. 7 argmin + per-arm constants
   ZS_CUDA(s, cudaGetLastError());
@@ -578,7 +654,8 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     b.ebar = s->d_ebar.as<double>();
     b.opt = s->d_opt.as<double>();
     b.opt_arm = s->d_optarm.as<int32_t>();
-    b.curve_slots = s->d_slots.as<double>();
+    b.curve_slots = s->d_slots.as<long long>();
+    b.curve_scale = std::ldexp(1.0, s->curve_bits);
     b.tot_cost = s->d_tot_cost.as<double>();
     b.tot_energy = s->d_tot_energy.as<double>();
     b.tot_time = s->d_tot_time.as<double>();
@@ -604,7 +681,8 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     c.pool = s->d_pool.as<int32_t>();
     c.logtab = s->d_logtab.as<double2>();
     c.arrivals = s->d_arrivals.as<double>();
-    c.curve_slots = s->d_slots.as<double>();
+    c.curve_slots = s->d_slots.as<long long>();
+    c.curve_scale = std::ldexp(1.0, s->curve_bits);
     c.tot_cost = s->d_tot_cost.as<double>();
     c.tot_energy = s->d_tot_energy.as<double>();
     c.tot_time = s->d_tot_time.as<double>();
@@ -649,7 +727,8 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     a.regret = s->d_regret.as<double>();
     a.opt_arm = s->d_optarm.as<int32_t>();
     a.pool = s->d_pool.as<int32_t>();
-    a.curve_slots = s->d_slots.as<double>();
+    a.curve_slots = s->d_slots.as<long long>();
+    a.curve_scale = std::ldexp(1.0, s->curve_bits);
     a.tot_cost = s->d_tot_cost.as<double>();
     a.tot_energy = s->d_tot_energy.as<double>();
     a.tot_time = s->d_tot_time.as<double>();
@@ -671,6 +750,8 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     // trials of each cell are regrouped by survivor-pair count so a warp's lanes
     // draw the same number of normals per decision in phase B
     a.t_split = std::min(s->R, 2 * s->B);
+    a.hist = s->d_hist.as<uint32_t>();
+    a.nhslot = s->nhslot;
     a.carry = s->d_carry.as<zs::Carry>();
     a.perm = s->d_perm.as<int32_t>();
     a.bucket = s->d_bucket.as<int32_t>();
@@ -713,6 +794,7 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     } else {
       s->launches += 4;
       ZS_CUDA(s, cudaMemsetAsync(s->d_bucket.p, 0, s->d_bucket.bytes, st));
+
       replay_launch(1);
       ZS_CUDA(s, cudaGetLastError());
       zs::bucket_scan_kernel<<<(unsigned)((nc * (int64_t)s->nwin + 127) / 128), 128, 0, st>>>(a.bucket, nc, s->nwin);
@@ -724,10 +806,20 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
       replay_launch(2);
       ZS_CUDA(s, cudaGetLastError());
     }
+    if (!s->any_ablation) {                    // the counted runs into the exact sums
+      const long long n = (long long)nc * s->R * 4 * s->B * s->K;
+      zs::curve_hist_fold_kernel<<<(unsigned)std::max<long long>(1, std::min<long long>(4 * 1184, (n + 127) / 128)),
+                                   128, 0, st>>>(
+          a.hist, a.curve_slots, a.arms, a.regret, a.opt_arm, a.pool, nc, s->nslot, s->nhslot, s->R, s->B,
+          s->S, s->K, s->max_epochs, s->reg_stride, s->opt_stride, a.curve_scale);
+      ZS_CUDA(s, cudaGetLastError());
+      s->launches += 1;
+    }
   }
   ZS_CUDA(s, record(s->ev1));
   zs::curve_reduce_kernel<<<std::max(1, std::min(1184, (int)((nc * (size_t)s->R * zs::kQ + 255) / 256))), 256, 0, st>>>(
-      s->d_slots.as<double>(), s->d_curves.as<double>(), nc, s->nslot, s->R);
+      s->d_slots.as<long long>(), s->d_fixed.as<long long>(), s->d_curves.as<double>(), nc, s->nslot,
+      s->R, std::ldexp(1.0, -s->curve_bits));
   ZS_CUDA(s, cudaGetLastError());
   ZS_CUDA(s, record(s->ev2));
   return ZEUS_OK;
@@ -739,6 +831,7 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
   if (!s->loaded) return fail(s, ZEUS_E_STATE, "zeus_sim_run before zeus_sim_load_profile");
   ZS_CUDA(s, cudaSetDevice(s->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (st != s->stream) ZS_CUDA(s, cudaStreamWaitEvent(st, s->ev_loaded, 0));   // the load's copies
   s->stream = st;
   if (!s->use_graph) {
     const zeus_status rc = enqueue_run(s, st, false);
@@ -760,6 +853,7 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
     s->launches = s->graph_launches;
   }
   s->ran = true;
+  s->tables_valid = true;                   // the run's step 1 wrote the tables
   return ZEUS_OK;
 }
 
@@ -769,28 +863,54 @@ zeus_status zeus_sim_results(zeus_sim *s, zeus_results *out) {
   if (!out) return fail(s, ZEUS_E_INVALID, "out is NULL");
   if (out->struct_size != sizeof(zeus_results)) return fail(s, ZEUS_E_INVALID, "zeus_results.struct_size mismatch (ABI)");
   if (!s->loaded) return fail(s, ZEUS_E_STATE, "zeus_sim_results before zeus_sim_load_profile");
+  // every request is validated before any copy is queued into a caller buffer
+  if (!s->ran && (out->curves || out->curves_fixed || out->tot_cost || out->tot_energy || out->tot_time || out->digest ||
+                  out->n_stop || out->final_arm || out->log || out->counters))
+    return fail(s, ZEUS_E_STATE, "replay outputs requested before zeus_sim_run");
+  if (out->log && !s->log_mode) return fail(s, ZEUS_E_STATE, "log requested but log_mode = 0");
   ZS_CUDA(s, cudaSetDevice(s->device));
   cudaStream_t st = s->stream;
+  const bool want_tables = out->pstar_index || out->c1 || out->t1 || out->e1 || out->c_prof ||
+                           out->t_prof || out->e_prof || out->opt_cost || out->opt_arm || out->pareto;
+  if (want_tables && !s->tables_valid) {    // step 1 of the loaded traces, before any run
+    launch_step1(s, st);
+    ZS_CUDA(s, cudaGetLastError());
+    s->tables_valid = true;
+  }
+  if (out->pareto && !s->pareto_valid) {    // f4, computed only when asked for
+    zs::pareto_kernel<<<s->S, 256, 0, st>>>(s->d_A.as<double>(), s->d_Th.as<double>(),
+                                           s->d_ebar.as<double>(), s->d_pool.as<int32_t>(),
+                                           s->d_pareto.as<uint8_t>(), s->B, s->P, s->K);
+    ZS_CUDA(s, cudaGetLastError());
+    s->pareto_valid = true;
+  }
   const int nc = (int)s->cells.size();
   const size_t n = (size_t)s->shard_total;
+  // host-built arrays into a caller buffer: a plain memcpy for host memory, else a copy on the
+  // handle's stream (a pageable source is staged before cudaMemcpyAsync returns)
+  auto put = [&](void *dst, const void *src, size_t bytes) -> cudaError_t {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, dst) == cudaSuccess && pa.type == cudaMemoryTypeDevice)
+      return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+    cudaGetLastError();                       // clear a "not a device pointer" from the query
+    std::memcpy(dst, src, bytes);
+    return cudaSuccess;
+  };
   auto cp = [&](void *dst, const DevBuf &src, size_t bytes) -> cudaError_t {
     if (!dst || bytes == 0) return cudaSuccess;
     return cudaMemcpyAsync(dst, src.p, bytes, cudaMemcpyDefault, st);   // host or device dst
   };
   if (s->ran) {
     ZS_CUDA(s, cp(out->curves, s->d_curves, (size_t)nc * s->R * zs::kQ * 8));
+    ZS_CUDA(s, cp(out->curves_fixed, s->d_fixed, (size_t)nc * s->R * zs::kRow * 8));
     ZS_CUDA(s, cp(out->tot_cost, s->d_tot_cost, n * 8));
     ZS_CUDA(s, cp(out->tot_energy, s->d_tot_energy, n * 8));
     ZS_CUDA(s, cp(out->tot_time, s->d_tot_time, n * 8));
     ZS_CUDA(s, cp(out->digest, s->d_digest, n * 8));
     ZS_CUDA(s, cp(out->n_stop, s->d_nstop, n * 4));
     ZS_CUDA(s, cp(out->final_arm, s->d_final, n * 4));
-    if (out->log && !s->log_mode) return fail(s, ZEUS_E_STATE, "log requested but log_mode = 0");
     ZS_CUDA(s, cp(out->log, s->d_log, n * (size_t)s->R * 4));
     ZS_CUDA(s, cp(out->counters, s->d_counters, zs::kCounters * 8));
-  } else if (out->curves || out->tot_cost || out->tot_energy || out->tot_time || out->digest ||
-             out->n_stop || out->final_arm || out->log || out->counters) {
-    return fail(s, ZEUS_E_STATE, "replay outputs requested before zeus_sim_run");
   }
   ZS_CUDA(s, cp(out->opt_cost, s->d_opt, (size_t)nc * s->S * 8));
   ZS_CUDA(s, cp(out->pareto, s->d_pareto, (size_t)s->S * s->B * s->P));
@@ -801,7 +921,7 @@ zeus_status zeus_sim_results(zeus_sim *s, zeus_results *out) {
     std::vector<int32_t> packed((size_t)nc * s->S);
     for (int c = 0; c < nc; ++c)
       std::memcpy(&packed[(size_t)c * s->S], &tmp[(size_t)c * s->opt_stride], (size_t)s->S * 4);
-    ZS_CUDA(s, cudaMemcpy(out->opt_arm, packed.data(), packed.size() * 4, cudaMemcpyDefault));
+    ZS_CUDA(s, put(out->opt_arm, packed.data(), packed.size() * 4));
   }
   const bool want_arms = out->pstar_index || out->c1 || out->t1 || out->e1 || out->c_prof ||
                          out->t_prof || out->e_prof;
@@ -819,9 +939,9 @@ zeus_status zeus_sim_results(zeus_sim *s, zeus_results *out) {
       f[3][i] = arms[i].cP; f[4][i] = arms[i].tP; f[5][i] = arms[i].eP;
     }
     double *dst[6] = {out->c1, out->t1, out->e1, out->c_prof, out->t_prof, out->e_prof};
-    if (out->pstar_index) ZS_CUDA(s, cudaMemcpy(out->pstar_index, ps.data(), ps.size() * 4, cudaMemcpyDefault));
+    if (out->pstar_index) ZS_CUDA(s, put(out->pstar_index, ps.data(), ps.size() * 4));
     for (int q = 0; q < 6; ++q)
-      if (dst[q]) ZS_CUDA(s, cudaMemcpy(dst[q], f[q].data(), f[q].size() * 8, cudaMemcpyDefault));
+      if (dst[q]) ZS_CUDA(s, put(dst[q], f[q].data(), f[q].size() * 8));
   }
   ZS_CUDA(s, cudaStreamSynchronize(st));
   out->replay_ms = 0.f;
@@ -833,6 +953,27 @@ zeus_status zeus_sim_results(zeus_sim *s, zeus_results *out) {
     ZS_CUDA(s, cudaEventElapsedTime(&out->reduce_ms, s->ev1, s->ev2));
   }
   out->kernel_launches = s->ran ? s->launches : 0;
+  out->curve_scale_bits = s->curve_bits;
+  return ZEUS_OK;
+}
+
+zeus_status zeus_sim_curves_from_fixed(zeus_sim *s, const int64_t *curves_fixed, double *curves) {
+  if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
+  s->err.clear();
+  if (!curves_fixed || !curves) return fail(s, ZEUS_E_INVALID, "curves_fixed / curves is NULL");
+  if (!s->loaded) return fail(s, ZEUS_E_STATE, "zeus_sim_curves_from_fixed before zeus_sim_load_profile");
+  ZS_CUDA(s, cudaSetDevice(s->device));
+  cudaPointerAttributes pa{}, pb{};
+  const bool dev_in = cudaPointerGetAttributes(&pa, curves_fixed) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+  const bool dev_out = cudaPointerGetAttributes(&pb, curves) == cudaSuccess && pb.type == cudaMemoryTypeDevice;
+  cudaGetLastError();
+  if (!dev_in || !dev_out) return fail(s, ZEUS_E_INVALID, "curves_fixed and curves must be device memory");
+  const long long rows = (long long)s->cells.size() * s->R;
+  zs::curves_from_fixed_kernel<<<std::max(1, (int)std::min<long long>(1184, (rows * zs::kQ + 255) / 256)), 256, 0,
+                                 s->stream>>>(reinterpret_cast<const long long *>(curves_fixed), curves, rows,
+                                              std::ldexp(1.0, -s->curve_bits));
+  ZS_CUDA(s, cudaGetLastError());
+  ZS_CUDA(s, cudaStreamSynchronize(s->stream));
   return ZEUS_OK;
 }
 

@@ -2,7 +2,7 @@
 
 Trials are independent and RNG counters use the GLOBAL trial index (NC-3), so a
 rank only needs its [begin, end) range; the one collective is an all-reduce
-(SUM) of the [cells][R][7] curves tensor (NCCL on GPUs, gloo in CPU tests).
+(SUM) of the curves' exact fixed-point sums (NCCL on GPUs, gloo in CPU tests).
 """
 from __future__ import annotations
 
@@ -23,10 +23,13 @@ def shard_range(trials_per_gpu: int, world: int, rank: int, scaling: str = "weak
     raise ValueError(scaling)
 
 
-def reduce_curves(curves, group=None):
-    """Sums per-rank curves in place (counts travel as exact fp64 integers < 2^53)."""
+def reduce_curves(curves_fixed, group=None):
+    """All-reduce (SUM) of every rank's fixed-point curve sums, [cells][R][7][3] int64 limbs
+    (zeus_results.curves_fixed).  Integer addition is exact and associative, so the sum has the
+    same bits for any world size and any reduction order; the library then rounds it once to
+    fp64 curves (zeus_sim_curves_from_fixed), giving N ranks the bits of one."""
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(curves, op=dist.ReduceOp.SUM, group=group)
-    return curves
+        dist.all_reduce(curves_fixed, op=dist.ReduceOp.SUM, group=group)
+    return curves_fixed

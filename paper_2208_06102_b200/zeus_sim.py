@@ -24,7 +24,8 @@ STATUS = {0: "ZEUS_OK", 1: "ZEUS_E_INVALID", 2: "ZEUS_E_STATE", 3: "ZEUS_E_NO_CO
 CURVE_Q = 7
 COUNTERS = 12
 EXPORTS = ("zeus_sim_create", "zeus_sim_load_profile", "zeus_sim_run", "zeus_sim_results",
-           "zeus_sim_destroy", "zeus_sim_last_error", "zeus_sim_shape")
+           "zeus_sim_destroy", "zeus_sim_last_error", "zeus_sim_shape", "zeus_sim_curves_from_fixed")
+CURVE_LIMBS = 3
 
 
 class ZeusError(RuntimeError):
@@ -55,7 +56,8 @@ class zeus_run_opts(C.Structure):
 
 
 class zeus_results(C.Structure):
-    _fields_ = [("struct_size", C.c_uint32), ("curves", C.c_void_p), ("tot_cost", C.c_void_p),
+    _fields_ = [("struct_size", C.c_uint32), ("curves", C.c_void_p), ("curves_fixed", C.c_void_p),
+                ("tot_cost", C.c_void_p),
                 ("tot_energy", C.c_void_p), ("tot_time", C.c_void_p), ("digest", C.c_void_p),
                 ("n_stop", C.c_void_p), ("final_arm", C.c_void_p), ("pstar_index", C.c_void_p),
                 ("c1", C.c_void_p), ("t1", C.c_void_p), ("e1", C.c_void_p), ("c_prof", C.c_void_p),
@@ -63,7 +65,7 @@ class zeus_results(C.Structure):
                 ("opt_arm", C.c_void_p), ("pareto", C.c_void_p), ("log", C.c_void_p),
                 ("counters", C.c_void_p),
                 ("step1_ms", C.c_float), ("replay_ms", C.c_float), ("reduce_ms", C.c_float),
-                ("kernel_launches", C.c_int32)]
+                ("kernel_launches", C.c_int32), ("curve_scale_bits", C.c_int32)]
 
 
 _lib = None
@@ -87,8 +89,9 @@ def lib():
         L.zeus_sim_last_error.argtypes = [C.c_void_p]
         L.zeus_sim_last_error.restype = C.c_char_p
         L.zeus_sim_shape.argtypes = [C.c_void_p] + [C.c_void_p] * 5
+        L.zeus_sim_curves_from_fixed.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         for f in ("zeus_sim_create", "zeus_sim_load_profile", "zeus_sim_run", "zeus_sim_results",
-                  "zeus_sim_shape"):
+                  "zeus_sim_shape", "zeus_sim_curves_from_fixed"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -120,6 +123,10 @@ def zeus_sim_run(h, cuda_stream=None):
 def zeus_sim_results(h, res: zeus_results):
     _check(lib().zeus_sim_results(h, C.byref(res)), h)
     return res
+
+
+def zeus_sim_curves_from_fixed(h, curves_fixed, curves):
+    _check(lib().zeus_sim_curves_from_fixed(h, _ptr(curves_fixed), _ptr(curves)), h)
 
 
 def zeus_sim_destroy(h):
@@ -202,7 +209,8 @@ class Simulation:
         """Copies outputs into host numpy arrays (default) or into caller buffers given in
         ``out`` (numpy arrays or torch tensors, host or device)."""
         nc, R, n, B, S = self.ncells, self.R, self.shard_n, self.B, self.S
-        shapes = {"curves": ((nc, R, CURVE_Q), np.float64), "tot_cost": ((n,), np.float64),
+        shapes = {"curves": ((nc, R, CURVE_Q), np.float64),
+                  "curves_fixed": ((nc, R, CURVE_Q, CURVE_LIMBS), np.int64), "tot_cost": ((n,), np.float64),
                   "tot_energy": ((n,), np.float64), "tot_time": ((n,), np.float64),
                   "digest": ((n,), np.uint64), "n_stop": ((n,), np.int32),
                   "final_arm": ((n,), np.int32), "pstar_index": ((nc, B), np.int32),
@@ -226,7 +234,13 @@ class Simulation:
         bufs["replay_ms"] = res.replay_ms
         bufs["reduce_ms"] = res.reduce_ms
         bufs["kernel_launches"] = res.kernel_launches
+        bufs["curve_scale_bits"] = res.curve_scale_bits
         return bufs
+
+    def curves_from_fixed(self, curves_fixed, curves):
+        """Device tensors: curves [cells][R][7] from (all-reduced) curves_fixed [cells][R][7][3]."""
+        zeus_sim_curves_from_fixed(self.h, curves_fixed, curves)
+        return curves
 
     def close(self):
         zeus_sim_destroy(self.h)

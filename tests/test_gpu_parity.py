@@ -4,7 +4,9 @@ Bar (BASELINE.json north_star): every (batch size, power limit) decision and
 early-stop event bit-exact -- checked through the per-decision log (CFG1) and
 the FNV-1a digest of (b_t, p_t, flags) per trial (all configs) -- and per-trial
 totals bit-exact (NC-8: both sides sum in recurrence order); curves summed over
-trials within 1e-9 relative (NC-8: order of the cross-trial sum is free).
+trials within 1e-9 relative of the oracle's fp64 sums.  The GPU curves are exact
+fixed-point sums rounded once (include/zeus_sim.h curves_fixed), so between GPU runs
+-- any layout, shard split or world size -- they are compared bit for bit.
 """
 import math
 
@@ -35,7 +37,7 @@ def oracle_threads(oracle):
 
 def run_gpu(zs, w, cells, trials, R, shard=(0, -1), log=False, want=None, layout=0):
     sim = zs.Simulation(w, cells, trials, R, shard=shard, log=log, layout=layout).load_profile().run()
-    keys = ["curves", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm",
+    keys = ["curves", "curves_fixed", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm",
             "counters", "pstar_index", "c1", "t1", "e1", "c_prof", "t_prof", "e_prof", "opt_cost",
             "opt_arm"] + (["log"] if log else [])
     out = sim.results(want=want or keys)
@@ -217,7 +219,17 @@ def test_empty_shard_and_sharding_invariance(zs, oracle):
     parts = [run_gpu(zs, w, cells, 3000, R, shard=(b, e)) for b, e in ((0, 1111), (1111, 2048), (2048, 3000))]
     for k in ("tot_cost", "digest", "tot_time", "n_stop", "final_arm"):
         assert np.array_equal(full[k], np.concatenate([p[k] for p in parts]))
-    np.testing.assert_allclose(full["curves"], sum(p["curves"] for p in parts), rtol=1e-12)
+    # the curves' fixed-point sums add exactly; rounded once they are the full run's bits
+    assert np.array_equal(_fixed_value(full["curves_fixed"]),
+                          _fixed_value(sum(p["curves_fixed"] for p in parts)))
+    import torch
+
+    sim = zs.Simulation(w, cells, 3000, R).load_profile()
+    fx = torch.from_numpy(sum(p["curves_fixed"] for p in parts)).cuda()
+    cv = torch.zeros((len(cells), R, 7), dtype=torch.float64, device="cuda")
+    sim.curves_from_fixed(fx, cv)
+    sim.close()
+    assert np.array_equal(cv.cpu().numpy(), full["curves"])
     empty = run_gpu(zs, w, cells, 3000, R, shard=(5000, 6000))
     assert empty["n"] == 0 and np.all(empty["curves"] == 0)
 
@@ -267,7 +279,7 @@ def test_schedules_bit_identical(zs, oracle, name):
         for k in ("log", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm"):
             assert np.array_equal(outs[0][k], o[k]), k
         assert np.array_equal(outs[0]["counters"][:9], o["counters"][:9])
-        np.testing.assert_allclose(outs[0]["curves"], o["curves"], rtol=1e-12)
+        assert np.array_equal(outs[0]["curves"], o["curves"])          # exact sums: same bits
     # evaluated work: lane groups transform every survivor pair (each with its own Philox
     # block); the bound screen of the one-pass and Thompson-phase kernels
     # transforms at most as many, and far fewer once the posteriors separate
@@ -439,3 +451,94 @@ def test_random_traces_one_cell(zs, oracle, B, P, S, K, window, beta, trials, R,
     g = run_gpu(zs, w, [cell], trials, R, log=True, layout=layout)
     compare_step1(oracle, g, w, [cell])
     compare_cell(oracle, g, w, cell, 0, np.arange(trials), R, trials, logs=True)
+
+
+def test_reload_is_stream_ordered(zs, oracle):
+    """include/zeus_sim.h "Async": load_profile enqueues its copies on the handle's stream after
+    the run in flight there, so run(A) -> load_profile(B) -> results() returns A's replay, and the
+    next run (on another stream) replays B.  No call synchronises the device."""
+    import torch
+
+    (job,) = synth.config("cfg5", trials=20000)
+    wa = job.workload
+    wb = dict(wa)
+    wb["pool"] = np.ascontiguousarray(np.maximum(1, wa["pool"][:, ::-1, :]))   # another trace, same shape
+    R = 400
+    ref_a = run_gpu(zs, wa, job.cells, 20000, R)
+    ref_b = run_gpu(zs, wb, job.cells, 20000, R)
+    assert not np.array_equal(ref_a["digest"], ref_b["digest"])
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    sim = zs.Simulation(wa, job.cells, 20000, R).load_profile()
+    sim.run(s1)
+    sim.w = wb
+    sim.load_profile()                      # while the first run is still in flight on s1
+    ga = sim.results(want=["digest", "tot_cost", "curves"])
+    assert np.array_equal(ga["digest"], ref_a["digest"]) and np.array_equal(ga["curves"], ref_a["curves"])
+    sim.run(s2)
+    gb = sim.results(want=["digest", "tot_cost", "tot_energy", "tot_time", "n_stop", "final_arm",
+                           "curves", "c1"])
+    assert np.array_equal(gb["digest"], ref_b["digest"]) and np.array_equal(gb["curves"], ref_b["curves"])
+    sim.close()
+    compare_cell(oracle, gb, wb, job.cells[0], 0, np.arange(0, 20000, 97), R, 20000, full_curves=False)
+
+
+def test_results_validates_before_copying(zs):
+    """A failing results() call (log without log_mode; replay outputs before any run) returns
+    ZEUS_E_STATE without writing any caller buffer; step-1 tables and the Pareto masks are
+    available before the first run (computed on request)."""
+    (job,) = synth.config("cfg1")
+    sim = zs.Simulation(job.workload, job.cells, job.trials, job.recurrences).load_profile()
+    sentinel = np.full((1, sim.R, 7), 7.0)
+    with pytest.raises(zs.ZeusError, match="ZEUS_E_STATE"):
+        sim.results(want=[], out={"curves": sentinel})
+    assert np.all(sentinel == 7.0)
+    t = sim.results(want=["c1", "pareto", "opt_cost"])
+    assert np.all(t["c1"] > 0) and t["pareto"].any()
+    sim.run()
+    log = np.full((sim.shard_n, sim.R), 5, np.uint32)
+    with pytest.raises(zs.ZeusError, match="log_mode"):
+        sim.results(want=[], out={"curves": sentinel, "log": log})
+    assert np.all(sentinel == 7.0) and np.all(log == 5)
+    sim.close()
+
+
+def test_two_ranks_through_bench_match_one(tmp_path):
+    """SURVEY §8(e) on one GPU: bench.py's real step under torchrun with 2 ranks sharing the GPU
+    over gloo (shard_range, zeus_sim_run, the fixed-point all-reduce, max-over-ranks timing) gives
+    per-trial digests and costs equal to one rank's, and curves with the same bits."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    common = ["--config", "cfg5", "--trials", "30000", "--steps", "1", "--warmup", "3",
+              "--scaling", "strong", "--no-cpu-baseline", "--e2e-steps", "1"]
+    env = dict(os.environ, ZEUS_DIST_BACKEND="gloo")
+    one = tmp_path / "one"
+    two = tmp_path / "two"
+    r1 = subprocess.run([sys.executable, "bench.py", *common, "--dump", str(one)], cwd=root, env=env,
+                        capture_output=True, text=True, timeout=900)
+    assert r1.returncode == 0, r1.stderr[-2000:]
+    r2 = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                         "--master-addr", "127.0.0.1", "--master-port", "29533", "bench.py", "--gpus", "2",
+                         *common, "--dump", str(two)], cwd=root, env=env, capture_output=True, text=True,
+                        timeout=900)
+    assert r2.returncode == 0, r2.stderr[-2000:]
+    line = [l for l in r2.stdout.splitlines() if l.startswith("{")][-1]
+    import json
+
+    assert json.loads(line)["n_gpus"] == 2
+    a = np.load(one / "rank0_job0.npz")
+    b0, b1 = np.load(two / "rank0_job0.npz"), np.load(two / "rank1_job0.npz")
+    assert int(b0["begin"]) == 0 and int(b0["end"]) == int(b1["begin"]) and int(b1["end"]) == 30000
+    for k in ("digest", "tot_cost", "n_stop", "final_arm"):
+        assert np.array_equal(a[k], np.concatenate([b0[k], b1[k]])), k
+    for b in (b0, b1):                      # every rank holds the all-reduced curves
+        assert np.array_equal(_fixed_value(b["curves_fixed"]), _fixed_value(a["curves_fixed"]))
+        assert np.array_equal(b["curves"], a["curves"])
+
+
+def _fixed_value(fx):
+    """The integers the limbs represent (limb sums are not canonical: carries differ)."""
+    return np.array([int(l0) + (int(l1) << 26) + (int(l2) << 52) for l0, l1, l2 in fx.reshape(-1, 3)],
+                    dtype=object)

@@ -40,33 +40,26 @@ __global__ void dmul_tput(double *out, double a) {
   if (s == 12345.0) out[0] = s;
 }
 
-__global__ void imadwide_tput(uint32_t *out, uint32_t m) {
-  uint32_t x[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
-  for (int it = 0; it < kIters; ++it) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = __umulhi(x[i], m) ^ (x[i] * m);
+// INT throughput: one PTX instruction per op, each a single SASS instruction (checked with
+// cuobjdump: 1024 LOP3 / IMAD / IMAD.HI per unrolled loop body and nothing else but the loop
+// counter), 8 independent chains per thread, operands in registers so nothing folds.  (A chain
+// of add.u32 is folded by ptxas into one IMAD, so the ALU pipe is measured with LOP3 only.)
+constexpr int kUnroll = 4;
+#define INT_TPUT(NAME, ASM)                                                                  \
+  __global__ void NAME(uint32_t *out, uint32_t a, uint32_t b) {                              \
+    uint32_t x[8];                                                                           \
+    _Pragma("unroll") for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 7 + i;                \
+    for (int it = 0; it < kIters / kUnroll; ++it) {                                          \
+      _Pragma("unroll") for (int u = 0; u < kUnroll; ++u)                                    \
+      _Pragma("unroll") for (int i = 0; i < 8; ++i) asm volatile(ASM : "+r"(x[i]) : "r"(a), "r"(b)); \
+    }                                                                                        \
+    uint32_t s = 0;                                                                          \
+    _Pragma("unroll") for (int i = 0; i < 8; ++i) s ^= x[i];                                 \
+    if (s == 12345u) out[0] = s;                                                             \
   }
-  uint32_t s = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) s ^= x[i];
-  if (s == 12345u) out[0] = s;
-}
-
-__global__ void lop3_tput(uint32_t *out, uint32_t a, uint32_t b) {
-  uint32_t x[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 7 + i;
-  for (int it = 0; it < kIters; ++it) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = (x[i] ^ a ^ (x[i] >> 3)) | b;   // folds to LOP3/SHF
-  }
-  uint32_t s = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) s ^= x[i];
-  if (s == 12345u) out[0] = s;
-}
+INT_TPUT(lop3_tput, "lop3.b32 %0, %0, %1, %2, 0x96;")          // LOP3.LUT (alu pipe)
+INT_TPUT(imad_tput, "mad.lo.u32 %0, %0, %1, %2;")               // IMAD (fma pipe)
+INT_TPUT(imadhi_tput, "mad.hi.u32 %0, %0, %1, %2;")             // IMAD.HI (fma pipe)
 
 __global__ void dfma_lat(double *out, long long *cyc, double a, double b) {
   double x = threadIdx.x;
@@ -126,8 +119,9 @@ int main() {
   const double ops = threads * kIters * 8;
   double ms_dfma = time_ms([&] { dfma_tput<<<blocks, tpb>>>(d, 0.999999, 1e-9); });
   double ms_dmul = time_ms([&] { dmul_tput<<<blocks, tpb>>>(d, 0.999999); });
-  double ms_imad = time_ms([&] { imadwide_tput<<<blocks, tpb>>>(u, 0xD2511F53u); });
   double ms_lop = time_ms([&] { lop3_tput<<<blocks, tpb>>>(u, 0x9E3779B9u, 0x10u); });
+  double ms_imad = time_ms([&] { imad_tput<<<blocks, tpb>>>(u, 0xD2511F53u, 0x10u); });
+  double ms_imadhi = time_ms([&] { imadhi_tput<<<blocks, tpb>>>(u, 0xD2511F53u, 0x10u); });
   CK(cudaGetLastError());
   long long h[3];
   dfma_lat<<<1, 1>>>(d, c, 0.999999, 1e-9);
@@ -137,11 +131,11 @@ int main() {
   imad_lat<<<1, 1>>>(u, c, 0xD2511F53u);
   CK(cudaMemcpy(&h[2], c, 8, cudaMemcpyDeviceToHost));
   printf("{\"device\": \"%s\", \"sms\": %d, \"clock_rate_mhz\": %.0f, "
-         "\"dfma_lane_per_s\": %.4e, \"dmul_lane_per_s\": %.4e, \"umulhi_mul_xor_per_s\": %.4e, "
-         "\"lop3_shf_per_s\": %.4e, \"dfma_latency_cyc\": %.2f, \"ddiv_latency_cyc\": %.1f, "
-         "\"imad_hi_xor_latency_cyc\": %.2f}\n",
+         "\"dfma_lane_per_s\": %.4e, \"dmul_lane_per_s\": %.4e, \"lop3_lane_per_s\": %.4e, "
+         "\"imad_lane_per_s\": %.4e, \"imad_hi_lane_per_s\": %.4e, "
+         "\"dfma_latency_cyc\": %.2f, \"ddiv_latency_cyc\": %.1f, \"imad_hi_xor_latency_cyc\": %.2f}\n",
          p.name, sms, clk_khz / 1e3, ops / (ms_dfma * 1e-3), ops / (ms_dmul * 1e-3),
-         ops / (ms_imad * 1e-3), ops / (ms_lop * 1e-3), (double)h[0] / kIters, (double)h[1] / 256,
-         (double)h[2] / kIters);
+         ops / (ms_lop * 1e-3), ops / (ms_imad * 1e-3),
+         ops / (ms_imadhi * 1e-3), (double)h[0] / kIters, (double)h[1] / 256, (double)h[2] / kIters);
   return 0;
 }

@@ -145,6 +145,16 @@ typedef struct {
                                           the caller's stream -- one launch instead of 5-10 for
                                           launch-bound configurations; same results.
                                           zeus_sim_load_profile discards the graph. */
+  int32_t draw;                      /* the Thompson draw of the two-phase schedule (Alg. 1
+                                        P:L455-463); same results for
+                                        every value:
+                                        0: certified fp32 -- every survivor's theta in fp32
+                                          with a proven error bound; the contract's fp64 draw
+                                          only when the bounds do not separate the argmin;
+                                        1: the exact fp64 draw with the bound screen;
+                                        2: certified fp32 with every decision sent to the fp64
+                                          fallback (a test of that path).
+                                        Cells with a window or an ablation always take 1. */
 } zeus_run_opts;
 
 /* Outputs.  Every pointer is caller-owned and may be NULL (skipped); each
@@ -184,13 +194,15 @@ typedef struct {
      arm | p_index << 8 | flags << 16, flags bit0 stopped, bit1 converged,
      bit2 paid the profiling epoch, bit3 decided by Thompson sampling */
   uint32_t *log;
-  /* instrumentation [12]: decisions, sampled TS decisions, normal pairs drawn,
+  /* instrumentation [14]: decisions, sampled TS decisions, normal pairs drawn,
      normals used, early stops, pruning decisions, forced explorations,
      posterior recomputations, Philox blocks drawn for normals (NC-3: two pairs each)
      -- [0..8] are events of the method, identical to the oracle's --
-     then the work this build evaluated for them: [9] Box-Muller transforms, [10] Philox
-     blocks, [11] pairs bound-screened (the bound screen skips the transform of pairs whose
-     arms provably cannot win: [9] <= [2]) */
+     then the work this build evaluated for them: [9] fp64 Box-Muller transforms, [10] Philox
+     blocks, [11] pairs bound-screened (exact-screen kernels: the screen skips the transform of
+     pairs whose arms provably cannot win: [9] <= [2]) plus pairs transformed
+     in fp32 (certified draw, §7.9), [12] draws decided by the certified fp32 bounds,
+     [13] draws sent to the exact fp64 fallback */
   int64_t *counters;
   /* timing of the last zeus_sim_run, CUDA events on the caller's stream:
      step 1 (Eq. 7) kernel, replay kernel, curve-reduction kernel */
@@ -250,6 +262,16 @@ const char *zeus_sim_last_error(const zeus_sim *sim);
 /* R actually used (after auto), shard size, number of cells; any out may be NULL. */
 zeus_status zeus_sim_shape(const zeus_sim *sim, int32_t *recurrences, int64_t *shard,
                            int32_t *num_cells, int32_t *num_batch_sizes, int32_t *num_slices);
+
+/* Exhaustive check of the two measured error bounds behind the certified fp32 draw
+ * (zeus_run_opts.draw = 0), on cuda_device, for every 32-bit word:
+ *   out[0] = max over radius words a of |r32 - r| / e_r(a)   (the bound holds iff <= 1),
+ *   out[1] = max r32                                          (must be <= out[5]),
+ *   out[2] = max over angle words b of |cos32 - cos|, out[3] of |sin32 - sin| (<= out[4]),
+ *   out[4] = the angle bound compiled into the kernels, out[5] = the radius cap,
+ * where r, cos, sin are the contract's fp64 values (NC-3).  out: host, 6 doubles.
+ * Returns ZEUS_OK, ZEUS_E_INVALID (out NULL) or ZEUS_E_CUDA.  About 0.1 s on a B200. */
+zeus_status zeus_sim_certify_bounds(int32_t cuda_device, double *out);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,8 @@
 namespace zs {
 
 constexpr int kQ = 7;             // curve quantities
-constexpr int kCounters = 12;   // 9 contract events + transforms, Philox blocks, pairs screened
+constexpr int kCounters = 14;   // 9 contract events + transforms, Philox blocks, pairs screened / in fp32,
+                                // draws certified in fp32, exact fallbacks (thompson_kernel)
 
 struct ArmConst {                 // per (cell, arm), 64 B
   double c1, t1, e1, cP, tP, eP;
@@ -177,6 +178,10 @@ struct ReplayArgs {
   // RK launches (one cell, grid.y = 1): the cell's Philox round keys, read by the rounds as
   // constant-bank operands instead of being recomputed as k + r W in every block
   RoundKeys rk;
+  // the Thompson phase runs thompson_kernel (certified fp32 draw): phase A
+  // then groups the lanes by survivor-quad count; force_exact sends every draw to its exact
+  // fp64 fallback (a test of that path)
+  int key_quads, force_exact;
 };
 
 constexpr int kBuckets = 34;      // 2 x popcount of the survivor-pair mask + parity of its lowest pair
@@ -194,7 +199,8 @@ __device__ __forceinline__ uint32_t quads_of(uint32_t pairs) {
 
 // phase-B grouping key: lanes with the same number of survivor pairs and the same parity of
 // the lowest one draw the same number of Philox blocks at the same loop steps
-__device__ __forceinline__ int regroup_key(uint32_t pairs) {
+__device__ __forceinline__ int regroup_key(uint32_t pairs, int key_quads) {
+  if (key_quads) return __popc(quads_of(pairs));          // thompson_kernel: quads per decision
   return pairs ? 2 * __popc(pairs) + ((__ffs(pairs) - 1) & 1) : 0;
 }
 
@@ -817,7 +823,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       c.nstop = nstop; c.last_b = last_b;
       c.n_sampled = n_sampled; c.n_prune = n_prune; c.n_forced = n_forced; c.n_recomp = n_recomp;
       a.carry[o] = c;
-      atomicAdd(&a.bucket[((size_t)cell * a.nwin + jj / kRegroupWindow) * kBuckets + regroup_key(ts_pairs)], 1);
+      atomicAdd(&a.bucket[((size_t)cell * a.nwin + jj / kRegroupWindow) * kBuckets + regroup_key(ts_pairs, a.key_quads)], 1);
     }
     return;
   }
@@ -1169,7 +1175,7 @@ __global__ void bucket_scan_kernel(int32_t *bucket, int ncells, int nwin) {
 
 // phase-B lane order: the trials of each window grouped by their survivor-pair count
 __global__ void bucket_scatter_kernel(const CellParam *cells, const Carry *carry, int32_t *bucket,
-                                      int32_t *perm, int ncells, int B, int nwin) {
+                                      int32_t *perm, int ncells, int B, int nwin, int key_quads) {
   const int cell = blockIdx.y;
   const CellParam cp = cells[cell];
   if (cp.policy != 0 || cp.conc) return;
@@ -1179,7 +1185,7 @@ __global__ void bucket_scatter_kernel(const CellParam *cells, const Carry *carry
     uint32_t pairs = 0;
     for (int k = 0; 2 * k < B; ++k)
       if ((ts_set >> (2 * k)) & 3u) pairs |= 1u << k;
-    const int pos = atomicAdd(&bucket[((size_t)cell * nwin + j / kRegroupWindow) * kBuckets + regroup_key(pairs)], 1);
+    const int pos = atomicAdd(&bucket[((size_t)cell * nwin + j / kRegroupWindow) * kBuckets + regroup_key(pairs, key_quads)], 1);
     perm[cp.out_off + pos] = (int32_t)j;
   }
 }

@@ -1,0 +1,370 @@
+// thompson.cuh -- the Thompson-sampling phase of the two-phase schedule
+// with the certified fp32 draw of certify.cuh.
+//
+// thompson_kernel<LOG, RK> runs recurrences t_split..R-1 of every trial of a launch whose
+// cells have no window and no ablation, after replay_kernel's phase A (Alg. 3 pruning) and the
+// regroup.  Per decision (Alg. 1, then steps 3-4 as in replay_kernel):
+//   * every survivor quad's Philox block (NC-3) is drawn; both of its Box-Muller pairs are
+//     transformed in fp32 and every arm's theta in fp32 with its error bound (certify.cuh);
+//   * when the smallest interval lies strictly below the others its arm is the contract's
+//     argmin; otherwise (rare) the exact fp64 draw of the contract decides, from the fp64
+//     posteriors recomputed from the Observe records;
+//   * the rest of the decision is the contract's fp64 arithmetic, unchanged.
+// Lanes were regrouped by their number of survivor quads, so the quad loop has the same trip
+// count in every lane of a warp.  (mu - ref, sigma) of every arm live in shared memory as fp32,
+// 8 B per arm (half of the fp64 pair the exact-screen kernel keeps).
+#pragma once
+#include "certify.cuh"
+#include "kernels.cuh"
+
+namespace zs {
+
+#ifndef ZS_PHILOX_PREFIX
+#define ZS_PHILOX_PREFIX 1
+#endif
+
+// Philox4x32-10 of counter (t, 1<<24 | q, lo32 trial, hi32 trial) for several q at one (trial,
+// t) (NC-3): the first three rounds share the products that do not depend on q.
+//   round 0: M0 t (per decision), M1 lo32(trial) (per trial)
+//   round 1: M1 z1 with z1 = hi(M0 t) ^ hi32(trial) ^ k1[0] (per decision)
+//   round 2: M0 x2 with x2 = hi(M1 z1) ^ lo(M1 lo32 trial) ^ k0[1] (per decision)
+struct PhiloxPrefix {
+  uint32_t x1b, w1, y2, h0, l0;
+};
+template <class K0, class K1>
+__device__ __forceinline__ PhiloxPrefix philox_prefix(uint32_t t, uint32_t tlo, uint32_t thi, K0 k0, K1 k1) {
+  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint32_t hi1 = __umulhi(M1, tlo), lo1 = M1 * tlo;
+  const uint32_t hi0 = __umulhi(M0, t), lo0 = M0 * t;
+  PhiloxPrefix p;
+  p.x1b = hi1 ^ 0x01000000u ^ k0(0);
+  const uint32_t z1 = hi0 ^ thi ^ k1(0);
+  p.w1 = lo0;
+  const uint32_t H1 = __umulhi(M1, z1), L1 = M1 * z1;
+  const uint32_t x2 = H1 ^ lo1 ^ k0(1);
+  p.y2 = L1;
+  p.h0 = __umulhi(M0, x2);
+  p.l0 = M0 * x2;
+  return p;
+}
+template <class K0, class K1>
+__device__ __forceinline__ U4 philox_from_prefix(const PhiloxPrefix &p, uint32_t q, K0 k0, K1 k1) {
+  constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+  const uint32_t x1 = p.x1b ^ q;                       // round 0 output x (y1 = lo(M1 tlo) is
+  const uint32_t H0 = __umulhi(M0, x1), L0 = M0 * x1;  // consumed by the prefix's x2)
+  const uint32_t z2 = H0 ^ p.w1 ^ k1(1);               // round 1 output (x2, y2 shared)
+  const uint32_t w2 = L0;
+  const uint32_t H1 = __umulhi(M1, z2), L1 = M1 * z2;
+  U4 c{H1 ^ p.y2 ^ k0(2), L1, p.h0 ^ w2 ^ k1(2), p.l0};   // round 2 output
+#pragma unroll
+  for (int r = 3; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    c = U4{hi1 ^ c.y ^ k0(r), lo1, hi0 ^ c.w ^ k1(r), lo0};
+  }
+  return c;
+}
+
+template <bool LOG, bool RK>
+__global__ void __launch_bounds__(128) thompson_kernel(ReplayArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t mbar;
+  const int cell = blockIdx.y;
+  const CellParam cp = a.cells[cell];
+  const int tid = threadIdx.x, TPB = blockDim.x;
+  const int64_t j0 = (int64_t)blockIdx.x * TPB;
+  if (j0 >= cp.n || cp.policy != 0 || cp.conc) return;
+  auto k0f = [&](int r) -> uint32_t {
+    if constexpr (RK) return a.rk.k0[r];
+    else return cp.key0 + (uint32_t)r * 0x9E3779B9u;
+  };
+  auto k1f = [&](int r) -> uint32_t {
+    if constexpr (RK) return a.rk.k1[r];
+    else return cp.key1 + (uint32_t)r * 0xBB67AE85u;
+  };
+  auto block_c = [&](int64_t tr, int tt, int q) -> U4 {
+    if constexpr (RK) return pair_block(a.rk, tr, tt, q);
+    else return pair_block(cp.key0, cp.key1, tr, tt, q);
+  };
+  auto replica_words_c = [&](int64_t tr, int tt) -> U4 {
+    if constexpr (RK) return replica_words(a.rk, tr, tt);
+    else return replica_words(cp.key0, cp.key1, tr, tt);
+  };
+
+  // ---- stage the cell's tables with TMA bulk copies (one elected thread)
+  const TabLayout L(a.B, a.S, a.K);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    const uint32_t p_arm = (a.B * (uint32_t)sizeof(ArmConst) + 15u) & ~15u;
+    const uint32_t p_reg = (a.S * a.B * 8u + 15u) & ~15u;
+    const uint32_t p_opt = (a.S * 4u + 15u) & ~15u;
+    const uint32_t p_pool = (a.S * a.B * a.K * 4u + 15u) & ~15u;
+    mbar_expect_tx(&mbar, p_arm + p_reg + p_opt + p_pool + kLogTab * 16u);
+    tma_bulk_load(smem + L.logtab, a.logtab, kLogTab * 16u, &mbar);
+    tma_bulk_load(smem + L.arms, a.arms + (size_t)cell * a.B, p_arm, &mbar);
+    tma_bulk_load(smem + L.regret, a.regret + (size_t)cell * a.reg_stride, p_reg, &mbar);
+    tma_bulk_load(smem + L.optarm, a.opt_arm + (size_t)cell * a.opt_stride, p_opt, &mbar);
+    tma_bulk_load(smem + L.pool, a.pool, p_pool, &mbar);
+  }
+  __syncthreads();
+  mbar_wait(&mbar, 0);
+
+  const ArmConst *arm = reinterpret_cast<const ArmConst *>(smem + L.arms);
+  const double *regret = reinterpret_cast<const double *>(smem + L.regret);
+  const int32_t *optarm = reinterpret_cast<const int32_t *>(smem + L.optarm);
+  const int32_t *pool = reinterpret_cast<const int32_t *>(smem + L.pool);
+  const double2 *logtab = reinterpret_cast<const double2 *>(smem + L.logtab);
+  const int B = a.B, R = a.R, S = a.S, K = a.K;
+  // fp32 (mu - ref, sigma) of arms 2k, 2k+1 of this thread: float4 [pair][thread]
+  float4 *s_f = reinterpret_cast<float4 *>(smem + a.tab_bytes);
+  float2 *s_f2 = reinterpret_cast<float2 *>(s_f);         // arm b: s_f2[2 ((b >> 1) TPB + tid) + (b & 1)]
+
+  const bool active = j0 + tid < cp.n;
+  const int64_t jj = active ? a.perm[cp.out_off + j0 + tid] : 0;
+  const int64_t trial = cp.begin + jj;
+  const size_t o = (size_t)(cp.out_off + jj);
+  ArmStat *st = a.st + o * B;
+  const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
+  long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
+  const int HB = 4 * B * K;
+  uint32_t *hist = a.hist + ((size_t)cell * R * a.nhslot + (warp_global % a.nhslot)) * (size_t)HB;
+  const double kInf = __longlong_as_double(0x7ff0000000000000ll);
+  const float kInfF = __int_as_float(0x7f800000);
+
+  double best = kInf, totC = 0.0, totE = 0.0, totT = 0.0;
+  unsigned long long dig = 0;
+  uint32_t ts_set = 0, ts_pairs = 0, quads = 0;
+  int nstop = 0, last_b = -1;
+  uint32_t n_sampled = 0, n_forced = 0, n_recomp = 0, n_cert = 0, n_fall = 0;
+  double ref = 0.0;
+  float c_trial = 0.0f;
+  const int npairs = (B + 1) >> 1;
+  if (active) {                                             // resume from phase A
+    const Carry c = a.carry[o];
+    best = c.best; totC = c.totC; totE = c.totE; totT = c.totT; dig = c.dig;
+    ts_set = c.ts_set;
+    nstop = c.nstop; last_b = c.last_b;
+    for (int k = 0; k < npairs; ++k)
+      if ((ts_set >> (2 * k)) & 3u) ts_pairs |= 1u << k;
+    quads = quads_of(ts_pairs);
+    // ref: the posterior mean of the leader (the last arm run, or the first survivor), so the
+    // fp32 (mu - ref) of the arms that compete with it are small
+    const int lead = (last_b >= 0 && ((ts_set >> last_b) & 1u)) ? last_b : __ffs(ts_set) - 1;
+    {
+      const ArmStat q = st[lead];
+      ref = posterior(q.sh, q.S1, q.S2, q.cnt, cp.prec0, cp.pm0).x;
+    }
+    if (!(fabs(ref) < 1e30)) ref = 0.0;
+    c_trial = __double2float_ru(fabs(ref) * 0x1p-52 + 0x1p-120);
+    for (int b = 0; b < 2 * npairs; ++b) {                  // every survivor was run (and observed
+      float2 v = make_float2(kInfF, 0.0f);                  // at least twice) in pruning
+      if ((ts_set >> b) & 1u) {
+        const ArmStat q = st[b];
+        const double2 ms = posterior(q.sh, q.S1, q.S2, q.cnt, cp.prec0, cp.pm0);
+        const double dm = ms.x - ref;
+        v = (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y) : make_float2(0.0f, kInfF);
+      }
+      s_f2[2 * ((b >> 1) * TPB + tid) + (b & 1)] = v;
+    }
+  }
+
+  int s = 0;
+  U4 rw{0u, 0u, 0u, 0u};
+  ArmStat qc{0.0, 0.0, 0.0, 0, 0};
+  int qc_b = -1;
+#if ZS_PHILOX_PREFIX
+  const uint32_t tlo = (uint32_t)trial, thi = (uint32_t)((uint64_t)trial >> 32);
+#endif
+  for (int t = a.t_split; t < R; ++t) {
+    double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
+    int vPacked = 0, b = 0, hkey = -1;
+    double C = 0.0;
+    if (S > 1)
+      while ((long long)(s + 1) * R <= (long long)t * S) ++s;
+    if (active) {
+      if ((t & 3) == 0 || t == a.t_split) rw = replica_words_c(trial, t);
+      // ---------------- step 2: Alg. 1, b = argmin_a theta_a over the survivors
+      const uint32_t unripe = 0u;   // every Thompson-phase arm has n >= 2 (run twice in pruning)
+      (void)unripe;
+      {
+        cert::Argmin32 am;
+        am.init();
+#if ZS_PHILOX_PREFIX
+        const PhiloxPrefix pre = philox_prefix((uint32_t)t, tlo, thi, k0f, k1f);
+#endif
+        uint32_t qm = quads;
+        while (qm) {                                        // same trip count across the warp
+          const int qd = __ffs(qm) - 1;
+          qm &= qm - 1u;
+#if ZS_PHILOX_PREFIX
+          const U4 x = philox_from_prefix(pre, (uint32_t)qd, k0f, k1f);
+#else
+          const U4 x = block_c(trial, t, qd);
+#endif
+          float z0, z1, ez;
+          const float4 m0 = s_f[(2 * qd) * TPB + tid];
+          cert::normal_pair32(x.x, x.y, z0, z1, ez);
+          am.ezmax = fmaxf(am.ezmax, ez);
+          am.arm(4 * qd, m0.x, m0.y, z0);
+          am.arm(4 * qd + 1, m0.z, m0.w, z1);
+          if (2 * qd + 1 < npairs) {
+            const float4 m1 = s_f[(2 * qd + 1) * TPB + tid];
+            cert::normal_pair32(x.z, x.w, z0, z1, ez);
+            am.ezmax = fmaxf(am.ezmax, ez);
+            am.arm(4 * qd + 2, m1.x, m1.y, z0);
+            am.arm(4 * qd + 3, m1.z, m1.w, z1);
+          }
+        }
+        b = am.b;
+        if (am.certified(c_trial) && !a.force_exact) {
+          n_cert += 1;
+        } else {
+          // the contract's exact draw (NC-3/NC-4): fp64 posteriors from the Observe records
+          // (the cached record is the newest of its arm), every survivor pair transformed,
+          // strict < in ascending arm order
+          n_fall += 1;
+          double bt = kInf;
+          b = -1;
+          int qcur = -1;
+          U4 xq{0u, 0u, 0u, 0u};
+          uint32_t pm = ts_pairs;
+          while (pm) {
+            const int k = __ffs(pm) - 1;
+            pm &= pm - 1u;
+            if ((k >> 1) != qcur) {
+              qcur = k >> 1;
+              xq = block_c(trial, t, qcur);
+            }
+            double z0, z1;
+            box_muller((k & 1) ? xq.z : xq.x, (k & 1) ? xq.w : xq.y, z0, z1, logtab);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int arm_i = 2 * k + h;
+              if (!((ts_set >> arm_i) & 1u)) continue;
+              const ArmStat q = (arm_i == qc_b) ? qc : st[arm_i];
+              const double2 ms = posterior(q.sh, q.S1, q.S2, q.cnt, cp.prec0, cp.pm0);
+              const double th = fma(ms.y, h ? z1 : z0, ms.x);
+              if (th < bt) { bt = th; b = arm_i; }
+            }
+          }
+        }
+        n_sampled += 1;
+      }
+      // Observe record of arm b (write-back cache)
+      if (b != qc_b) {
+        if (qc_b >= 0) st[qc_b] = qc;
+        qc = st[b];
+        qc_b = b;
+      }
+      const ArmConst ac = arm[b];
+      const int p = ac.pstar;
+      const double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;
+      // ---------------- step 3: replay one recorded run
+      const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
+      const int E = pool[((size_t)s * B + b) * K + r];
+      const int Erun = E > 0 ? E : a.max_epochs;
+      hkey = 2 * B * K + b * K + (int)r;                   // class: Thompson decision, no profiling
+      const double em1 = (double)(Erun - 1);
+      const double Cf = c1b + em1 * c1b;
+      // ---------------- step 4: early stop at β·min_t C_t, truncated charge
+      const double thr = cp.beta * best;
+      double Tm, En;
+      const bool stopped = Cf > thr;
+      if (stopped) {
+        C = thr;
+        if (thr <= c1b) {
+          const double phi = thr / c1b;
+          Tm = phi * t1b;
+          En = phi * e1b;
+        } else {
+          const double phi = (thr - c1b) / c1b;
+          Tm = t1b + phi * t1b;
+          En = e1b + phi * e1b;
+        }
+      } else {
+        C = Cf;
+        Tm = t1b + em1 * t1b;
+        En = e1b + em1 * e1b;
+      }
+      const bool conv = (E > 0) && !stopped;
+      if (conv && !(C >= best)) best = C;
+      const uint32_t flags = (stopped ? 1u : 0u) | (conv ? 2u : 0u) | 8u;
+      totC += C;
+      totE += En;
+      totT += Tm;
+      nstop += stopped ? 1 : 0;
+      last_b = b;
+      dig = (dig ^ (unsigned long long)(uint32_t)b) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)(uint32_t)p) * 0x100000001b3ull;
+      dig = (dig ^ (unsigned long long)flags) * 0x100000001b3ull;
+      if (LOG) a.log[o * R + t] = (uint32_t)b | ((uint32_t)p << 8) | (flags << 16);
+      vC = C;
+      vE = En;
+      vT = Tm;
+      vReg = regret[s * B + b];
+      vPacked = (stopped ? 1 : 0) | ((b == optarm[s]) ? (1 << 8) : 0) | (1 << 16);
+    }
+    {
+      const bool special = active && (vPacked & 1);
+      if (active && !special) red_add_u32(hist + (size_t)t * a.nhslot * HB + hkey, 1u);
+      if (__any_sync(0xffffffffu, special))
+        curve_accumulate(curves, t, tid & 31, special ? vC : 0.0, special ? vE : 0.0, special ? vT : 0.0,
+                         special ? vReg : 0.0, special ? vPacked : 0, a.curve_scale);
+    }
+    if (active) {
+      // ---------------- Alg. 2 Observe(b, C) with shifted sums (NC-6)
+      const double d = C - qc.sh;
+      qc.S1 = qc.S1 + d;
+      qc.S2 = qc.S2 + d * d;
+      qc.cnt += 1;
+      const double2 ms = posterior(qc.sh, qc.S1, qc.S2, qc.cnt, cp.prec0, cp.pm0);
+      const double dm = ms.x - ref;
+      s_f2[2 * ((b >> 1) * TPB + tid) + (b & 1)] =
+          (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y) : make_float2(0.0f, kInfF);
+      n_recomp += 1;
+    }
+  }
+  if (active && qc_b >= 0) st[qc_b] = qc;
+  if (active) {
+    a.tot_cost[o] = totC;
+    a.tot_energy[o] = totE;
+    a.tot_time[o] = totT;
+    a.digest[o] = dig;
+    a.n_stop[o] = nstop;
+    a.final_arm[o] = last_b;
+  }
+  // counters: the method's events (as replay_kernel), then the work: [9] fp64 transforms
+  // (fallback draws), [10] Philox blocks, [11] fp32 pairs, [12] certified, [13] fallbacks
+  unsigned long long fall_pairs = (unsigned long long)n_fall * __popc(ts_pairs);
+  unsigned long long fp32_pairs = 0;
+  {
+    uint32_t qm = quads;
+    int np = 0;
+    while (qm) { const int qd = __ffs(qm) - 1; qm &= qm - 1u; np += (2 * qd + 1 < npairs) ? 2 : 1; }
+    fp32_pairs = (unsigned long long)n_sampled * np;
+  }
+  const unsigned long long blocks_fp32 = (unsigned long long)n_sampled * __popc(quads);
+  const unsigned long long blocks_fall = (unsigned long long)n_fall * __popc(quads);
+  uint32_t n_prune = 0;
+  if (active) {
+    const Carry c = a.carry[o];
+    n_sampled += c.n_sampled; n_prune = c.n_prune; n_forced += c.n_forced; n_recomp += c.n_recomp;
+  }
+  const unsigned long long pairs_all = (unsigned long long)n_sampled * __popc(ts_pairs);
+  const unsigned long long blocks_all = (unsigned long long)n_sampled * __popc(quads);
+  unsigned long long ctr[kCounters] = {
+      active ? (unsigned long long)R : 0ull, n_sampled, pairs_all,
+      (unsigned long long)n_sampled * __popc(ts_set),
+      (unsigned long long)nstop, n_prune, n_forced, n_recomp, blocks_all,
+      active ? fall_pairs : 0ull, active ? blocks_fp32 + blocks_fall : 0ull, active ? fp32_pairs : 0ull,
+      active ? n_cert : 0ull, active ? n_fall : 0ull};
+#pragma unroll
+  for (int q = 0; q < kCounters; ++q) {
+    unsigned long long v = ctr[q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((tid & 31) == 0 && v) atomicAdd(a.counters + q, v);
+  }
+}
+
+}  // namespace zs

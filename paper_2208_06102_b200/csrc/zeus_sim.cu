@@ -16,6 +16,7 @@
 
 #include "../../include/zeus_sim.h"
 #include "kernels.cuh"
+#include "thompson.cuh"
 
 namespace {
 
@@ -48,7 +49,7 @@ struct zeus_sim {
   // cells / run
   std::vector<zeus_cell> cells;
   std::vector<zs::CellParam> cpar;
-  int R = 0, log_mode = 0, layout = 0, device = 0, wmax = 0;
+  int R = 0, log_mode = 0, layout = 0, device = 0, wmax = 0, draw = 0;
   int64_t shard_total = 0, max_shard = 0;
   // trace
   int S = 0, K = 0, reg_stride = 0, opt_stride = 0;
@@ -307,6 +308,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     if (opts->log_mode != 0 && opts->log_mode != 1) E.add(ZEUS_E_INVALID, "log_mode must be 0 or 1");
     if (opts->layout < 0 || opts->layout > 3) E.add(ZEUS_E_INVALID, "layout must be 0, 1, 2 or 3");
     if (opts->graph != 0 && opts->graph != 1) E.add(ZEUS_E_INVALID, "graph must be 0 or 1");
+    if (opts->draw < 0 || opts->draw > 2) E.add(ZEUS_E_INVALID, "draw must be 0, 1 or 2");
   }
   if (E.code != ZEUS_OK) return fail(nullptr, E.code, E.s);
 
@@ -334,6 +336,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
   s->log_mode = opts->log_mode;
   s->layout = opts->layout;
   s->use_graph = opts->graph;
+  s->draw = opts->draw;
   {                                      // arrival schedules: finite, non-decreasing (R-Q31)
     Errors EA;
     for (int i = 0; i < num_cells; ++i) {
@@ -616,6 +619,10 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
       for (int ph = 0; ph < 3; ++ph)
         for (int ab = 0; ab < 3; ++ab)            // ab == 2: the RK kernels
           ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph, ab == 1, ab == 2), s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, false>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, false>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, true>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, true>, s->device));
   ZS_CUDA(s, grant_group<2>(s->device));
   ZS_CUDA(s, grant_group<4>(s->device));
   ZS_CUDA(s, grant_group<8>(s->device));
@@ -777,6 +784,22 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     auto replay_launch = [&](int phase) {
       replay_fn(windowed, s->log_mode, phase, s->any_ablation, rk)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
     };
+    // the Thompson phase with the certified fp32 draw unless the run asks for
+    // the exact-screen kernel (draw = 1); cells with a window or an ablation keep replay_kernel
+    const bool certified = !windowed && !s->any_ablation && s->draw != 1;
+    a.key_quads = certified ? 1 : 0;
+    a.force_exact = s->draw == 2 ? 1 : 0;
+    auto thompson_launch = [&]() {
+      const dim3 tgrid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
+      const size_t tsmem = (size_t)s->tab_bytes + (size_t)128 * (((s->B + 1) / 2) * 16);
+      if (rk) {
+        if (s->log_mode) zs::thompson_kernel<true, true><<<tgrid, 128, tsmem, st>>>(a);
+        else zs::thompson_kernel<false, true><<<tgrid, 128, tsmem, st>>>(a);
+      } else {
+        if (s->log_mode) zs::thompson_kernel<true, false><<<tgrid, 128, tsmem, st>>>(a);
+        else zs::thompson_kernel<false, false><<<tgrid, 128, tsmem, st>>>(a);
+      }
+    };
     // auto: two phases except for windowed launches, where the one-pass kernel measured
     // faster (CFG4 1.45e10 vs 1.30e10 decisions/s); explicit layouts are honoured
     const bool two_phase = (s->layout == 2 || (s->layout == 0 && !windowed)) && a.t_split < s->R;
@@ -801,9 +824,10 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
       ZS_CUDA(s, cudaGetLastError());
       const unsigned sx = (unsigned)std::min<int64_t>((s->max_shard + 255) / 256, 1184);
       zs::bucket_scatter_kernel<<<dim3(std::max(1u, sx), (unsigned)nc), 256, 0, st>>>(
-          a.cells, a.carry, a.bucket, a.perm, nc, s->B, s->nwin);
+          a.cells, a.carry, a.bucket, a.perm, nc, s->B, s->nwin, a.key_quads);
       ZS_CUDA(s, cudaGetLastError());
-      replay_launch(2);
+      if (certified) thompson_launch();
+      else replay_launch(2);
       ZS_CUDA(s, cudaGetLastError());
     }
     if (!s->any_ablation) {                    // the counted runs into the exact sums
@@ -991,6 +1015,46 @@ zeus_status zeus_sim_shape(const zeus_sim *s, int32_t *recurrences, int64_t *sha
   if (num_cells) *num_cells = (int32_t)s->cells.size();
   if (num_batch_sizes) *num_batch_sizes = s->B;
   if (num_slices) *num_slices = s->S;
+  return ZEUS_OK;
+}
+
+zeus_status zeus_sim_certify_bounds(int32_t cuda_device, double *out) {
+  if (!out) return ZEUS_E_INVALID;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) return ZEUS_E_CUDA;
+  if (cudaSetDevice(cuda_device) != cudaSuccess) return ZEUS_E_CUDA;
+  cudaStream_t st = nullptr;
+  double2 *tab = nullptr;
+  unsigned *d_out = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&tab, zs::kLogTab * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, 4 * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_out, 0, 4 * sizeof(unsigned), st);
+  if (e == cudaSuccess) {
+    zs::log_table_kernel<<<1, 128, 0, st>>>(tab);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    const uint64_t N = 1ull << 32, chunk = 1ull << 30;    // every 32-bit word, in four launches
+    for (uint64_t b = 0; b < N; b += chunk) {
+      zs::cert::certify_radius_kernel<<<sms * 8, 256, 0, st>>>(tab, b, chunk, d_out);
+      zs::cert::certify_angle_kernel<<<sms * 8, 256, 0, st>>>(b, chunk, d_out);
+    }
+    e = cudaGetLastError();
+  }
+  unsigned h[4] = {0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, d_out, sizeof(h), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (tab) cudaFree(tab);
+  if (d_out) cudaFree(d_out);
+  if (st) cudaStreamDestroy(st);
+  if (e != cudaSuccess) return ZEUS_E_CUDA;
+  for (int i = 0; i < 4; ++i) {
+    float f;
+    std::memcpy(&f, &h[i], 4);
+    out[i] = f;
+  }
+  out[4] = zs::cert::kAng;
+  out[5] = zs::cert::kRMax;
   return ZEUS_OK;
 }
 

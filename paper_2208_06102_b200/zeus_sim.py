@@ -22,9 +22,10 @@ ZEUS_OK = 0
 STATUS = {0: "ZEUS_OK", 1: "ZEUS_E_INVALID", 2: "ZEUS_E_STATE", 3: "ZEUS_E_NO_CONVERGENT_ARM",
           4: "ZEUS_E_CUDA", 5: "ZEUS_E_NOMEM", 6: "ZEUS_E_UNSUPPORTED"}
 CURVE_Q = 7
-COUNTERS = 12
+COUNTERS = 14
 EXPORTS = ("zeus_sim_create", "zeus_sim_load_profile", "zeus_sim_run", "zeus_sim_results",
-           "zeus_sim_destroy", "zeus_sim_last_error", "zeus_sim_shape", "zeus_sim_curves_from_fixed")
+           "zeus_sim_destroy", "zeus_sim_last_error", "zeus_sim_shape", "zeus_sim_curves_from_fixed",
+           "zeus_sim_certify_bounds")
 CURVE_LIMBS = 3
 
 
@@ -52,7 +53,7 @@ class zeus_cell(C.Structure):
 class zeus_run_opts(C.Structure):
     _fields_ = [("struct_size", C.c_uint32), ("recurrences", C.c_int32),
                 ("shard_begin", C.c_int64), ("shard_end", C.c_int64), ("log_mode", C.c_int32),
-                ("layout", C.c_int32), ("graph", C.c_int32)]
+                ("layout", C.c_int32), ("graph", C.c_int32), ("draw", C.c_int32)]
 
 
 class zeus_results(C.Structure):
@@ -90,8 +91,9 @@ def lib():
         L.zeus_sim_last_error.restype = C.c_char_p
         L.zeus_sim_shape.argtypes = [C.c_void_p] + [C.c_void_p] * 5
         L.zeus_sim_curves_from_fixed.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.zeus_sim_certify_bounds.argtypes = [C.c_int32, C.c_void_p]
         for f in ("zeus_sim_create", "zeus_sim_load_profile", "zeus_sim_run", "zeus_sim_results",
-                  "zeus_sim_shape", "zeus_sim_curves_from_fixed"):
+                  "zeus_sim_shape", "zeus_sim_curves_from_fixed", "zeus_sim_certify_bounds"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -129,6 +131,13 @@ def zeus_sim_curves_from_fixed(h, curves_fixed, curves):
     _check(lib().zeus_sim_curves_from_fixed(h, _ptr(curves_fixed), _ptr(curves)), h)
 
 
+def zeus_sim_certify_bounds(cuda_device: int = 0):
+    """Exhaustive check of the certified draw's error bounds (include/zeus_sim.h): 6 doubles."""
+    out = np.zeros(6)
+    _check(lib().zeus_sim_certify_bounds(int(cuda_device), _ptr(out)), None)
+    return out
+
+
 def zeus_sim_destroy(h):
     if h:
         lib().zeus_sim_destroy(h)
@@ -156,7 +165,7 @@ class Simulation:
     """
 
     def __init__(self, workload, cells, trials, recurrences=0, shard=(0, -1), log=False,
-                 device=0, layout=0, graph=False):
+                 device=0, layout=0, graph=False, draw=0):
         self.w = workload
         bs = np.ascontiguousarray(workload["batch_sizes"], dtype=np.int32)
         pl = np.ascontiguousarray(workload["power_limits"], dtype=np.float64)
@@ -178,7 +187,8 @@ class Simulation:
                                 int(c.get("seed", 0)), int(trials), int(c.get("policy", 0)),
                                 int(c.get("ablation", 0)), ptr))
         opts = zeus_run_opts(C.sizeof(zeus_run_opts), int(recurrences), int(shard[0]),
-                             int(shard[1]), 1 if log else 0, int(layout), 1 if graph else 0)
+                             int(shard[1]), 1 if log else 0, int(layout), 1 if graph else 0,
+                             int(draw))
         self.h = zeus_sim_create(job, cs, opts, device)
         R, n, nc, B, S = (C.c_int32(), C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32())
         lib().zeus_sim_shape(self.h, C.byref(R), C.byref(n), C.byref(nc), C.byref(B), None)

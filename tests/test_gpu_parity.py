@@ -35,8 +35,9 @@ def oracle_threads(oracle):
     return max(1, min(64, oracle.hardware_threads()))
 
 
-def run_gpu(zs, w, cells, trials, R, shard=(0, -1), log=False, want=None, layout=0):
-    sim = zs.Simulation(w, cells, trials, R, shard=shard, log=log, layout=layout).load_profile().run()
+def run_gpu(zs, w, cells, trials, R, shard=(0, -1), log=False, want=None, layout=0, draw=0):
+    sim = zs.Simulation(w, cells, trials, R, shard=shard, log=log, layout=layout,
+                        draw=draw).load_profile().run()
     keys = ["curves", "curves_fixed", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm",
             "counters", "pstar_index", "c1", "t1", "e1", "c_prof", "t_prof", "e_prof", "opt_cost",
             "opt_arm"] + (["log"] if log else [])
@@ -273,8 +274,8 @@ def test_schedules_bit_identical(zs, oracle, name):
     phase) and layout 3 (lane group per trial) give the same bits for every trial and
     decision."""
     (job,) = synth.config(name, trials=2000 if name != "cfg5" else 700)
-    outs = [run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True, layout=l)
-            for l in (1, 2, 3)]
+    outs = [run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True, layout=l, draw=d)
+            for l, d in ((1, 0), (2, 1), (3, 0), (2, 0), (2, 2))]
     for o in outs[1:]:
         for k in ("log", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm"):
             assert np.array_equal(outs[0][k], o[k]), k
@@ -283,12 +284,20 @@ def test_schedules_bit_identical(zs, oracle, name):
     # evaluated work: lane groups transform every survivor pair (each with its own Philox
     # block); the bound screen of the one-pass and Thompson-phase kernels
     # transforms at most as many, and far fewer once the posteriors separate
-    c1, c2, c3 = (o["counters"] for o in outs)
+    c1, c2, c3, c4, c5 = (o["counters"] for o in outs)
     assert c3[9] == c3[2] and c3[10] == c3[2]
     for c in (c1, c2):
         assert c[9] <= c[2] and c[10] >= c[8]
         if name == "cfg5":
             assert c[9] < 0.6 * c[2]
+    # certified fp32 draw: every Thompson-phase draw is either certified or
+    # sent to the exact fallback; draw = 2 sends all of them
+    ts_b = c4[12] + c4[13]
+    if job.cells[0]["window"] == 0:
+        assert ts_b > 0 and c5[12] == 0 and c5[13] == ts_b
+        assert c4[13] <= 0.01 * ts_b
+    else:                                    # a window keeps the exact-screen kernel
+        assert ts_b == 0 and c5[12] + c5[13] == 0
     compare_cell(oracle, outs[1], job.workload, job.cells[0], 0, np.arange(job.trials),
                  job.recurrences, job.trials, logs=True)
 
@@ -407,7 +416,7 @@ def test_bound_screen_every_path(zs, oracle):
                         prior_var=math.inf)]
     trials, R = 400, 90
     for layout in (1, 2):
-        g = run_gpu(zs, w, cells, trials, R, log=True, layout=layout)
+        g = run_gpu(zs, w, cells, trials, R, log=True, layout=layout, draw=1)
         c = g["counters"]
         assert c[9] < c[2]                       # pairs screened out
         assert c[10] > c[8]                      # a third residual redrew its block
@@ -440,17 +449,46 @@ def test_round_key_kernels_match_multicell_launch(zs):
     (6, 7, 40, 4, 10, 2.0, 300, 40),      # drift-shaped: one slice per recurrence, window N = 10
     (3, 4, 1, 2, 0, math.inf, 130, 30),   # two pairs, no early stop
 ])
-@pytest.mark.parametrize("layout", [1, 2])
-def test_random_traces_one_cell(zs, oracle, B, P, S, K, window, beta, trials, R, layout):
+@pytest.mark.parametrize("layout,draw", [(1, 0), (2, 0), (2, 1), (2, 2)])
+def test_random_traces_one_cell(zs, oracle, B, P, S, K, window, beta, trials, R, layout, draw):
     """One-cell launches run the RK kernels (round keys in the parameters, the
     record cache with write-back in the Thompson phase); edge shapes in both schedules,
     every decision bit-exact vs the oracle."""
     rng = np.random.default_rng(B * 7919 + S)
     w = _random_trace(rng, B, P, S, K)
     cell = synth.cell(eta=0.6, beta=beta, window=window, seed=int(rng.integers(2**63)))
-    g = run_gpu(zs, w, [cell], trials, R, log=True, layout=layout)
+    g = run_gpu(zs, w, [cell], trials, R, log=True, layout=layout, draw=draw)
     compare_step1(oracle, g, w, [cell])
     compare_cell(oracle, g, w, cell, 0, np.arange(trials), R, trials, logs=True)
+
+
+def test_certified_draw_bounds(zs):
+    """the two measured bounds behind the certified fp32 draw hold for EVERY
+    32-bit word -- |r32 - r| <= e_r(a) for all 2^32 radius words and |cos32 - cos|, |sin32 - sin|
+    <= kAng for all 2^32 angle words, against the contract's fp64 values (NC-3)."""
+    out = zs.zeus_sim_certify_bounds(0)
+    assert out[0] <= 1.0, f"radius bound exceeded: ratio {out[0]}"
+    assert 6.66 < out[1] <= out[5]
+    assert out[2] <= out[4] and out[3] <= out[4], out
+    assert out[2] > 0.5 * out[4] and out[3] > 0.5 * out[4]      # the bound is measured, not loose
+
+
+def test_certified_draw_multicell_and_drift(zs, oracle):
+    """The certified draw in multi-cell launches (keys derived in-kernel, no RK), a proper prior
+    and a drifting trace without a window: draw 0, 1 and 2 give the oracle's bits."""
+    rng = np.random.default_rng(2024)
+    w = _random_trace(rng, 12, 6, 5, 4)
+    cells = [synth.cell(eta=0.3, beta=2.0, seed=11, prior_mean=500.0, prior_var=1e4),
+             synth.cell(eta=0.8, beta=math.inf, seed=12)]
+    trials, R = 600, 150
+    ref = None
+    for d in (0, 1, 2):
+        g = run_gpu(zs, w, cells, trials, R, log=True, layout=2, draw=d)
+        for ci, c in enumerate(cells):
+            compare_cell(oracle, g, w, c, ci, np.arange(trials), R, trials, logs=True, full_curves=False)
+        if ref is None:
+            ref = g
+        assert np.array_equal(ref["curves"], g["curves"])
 
 
 def test_reload_is_stream_ordered(zs, oracle):

@@ -22,6 +22,14 @@ namespace zs {
 #ifndef ZS_PHILOX_PREFIX
 #define ZS_PHILOX_PREFIX 1
 #endif
+#ifndef ZS_PHILOX_WIDE
+#define ZS_PHILOX_WIDE 1
+#endif
+#ifdef ZS_TH_MIN_BLOCKS
+#define ZS_TH_BOUNDS __launch_bounds__(128, ZS_TH_MIN_BLOCKS)
+#else
+#define ZS_TH_BOUNDS __launch_bounds__(128)
+#endif
 
 // Philox4x32-10 of counter (t, 1<<24 | q, lo32 trial, hi32 trial) for several q at one (trial,
 // t) (NC-3): the first three rounds share the products that do not depend on q.
@@ -47,26 +55,43 @@ __device__ __forceinline__ PhiloxPrefix philox_prefix(uint32_t t, uint32_t tlo, 
   p.l0 = M0 * x2;
   return p;
 }
+// 32 x 32 -> 64-bit product as one IMAD.WIDE.U32 (the compiler otherwise splits some of the
+// rounds' products into IMAD.HI + IMAD under register pressure)
+__device__ __forceinline__ void mul_wide(uint32_t a, uint32_t m, uint32_t &hi, uint32_t &lo) {
+#if ZS_PHILOX_WIDE
+  uint64_t p;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(m));
+  lo = (uint32_t)p;
+  hi = (uint32_t)(p >> 32);
+#else
+  hi = __umulhi(a, m);
+  lo = a * m;
+#endif
+}
+
 template <class K0, class K1>
 __device__ __forceinline__ U4 philox_from_prefix(const PhiloxPrefix &p, uint32_t q, K0 k0, K1 k1) {
   constexpr uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
   const uint32_t x1 = p.x1b ^ q;                       // round 0 output x (y1 = lo(M1 tlo) is
-  const uint32_t H0 = __umulhi(M0, x1), L0 = M0 * x1;  // consumed by the prefix's x2)
+  uint32_t H0, L0;                                     // consumed by the prefix's x2)
+  mul_wide(x1, M0, H0, L0);
   const uint32_t z2 = H0 ^ p.w1 ^ k1(1);               // round 1 output (x2, y2 shared)
   const uint32_t w2 = L0;
-  const uint32_t H1 = __umulhi(M1, z2), L1 = M1 * z2;
+  uint32_t H1, L1;
+  mul_wide(z2, M1, H1, L1);
   U4 c{H1 ^ p.y2 ^ k0(2), L1, p.h0 ^ w2 ^ k1(2), p.l0};   // round 2 output
 #pragma unroll
   for (int r = 3; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
-    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    uint32_t hi0, lo0, hi1, lo1;
+    mul_wide(c.x, M0, hi0, lo0);
+    mul_wide(c.z, M1, hi1, lo1);
     c = U4{hi1 ^ c.y ^ k0(r), lo1, hi0 ^ c.w ^ k1(r), lo0};
   }
   return c;
 }
 
 template <bool LOG, bool RK>
-__global__ void __launch_bounds__(128) thompson_kernel(ReplayArgs a) {
+__global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
   const int cell = blockIdx.y;

@@ -15,7 +15,9 @@ import json, sys
 try:
     d = json.loads(open(sys.argv[2]).read().strip().splitlines()[-1])
     r = d["roofline"]
-    print(f"{sys.argv[1]:10s} {d['value']:.4g} dec/s  replay {d['replay_ms_per_step']:.1f} ms  issue-frac {r['frac']:.3f} fp64-frac {r['fp64']['frac']:.3f} clk {d['clocks']['sm_mhz']}")
+    c = d["counters_per_step"]
+    fb = c[13] / max(1, c[12] + c[13]) if len(c) > 13 else float("nan")
+    print(f"{sys.argv[1]:10s} {d['value']:.4g} dec/s  replay {d['replay_ms_per_step']:.1f} ms  frac {r['frac']:.3f} fallback {fb:.2e} clk {d['clocks']['sm_mhz']}")
 except Exception as e:
     print(sys.argv[1], "FAILED", e)
 PY

@@ -34,6 +34,11 @@ VARIANTS = {
     "u1_r72": (["ZS_MAXNREG=72"], []),
     "u1_r64": (["ZS_MAXNREG=64"], []),
     "u1_r56": (["ZS_MAXNREG=56"], []),
+    # round 2: the certified-draw Thompson kernel (thompson.cuh)
+    "th_mb5": (["ZS_TH_MIN_BLOCKS=5"], []),
+    "th_nowide": (["ZS_PHILOX_WIDE=0"], []),
+    "th_noprefix": (["ZS_PHILOX_PREFIX=0"], []),
+    "th_mb6": (["ZS_TH_MIN_BLOCKS=6"], []),
 }
 
 if __name__ == "__main__":
@@ -45,7 +50,7 @@ if __name__ == "__main__":
         log = open(out + ".ptxas.log").read().split("Compiling entry function")
         for part in log:
             head = part.split("\n")[0]
-            if "replay_kernelILb0ELb0E" in head or "replay_kernel_tsILb0ELb0E" in head:
+            if "replay_kernelILb0ELb0E" in head or "thompson_kernelILb0ELb1E" in head:
                 ph = head.split("ELi")[1][0] if "ELi" in head else "ts"
                 print(n, "phase", ph, [l.strip()[-70:] for l in part.splitlines()
                                        if "Used" in l or "spill" in l])

@@ -22,22 +22,23 @@ src = open("paper_2208_06102_b200/csrc/kernels.cuh").read().splitlines()
 
 
 def region(f, ln):
-    if f == "contract.cuh":
-        s = open("paper_2208_06102_b200/csrc/contract.cuh").read().splitlines()
+    if f in ("contract.cuh", "certify.cuh"):
+        s = open("paper_2208_06102_b200/csrc/" + f).read().splitlines()
         # name the enclosing function
         for i in range(ln - 1, -1, -1):
-            t = s[i]
+            t = s[i].strip()
             if t.startswith("__device__") or t.startswith("__global__"):
-                return "contract:" + t.split("(")[0].split()[-1]
-        return "contract:?"
-    if f != "kernels.cuh":
+                return f.split(".")[0] + ":" + t.split("(")[0].split()[-1]
+        return f + ":?"
+    if f not in ("kernels.cuh", "thompson.cuh"):
         return f
+    lines = src if f == "kernels.cuh" else open("paper_2208_06102_b200/csrc/thompson.cuh").read().splitlines()
     for i in range(ln - 1, -1, -1):
-        t = src[i].strip()
+        t = lines[i].strip()
         if t.startswith("// ----------------") or t.startswith("__device__") or t.startswith("__global__") \
                 or t.startswith("auto ") or "// REGION" in t:
-            return "kernels:" + t[:60]
-    return "kernels:?"
+            return f.split(".")[0] + ":" + t[:60]
+    return f + ":?"
 
 
 agg = {}

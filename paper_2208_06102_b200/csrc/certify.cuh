@@ -72,44 +72,50 @@ __device__ __forceinline__ void angle32(uint32_t b, float &s, float &c) {
   __sincosf((float)(int)b * 1.4629180792671596e-09f, &s, &c);       // 2 pi 2^-32
 }
 
-// One Box-Muller pair in fp32: z0~, z1~ and e_z >= |z~ - z| for both (+inf when unbounded).
-__device__ __forceinline__ void normal_pair32(uint32_t a, uint32_t b, float &z0, float &z1, float &ez) {
-  float r, rsq, s, c;
+// One Box-Muller pair in fp32: z0~, z1~, and rsq = 1/r~ for its error bound: for every pair,
+// |z~ - z| <= e_z = kZr kRMax + kZb rsq (the r~-dependent term at its largest; +inf at r2 = 0).
+__device__ __forceinline__ void normal_pair32(uint32_t a, uint32_t b, float &z0, float &z1, float &rsq) {
+  float r, s, c;
   radius32(a, r, rsq);
   angle32(b, s, c);
   z0 = r * c;
   z1 = r * s;
-  ez = __fmaf_ru(fminf(r, kRMax), kZr, __fmul_ru(rsq, kZb));
 }
 
-// Running argmin with the second-smallest value and the largest sigma (every arm of a touched
-// pair is passed; non-survivor slots hold mu' = +inf, sigma = 0 and drop out).
+// Running argmin over packed keys: arm a's key is theta~_a with its low `bits` mantissa bits
+// replaced by a, so one FMNMX carries the arm along (|key - theta~| < 2^bits ulp, charged to
+// kTheta); the second-smallest key, the largest sigma and the largest 1/r~ come along.
+// Non-survivor slots hold mu' = 3e38, sigma = 0: a finite key above every survivor's.
 struct Argmin32 {
-  float m1, m2, smax, ezmax;
-  int b;
+  float m1, m2, smax, rsqmax;
   __device__ __forceinline__ void init() {
     m1 = m2 = __int_as_float(0x7f800000);
     smax = 0.0f;
-    ezmax = 0.0f;
-    b = -1;
+    rsqmax = 0.0f;
   }
-  __device__ __forceinline__ void arm(int a, float mu, float sig, float z) {
-    const float th = fmaf(sig, z, mu);
-    const bool take = th < m1;
-    m2 = fminf(m2, fmaxf(m1, th));
-    m1 = fminf(m1, th);
-    b = take ? a : b;
-    smax = fmaxf(smax, sig);
+  // arms 2k, 2k+1 (index a0, a0 + 1) of one Box-Muller pair
+  __device__ __forceinline__ void pair(int a0, float4 ms, float z0, float z1, float rsq, uint32_t keep) {
+    const float t0 = fmaf(ms.y, z0, ms.x);
+    const float t1 = fmaf(ms.w, z1, ms.z);
+    const float k0 = __int_as_float((__float_as_int(t0) & (int)keep) | a0);
+    const float k1 = __int_as_float((__float_as_int(t1) & (int)keep) | (a0 + 1));
+    const float lo = fminf(k0, k1), hi = fmaxf(k0, k1);
+    m2 = fminf(fminf(m2, hi), fmaxf(m1, lo));
+    m1 = fminf(m1, lo);
+    smax = fmaxf(smax, fmaxf(ms.y, ms.w));
+    rsqmax = fmaxf(rsqmax, rsq);
   }
-  // Is b the contract's argmin?  For every other survivor x: theta~_x >= m2, and
-  // t - kTheta |t| is increasing in t, so theta_x - ref >= m2 - kTheta |m2| - S, while
-  // theta_b - ref <= m1 + kTheta |m1| + S, S = smax (ezmax + kSig) kSigScale + c_trial.
-  // NaN anywhere (an unbounded pair, overflow) fails the test; m2 = +inf (one survivor) passes
-  // whenever S is finite.
-  __device__ __forceinline__ bool certified(float c_trial) const {
-    const float S = __fmaf_ru(__fmul_ru(smax, kSigScale), __fadd_ru(ezmax, kSig), c_trial);
-    const float lo2 = (m2 == __int_as_float(0x7f800000)) ? m2 : __fmaf_rd(-kTheta, fabsf(m2), m2);
-    const float hi1 = __fmaf_ru(kTheta, fabsf(m1), m1);
+  __device__ __forceinline__ int arg(uint32_t keep) const { return __float_as_int(m1) & (int)~keep; }
+  // Is arg() the contract's argmin?  For every other survivor x: key_x >= m2 (distinct arms have
+  // distinct keys), and t - kth |t| is increasing in t, so theta_x - ref >= m2 - kth |m2| - S,
+  // while theta_b - ref <= m1 + kth |m1| + S, S = smax (e_z + kSig) kSigScale + c_trial,
+  // kth = kTheta + 2^(bits-23) (1 + 2^-20).  NaN anywhere fails the test; m2 = +inf (one
+  // survivor) passes whenever S is finite.
+  __device__ __forceinline__ bool certified(float c_trial, float kth) const {
+    const float ez = __fmaf_ru(rsqmax, kZb, kZr * kRMax * 1.000001f);
+    const float S = __fmaf_ru(__fmul_ru(smax, kSigScale), __fadd_ru(ez, kSig), c_trial);
+    const float lo2 = (m2 == __int_as_float(0x7f800000)) ? m2 : __fmaf_rd(-kth, fabsf(m2), m2);
+    const float hi1 = __fmaf_ru(kth, fabsf(m1), m1);
     return __fsub_rd(lo2, hi1) > __fmul_ru(2.0f, S);
   }
 };

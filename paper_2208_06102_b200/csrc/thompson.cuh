@@ -152,7 +152,10 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
   long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
   const int HB = 4 * B * K;
-  uint32_t *hist = a.hist + ((size_t)cell * R * a.nhslot + (warp_global % a.nhslot)) * (size_t)HB;
+  // counted runs of class (Thompson decision, no profiling), row t_split; one row per t
+  const size_t hstride = (size_t)a.nhslot * HB;
+  uint32_t *hrow = a.hist + ((size_t)cell * R * a.nhslot + (warp_global % a.nhslot)) * (size_t)HB +
+                   (size_t)a.t_split * hstride + 2 * B * K;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const float kInfF = __int_as_float(0x7f800000);
 
@@ -164,6 +167,10 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   double ref = 0.0;
   float c_trial = 0.0f;
   const int npairs = (B + 1) >> 1;
+  // key packing (certify.cuh Argmin32): the arm index in the low `bits` mantissa bits
+  const int kbits = 32 - __clz(2 * npairs - 1);
+  const uint32_t keep = ~((1u << kbits) - 1u);
+  const float kth = cert::kTheta + __int_as_float((127 - 23 + kbits) << 23) * 1.000001f;
   if (active) {                                             // resume from phase A
     const Carry c = a.carry[o];
     best = c.best; totC = c.totC; totE = c.totE; totT = c.totT; dig = c.dig;
@@ -182,7 +189,9 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
     if (!(fabs(ref) < 1e30)) ref = 0.0;
     c_trial = __double2float_ru(fabs(ref) * 0x1p-52 + 0x1p-120);
     for (int b = 0; b < 2 * npairs; ++b) {                  // every survivor was run (and observed
-      float2 v = make_float2(kInfF, 0.0f);                  // at least twice) in pruning
+      // non-survivor slot: theta~ = 3e38 for every z, a finite key above every survivor's
+      // (|mu'| < 1e30, sigma < 1e30), so it never wins and never hides a survivor's key
+      float2 v = make_float2(3.0e38f, 0.0f);                // (every survivor ran at least twice)
       if ((ts_set >> b) & 1u) {
         const ArmStat q = st[b];
         const double2 ms = posterior(q.sh, q.S1, q.S2, q.cnt, cp.prec0, cp.pm0);
@@ -226,22 +235,18 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
 #else
           const U4 x = block_c(trial, t, qd);
 #endif
-          float z0, z1, ez;
+          float z0, z1, rsq;
           const float4 m0 = s_f[(2 * qd) * TPB + tid];
-          cert::normal_pair32(x.x, x.y, z0, z1, ez);
-          am.ezmax = fmaxf(am.ezmax, ez);
-          am.arm(4 * qd, m0.x, m0.y, z0);
-          am.arm(4 * qd + 1, m0.z, m0.w, z1);
+          cert::normal_pair32(x.x, x.y, z0, z1, rsq);
+          am.pair(4 * qd, m0, z0, z1, rsq, keep);
           if (2 * qd + 1 < npairs) {
             const float4 m1 = s_f[(2 * qd + 1) * TPB + tid];
-            cert::normal_pair32(x.z, x.w, z0, z1, ez);
-            am.ezmax = fmaxf(am.ezmax, ez);
-            am.arm(4 * qd + 2, m1.x, m1.y, z0);
-            am.arm(4 * qd + 3, m1.z, m1.w, z1);
+            cert::normal_pair32(x.z, x.w, z0, z1, rsq);
+            am.pair(4 * qd + 2, m1, z0, z1, rsq, keep);
           }
         }
-        b = am.b;
-        if (am.certified(c_trial) && !a.force_exact) {
+        b = am.arg(keep);
+        if (am.certified(c_trial, kth) && !a.force_exact) {
           n_cert += 1;
         } else {
           // the contract's exact draw (NC-3/NC-4): fp64 posteriors from the Observe records
@@ -288,7 +293,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
       const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
       const int E = pool[((size_t)s * B + b) * K + r];
       const int Erun = E > 0 ? E : a.max_epochs;
-      hkey = 2 * B * K + b * K + (int)r;                   // class: Thompson decision, no profiling
+      hkey = b * K + (int)r;                               // bin (b, replica) of the row
       const double em1 = (double)(Erun - 1);
       const double Cf = c1b + em1 * c1b;
       // ---------------- step 4: early stop at β·min_t C_t, truncated charge
@@ -331,7 +336,8 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
     }
     {
       const bool special = active && (vPacked & 1);
-      if (active && !special) red_add_u32(hist + (size_t)t * a.nhslot * HB + hkey, 1u);
+      if (active && !special) red_add_u32(hrow + hkey, 1u);
+      hrow += hstride;
       if (__any_sync(0xffffffffu, special))
         curve_accumulate(curves, t, tid & 31, special ? vC : 0.0, special ? vE : 0.0, special ? vT : 0.0,
                          special ? vReg : 0.0, special ? vPacked : 0, a.curve_scale);

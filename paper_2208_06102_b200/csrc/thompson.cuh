@@ -167,8 +167,9 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   double ref = 0.0;
   float c_trial = 0.0f;
   const int npairs = (B + 1) >> 1;
+  const int npairs2 = (npairs + 1) & ~1;                    // whole quads (padding: non-survivors)
   // key packing (certify.cuh Argmin32): the arm index in the low `bits` mantissa bits
-  const int kbits = 32 - __clz(2 * npairs - 1);
+  const int kbits = 32 - __clz(2 * npairs2 - 1);
   const uint32_t keep = ~((1u << kbits) - 1u);
   const float kth = cert::kTheta + __int_as_float((127 - 23 + kbits) << 23) * 1.000001f;
   if (active) {                                             // resume from phase A
@@ -188,7 +189,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
     }
     if (!(fabs(ref) < 1e30)) ref = 0.0;
     c_trial = __double2float_ru(fabs(ref) * 0x1p-52 + 0x1p-120);
-    for (int b = 0; b < 2 * npairs; ++b) {                  // every survivor was run (and observed
+    for (int b = 0; b < 2 * npairs2; ++b) {                 // every survivor was run (and observed
       // non-survivor slot: theta~ = 3e38 for every z, a finite key above every survivor's
       // (|mu'| < 1e30, sigma < 1e30), so it never wins and never hides a survivor's key
       float2 v = make_float2(3.0e38f, 0.0f);                // (every survivor ran at least twice)
@@ -227,7 +228,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
         const PhiloxPrefix pre = philox_prefix((uint32_t)t, tlo, thi, k0f, k1f);
 #endif
         uint32_t qm = quads;
-        while (qm) {                                        // same trip count across the warp
+        while (qm) {                                        // the same trip count in a warp
           const int qd = __ffs(qm) - 1;
           qm &= qm - 1u;
 #if ZS_PHILOX_PREFIX
@@ -237,13 +238,11 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
 #endif
           float z0, z1, rsq;
           const float4 m0 = s_f[(2 * qd) * TPB + tid];
+          const float4 m1 = s_f[(2 * qd + 1) * TPB + tid];
           cert::normal_pair32(x.x, x.y, z0, z1, rsq);
           am.pair(4 * qd, m0, z0, z1, rsq, keep);
-          if (2 * qd + 1 < npairs) {
-            const float4 m1 = s_f[(2 * qd + 1) * TPB + tid];
-            cert::normal_pair32(x.z, x.w, z0, z1, rsq);
-            am.pair(4 * qd + 2, m1, z0, z1, rsq, keep);
-          }
+          cert::normal_pair32(x.z, x.w, z0, z1, rsq);
+          am.pair(4 * qd + 2, m1, z0, z1, rsq, keep);
         }
         b = am.arg(keep);
         if (am.certified(c_trial, kth) && !a.force_exact) {
@@ -367,13 +366,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   // counters: the method's events (as replay_kernel), then the work: [9] fp64 transforms
   // (fallback draws), [10] Philox blocks, [11] fp32 pairs, [12] certified, [13] fallbacks
   unsigned long long fall_pairs = (unsigned long long)n_fall * __popc(ts_pairs);
-  unsigned long long fp32_pairs = 0;
-  {
-    uint32_t qm = quads;
-    int np = 0;
-    while (qm) { const int qd = __ffs(qm) - 1; qm &= qm - 1u; np += (2 * qd + 1 < npairs) ? 2 : 1; }
-    fp32_pairs = (unsigned long long)n_sampled * np;
-  }
+  const unsigned long long fp32_pairs = (unsigned long long)n_sampled * 2 * __popc(quads);
   const unsigned long long blocks_fp32 = (unsigned long long)n_sampled * __popc(quads);
   const unsigned long long blocks_fall = (unsigned long long)n_fall * __popc(quads);
   uint32_t n_prune = 0;

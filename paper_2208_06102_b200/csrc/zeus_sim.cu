@@ -791,7 +791,7 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     a.force_exact = s->draw == 2 ? 1 : 0;
     auto thompson_launch = [&]() {
       const dim3 tgrid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
-      const size_t tsmem = (size_t)s->tab_bytes + (size_t)128 * (((s->B + 1) / 2) * 16);
+      const size_t tsmem = (size_t)s->tab_bytes + (size_t)128 * (((((s->B + 1) / 2) + 1) & ~1) * 16);
       if (rk) {
         if (s->log_mode) zs::thompson_kernel<true, true><<<tgrid, 128, tsmem, st>>>(a);
         else zs::thompson_kernel<false, true><<<tgrid, 128, tsmem, st>>>(a);

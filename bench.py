@@ -150,14 +150,18 @@ def method_work(counters):
 
 
 def evaluated_work(counters):
-    """The work this kernel evaluated: only the Box-Muller transforms the bound screen could not
-    rule out ([9]), the Philox blocks drawn ([10]) and the pairs screened ([11])."""
+    """The work this build evaluated for the same events: the fp64 Box-Muller transforms it
+    performed ([9]), the Philox blocks it drew ([10]), and [11] either the pairs the bound screen
+    handled or -- when the Thompson phase ran the certified draw ([12] + [13] > 0,
+    §7.9) -- the pairs transformed in fp32 with their bound and packed-key argmin update."""
     wm = _work_model()
     c = [int(x) for x in counters]
     dec, pairs, normals = c[0], c[2], c[3]
-    bm_done, blocks_done, screened = c[9], c[10], c[11]
+    bm_done, blocks_done, handled = c[9], c[10], c[11]
+    certified = len(c) > 13 and c[12] + c[13] > 0
+    per_pair = wm["fpair"] if certified else wm["screen"]
     used = normals * bm_done / max(1, pairs)
-    return {k: bm_done * wm["bm"][k] + blocks_done * wm["philox"][k] + screened * wm["screen"][k]
+    return {k: bm_done * wm["bm"][k] + blocks_done * wm["philox"][k] + handled * per_pair[k]
             + used * wm["theta"][k] + dec * (wm["serial"][k] + wm["philox"][k] / 4.0 + wm["curves"][k])
             for k in PIPES}
 
@@ -198,7 +202,7 @@ def cpu_sample(job, seconds, threads):
     from oracle import oracle as O
 
     w, c, R = job.workload, job.cells[0], job.recurrences
-    n = max(threads, 64)
+    n = max(threads, 16)
     while True:
         t0 = time.perf_counter()
         O.replay(w, c, R, np.arange(n), threads=threads, curves=True)
@@ -206,6 +210,45 @@ def cpu_sample(job, seconds, threads):
         if dt >= seconds or n >= job.trials:
             return n, dt
         n = min(job.trials, int(n * max(2.0, min(10.0, 1.2 * seconds / max(dt, 1e-3)))))
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(args, jobs, seconds):
+    """the oracle as it stands on the host's cores.  The whole workload (every job,
+    cell and trial) when it takes at most ~2 * `seconds` on all threads, else a bounded prefix of
+    the first cell's trials; plus the 1-thread rate on a small prefix and the CPU model."""
+    from oracle import oracle as O
+
+    threads = os.cpu_count() or 1
+    job = jobs[0]
+    n, dt = cpu_sample(job, min(seconds, 4.0), threads)            # rate estimate
+    rate = n * job.recurrences / dt
+    total = sum(len(jb.cells) * jb.trials * jb.recurrences for jb in jobs)
+    if total / rate <= 2.0 * seconds:
+        t0 = time.perf_counter()
+        for jb in jobs:
+            for c in jb.cells:
+                O.replay(jb.workload, c, jb.recurrences, np.arange(jb.trials), threads=threads, curves=True)
+        dt = time.perf_counter() - t0
+        value, sample, full = total / dt, f"the whole {args.config} workload ({total:.3g} decisions), {dt:.1f} s", True
+    else:
+        n, dt = cpu_sample(job, seconds, threads)
+        value, full = n * job.recurrences / dt, False
+        sample = (f"first {n} of {job.trials} trials x {job.recurrences} recurrences of {args.config} "
+                  f"({job.workload['name']}, cell 0), {dt:.1f} s")
+    n1, dt1 = cpu_sample(job, min(3.0, seconds / 4), 1)
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+            "full_workload": full, "value_1thread": n1 * job.recurrences / dt1,
+            "sample_1thread": f"first {n1} trials of cell 0, {dt1:.1f} s on 1 thread", "cpu_model": cpu_model()}
 
 
 def reference_main(args, rank, world):
@@ -234,7 +277,7 @@ def reference_main(args, rank, world):
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args, job, 1),
             "cpu_baseline": {"value": dps, "unit": UNIT, "cores": threads, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": dps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -443,12 +486,7 @@ def main():
                 "replay_ms_per_step": replay_total / args.steps, "jobs": len(jobs),
                 "counters_per_step": [int(x) for x in counters]}
         if world == 1 and not args.no_cpu_baseline:
-            threads = os.cpu_count() or 1
-            n, dt = cpu_sample(job, args.cpu_seconds, threads)
-            line["cpu_baseline"] = {"value": n * job.recurrences / dt, "unit": UNIT, "cores": threads,
-                                    "kind": "oracle",
-                                    "sample": f"first {n} trials x {job.recurrences} recurrences of "
-                                              f"{args.config}, {dt:.1f} s on {threads} threads"}
+            line["cpu_baseline"] = cpu_baseline(args, jobs, args.cpu_seconds)
         print(json.dumps(line), flush=True)
     for sm in sims:
         sm.close()

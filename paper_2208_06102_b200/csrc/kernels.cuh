@@ -1198,6 +1198,7 @@ __global__ void bucket_scatter_kernel(const CellParam *cells, const Carry *carry
 // best-known batch size; at most kMaxOutstanding runs per trial are in flight (R-Q31).
 // One thread per trial, one pass, tables read through the read-only cache.
 constexpr int kMaxOutstanding = 8;
+constexpr int kQueueBytes = kMaxOutstanding * (8 + 8 + 4 + 4 + 4);   // per thread, concurrent_kernel
 
 struct ConcArgs {
   const CellParam *cells;
@@ -1261,19 +1262,28 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
   unsigned long long dig = 0xcbf29ce484222325ull;
   int nstop = 0, last_b = -1;
   uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
-  // outstanding runs
-  double q_done[kMaxOutstanding], q_C[kMaxOutstanding];
-  int q_seq[kMaxOutstanding], q_b[kMaxOutstanding];
-  uint32_t q_flags[kMaxOutstanding];                         // bit0 converged, bit1 walk
+  // outstanding runs: a queue of kMaxOutstanding entries per trial in shared memory, after the
+  // (mu, sigma) table, each field [slot][thread] (conflict-free; dynamically indexed, so registers
+  // would put it on the local-memory stack)
+  double *const q_done_s = reinterpret_cast<double *>(smem + (size_t)((B + 1) & ~1) * 16 * TPB);
+  double *const q_C_s = q_done_s + kMaxOutstanding * TPB;
+  int *const q_seq_s = reinterpret_cast<int *>(q_C_s + kMaxOutstanding * TPB);
+  int *const q_b_s = q_seq_s + kMaxOutstanding * TPB;
+  uint32_t *const q_flags_s = reinterpret_cast<uint32_t *>(q_b_s + kMaxOutstanding * TPB);
+  auto q_done = [&](int i) -> double & { return q_done_s[i * TPB + tid]; };
+  auto q_C = [&](int i) -> double & { return q_C_s[i * TPB + tid]; };
+  auto q_seq = [&](int i) -> int & { return q_seq_s[i * TPB + tid]; };
+  auto q_b = [&](int i) -> int & { return q_b_s[i * TPB + tid]; };
+  auto q_flags = [&](int i) -> uint32_t & { return q_flags_s[i * TPB + tid]; };   // bit0 converged, bit1 walk
   int nq = 0;
 
   ArmStat qc{0.0, 0.0, 0.0, 0, 0};                     // the last arm's record (read cache)
   int qc_b = -1;
   // a run's outcome reaching the optimiser
   auto complete = [&](int i) {
-    const int b = q_b[i];
-    const double C = q_C[i];
-    const bool conv = q_flags[i] & 1u, walk = q_flags[i] & 2u;
+    const int b = q_b(i);
+    const double C = q_C(i);
+    const bool conv = q_flags(i) & 1u, walk = q_flags(i) & 2u;
     if (conv && !(C >= best)) { best = C; best_arm = b; }
     {                                                        // Alg. 2 Observe (NC-6)
       const bool was_seen = (seen >> b) & 1u;
@@ -1344,11 +1354,11 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
   auto complete_earliest = [&]() {                          // by (completion, submission)
     int e = 0;
     for (int i = 1; i < nq; ++i)
-      if (q_done[i] < q_done[e] || (q_done[i] == q_done[e] && q_seq[i] < q_seq[e])) e = i;
+      if (q_done(i) < q_done(e) || (q_done(i) == q_done(e) && q_seq(i) < q_seq(e))) e = i;
     complete(e);
     --nq;                                                    // move the last entry into slot e
-    q_done[e] = q_done[nq]; q_C[e] = q_C[nq]; q_seq[e] = q_seq[nq]; q_b[e] = q_b[nq];
-    q_flags[e] = q_flags[nq];
+    q_done(e) = q_done(nq); q_C(e) = q_C(nq); q_seq(e) = q_seq(nq); q_b(e) = q_b(nq);
+    q_flags(e) = q_flags(nq);
   };
 
   int s = 0;
@@ -1362,7 +1372,7 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
       const double tau = __ldg(arr + t);
       for (;;) {                                             // runs finished by this submission
         bool any = false;
-        for (int i = 0; i < nq; ++i) any |= q_done[i] <= tau;
+        for (int i = 0; i < nq; ++i) any |= q_done(i) <= tau;
         if (!any) break;
         complete_earliest();
       }
@@ -1447,8 +1457,8 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
         En = e0 + em1 * ac.e1;
       }
       const bool conv = (E > 0) && !stopped;
-      q_done[nq] = tau + Tm; q_C[nq] = C; q_seq[nq] = t; q_b[nq] = b;
-      q_flags[nq] = (conv ? 1u : 0u) | (walk_issue ? 2u : 0u);
+      q_done(nq) = tau + Tm; q_C(nq) = C; q_seq(nq) = t; q_b(nq) = b;
+      q_flags(nq) = (conv ? 1u : 0u) | (walk_issue ? 2u : 0u);
       ++nq;
       const uint32_t flags = (stopped ? 1u : 0u) | (conv ? 2u : 0u) | (prof_now ? 4u : 0u) |
                              (ts_dec ? 8u : 0u);

@@ -365,15 +365,17 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   }
   // counters: the method's events (as replay_kernel), then the work: [9] fp64 transforms
   // (fallback draws), [10] Philox blocks, [11] fp32 pairs, [12] certified, [13] fallbacks
-  unsigned long long fall_pairs = (unsigned long long)n_fall * __popc(ts_pairs);
+  // (phase A's Thompson draws, carried in n_sampled, are full fp64 draws: counted in [9], [10])
   const unsigned long long fp32_pairs = (unsigned long long)n_sampled * 2 * __popc(quads);
-  const unsigned long long blocks_fp32 = (unsigned long long)n_sampled * __popc(quads);
-  const unsigned long long blocks_fall = (unsigned long long)n_fall * __popc(quads);
-  uint32_t n_prune = 0;
+  uint32_t n_prune = 0, n_full = n_fall;
   if (active) {
     const Carry c = a.carry[o];
+    n_full += c.n_sampled;
     n_sampled += c.n_sampled; n_prune = c.n_prune; n_forced += c.n_forced; n_recomp += c.n_recomp;
   }
+  const unsigned long long fall_pairs = (unsigned long long)n_full * __popc(ts_pairs);
+  const unsigned long long blocks_fp32 = (unsigned long long)(n_sampled - n_full + n_fall) * __popc(quads);
+  const unsigned long long blocks_fall = (unsigned long long)n_full * __popc(quads);
   const unsigned long long pairs_all = (unsigned long long)n_sampled * __popc(ts_pairs);
   const unsigned long long blocks_all = (unsigned long long)n_sampled * __popc(quads);
   unsigned long long ctr[kCounters] = {

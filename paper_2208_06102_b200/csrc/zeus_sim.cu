@@ -6,6 +6,7 @@
 // D2H of the results.  There is no CPU compute path: without a usable CUDA
 // device every call that would launch work fails with ZEUS_E_CUDA.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -39,6 +40,13 @@ struct DevBuf {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
+
+// NVTX range around each C-ABI call (visible in nsys / ncu timelines; the header-only
+// NVTX3 API is a no-op unless a tool injects itself)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct zeus_sim {
   // job
@@ -293,6 +301,7 @@ const char *zeus_sim_last_error(const zeus_sim *sim) {
 
 zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t num_cells,
                             const zeus_run_opts *opts, int32_t cuda_device, zeus_sim **out) {
+  NvtxRange nvtx_("zeus_sim_create");
   g_create_error.clear();
   if (!out) return fail(nullptr, ZEUS_E_INVALID, "out is NULL");
   *out = nullptr;
@@ -451,6 +460,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
 
 zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th, int32_t S,
                                   int32_t K, const int32_t *pool) {
+  NvtxRange nvtx_("zeus_sim_load_profile");
   if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
   s->err.clear();
   const std::vector<uintptr_t> sig0 = s->launch_signature();
@@ -714,9 +724,10 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     c.MP = s->MP;
     const size_t smem = (size_t)128 * (((s->B + 1) & ~1) * 16);
     const dim3 grid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
-    if (s->any_conc) {
-      if (s->log_mode) zs::concurrent_kernel<true><<<grid, 128, smem, st>>>(c);
-      else zs::concurrent_kernel<false><<<grid, 128, smem, st>>>(c);
+    if (s->any_conc) {                      // + the outstanding-run queues (kernels.cuh)
+      const size_t csmem = smem + (size_t)128 * zs::kQueueBytes;
+      if (s->log_mode) zs::concurrent_kernel<true><<<grid, 128, csmem, st>>>(c);
+      else zs::concurrent_kernel<false><<<grid, 128, csmem, st>>>(c);
       ZS_CUDA(s, cudaGetLastError());
       s->launches += 1;
     }
@@ -850,6 +861,7 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
 }
 
 zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
+  NvtxRange nvtx_("zeus_sim_run");
   if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
   s->err.clear();
   if (!s->loaded) return fail(s, ZEUS_E_STATE, "zeus_sim_run before zeus_sim_load_profile");
@@ -882,6 +894,7 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
 }
 
 zeus_status zeus_sim_results(zeus_sim *s, zeus_results *out) {
+  NvtxRange nvtx_("zeus_sim_results");
   if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
   s->err.clear();
   if (!out) return fail(s, ZEUS_E_INVALID, "out is NULL");
@@ -982,6 +995,7 @@ zeus_status zeus_sim_results(zeus_sim *s, zeus_results *out) {
 }
 
 zeus_status zeus_sim_curves_from_fixed(zeus_sim *s, const int64_t *curves_fixed, double *curves) {
+  NvtxRange nvtx_("zeus_sim_curves_from_fixed");
   if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
   s->err.clear();
   if (!curves_fixed || !curves) return fail(s, ZEUS_E_INVALID, "curves_fixed / curves is NULL");

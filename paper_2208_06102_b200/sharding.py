@@ -28,8 +28,14 @@ def reduce_curves(curves_fixed, group=None):
     (zeus_results.curves_fixed).  Integer addition is exact and associative, so the sum has the
     same bits for any world size and any reduction order; the library then rounds it once to
     fp64 curves (zeus_sim_curves_from_fixed), giving N ranks the bits of one."""
+    import torch
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        nvtx = torch.cuda.nvtx if curves_fixed.is_cuda else None   # NVTX range (SURVEY §5)
+        if nvtx:
+            nvtx.range_push("zeus_reduce_curves")
         dist.all_reduce(curves_fixed, op=dist.ReduceOp.SUM, group=group)
+        if nvtx:
+            nvtx.range_pop()
     return curves_fixed

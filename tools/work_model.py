@@ -55,7 +55,7 @@ def main():
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "--fmad=false",
                            "-cubin", "-o", cubin, os.path.join(HERE, "work_probe.cu")])
     names = ["philox", "zlog", "sincospi", "sqrt", "div", "bm", "pair", "theta", "observe", "charge",
-             "serial", "curves", "screen"]
+             "serial", "curves", "screen", "philox_q", "fpair"]
     model = {n: classify(sass(cubin, f"probe_{n}")) for n in names}
     model["_doc"] = ("lane-instructions per primitive on sm_100a (nvcc 12.9, -O3 --fmad=false), main "
                      "path from tools/work_probe.cu; fp64 = FP64-unit ops (DFMA/DADD/DMUL/DSETP/MUFU.*64H/"

@@ -1,7 +1,7 @@
 // work_probe.cu -- per-primitive SASS instruction counts of the contract functions
 // (compiled, never run): each probe kernel wraps ONE primitive between a load and a
 // store so `tools/work_model.py` can count its straight-line instructions by pipe.
-#include "../paper_2208_06102_b200/csrc/kernels.cuh"
+#include "../paper_2208_06102_b200/csrc/thompson.cuh"
 using namespace zs;
 extern "C" __global__ void probe_empty(const double *in, double *out) {
   out[threadIdx.x] = in[threadIdx.x];
@@ -100,9 +100,28 @@ extern "C" __global__ void probe_serial(const double *in, const int *pool, const
   out[0] = C + in[11]; out[1] = En + in[12]; out[2] = Tm + in[13];
   out[3] = tab[s * B + b]; out[4] = best; out[5] = ms.x; out[6] = ms.y; out[7] = S1; out[8] = S2;
 }
-// One warp's per-recurrence curve reduction (executed once per warp-recurrence = 32 decisions)
+// The method's curve accumulation (a7: Eq. 4 sums per recurrence), as one warp's fp64
+// reduce-scatter of the four sums (12 shuffles), one REDUX of the packed counts and one 4-lane
+// RED.F64 + one count RED per warp-recurrence (32 decisions).  This is the algorithmic work;
+// the build's exact fixed-point curves (counted runs + limbs for stops) are an implementation.
 extern "C" __global__ void probe_curves(double *curves, const double *v, const int *pk, int t) {
-  curve_accumulate(curves, t, threadIdx.x & 31, v[0], v[1], v[2], v[3], pk[0]);
+  const int lane = threadIdx.x & 31;
+  double a0 = v[0], a1 = v[1], a2 = v[2], a3 = v[3];
+  // reduce-scatter: after 16/8 the four quantities live in lanes 0, 8, 16, 24
+  const bool hi16 = lane & 16;
+  double x0 = hi16 ? a0 : a2, x1 = hi16 ? a1 : a3;
+  double y0 = hi16 ? a2 : a0, y1 = hi16 ? a3 : a1;
+  y0 += __shfl_xor_sync(0xffffffffu, x0, 16);
+  y1 += __shfl_xor_sync(0xffffffffu, x1, 16);
+  const bool hi8 = lane & 8;
+  double x = hi8 ? y0 : y1, y = hi8 ? y1 : y0;
+  y += __shfl_xor_sync(0xffffffffu, x, 8);
+  y += __shfl_xor_sync(0xffffffffu, y, 4);
+  y += __shfl_xor_sync(0xffffffffu, y, 2);
+  y += __shfl_xor_sync(0xffffffffu, y, 1);
+  const unsigned c = __reduce_add_sync(0xffffffffu, (unsigned)pk[0]);
+  if ((lane & 7) == 0) atomicAdd(curves + t * 8 + (lane >> 3), y);
+  if (lane == 0) atomicAdd((unsigned long long *)(curves + t * 8 + 4), (unsigned long long)c);
 }
 // Bound screen of one survivor pair: radius bound from the radius word, the
 // rounded-down lower bounds of both arms against bt, and parking a residual pair's words
@@ -113,4 +132,22 @@ extern "C" __global__ void probe_screen(const uint32_t *w, const double2 *ms, co
     park[threadIdx.x] = make_uint4(w[0], w[1], w[3], 0u);
     nres[0] += 1;
   }
+}
+
+// Certified draw: one Philox block of a quad from the per-decision prefix
+// (rounds 0-2 partly shared), as the Thompson kernel draws it
+extern "C" __global__ void probe_philox_q(const uint32_t *in, uint32_t *out) {
+  const PhiloxPrefix p{in[0], in[1], in[2], in[3], in[4]};
+  const U4 x = philox_from_prefix(p, in[5], [&](int r) { return in[6] + (uint32_t)r; },
+                                  [&](int r) { return in[7] + (uint32_t)r; });
+  out[0] = x.x; out[1] = x.y; out[2] = x.z; out[3] = x.w;
+}
+// ... one Box-Muller pair in fp32 with its bound and the packed-key argmin update of its two arms
+extern "C" __global__ void probe_fpair(const uint32_t *w, const float4 *ms, float *io, uint32_t keep) {
+  cert::Argmin32 am;
+  am.m1 = io[0]; am.m2 = io[1]; am.smax = io[2]; am.rsqmax = io[3];
+  float z0, z1, rsq;
+  cert::normal_pair32(w[0], w[1], z0, z1, rsq);
+  am.pair((int)w[2], ms[0], z0, z1, rsq, keep);
+  io[0] = am.m1; io[1] = am.m2; io[2] = am.smax; io[3] = am.rsqmax;
 }

@@ -269,7 +269,9 @@ zeus_status zeus_sim_shape(const zeus_sim *sim, int32_t *recurrences, int64_t *s
  *   out[1] = max r32                                          (must be <= out[5]),
  *   out[2] = max over angle words b of |cos32 - cos|, out[3] of |sin32 - sin| (<= out[4]),
  *   out[4] = the angle bound compiled into the kernels, out[5] = the radius cap,
- * where r, cos, sin are the contract's fp64 values (NC-3).  out: host, 6 doubles.
+ *   out[6] = max over out[7] seeded random (words, mu, sigma, ref) of |key - (theta - ref)| / E,
+ *            the composed per-arm bound of the certified argmin (holds iff <= 1),
+ * where r, cos, sin, theta are the contract's fp64 values (NC-3, NC-4).  out: host, 8 doubles.
  * Returns ZEUS_OK, ZEUS_E_INVALID (out NULL) or ZEUS_E_CUDA.  About 0.1 s on a B200. */
 zeus_status zeus_sim_certify_bounds(int32_t cuda_device, double *out);
 

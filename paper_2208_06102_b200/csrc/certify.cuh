@@ -165,5 +165,58 @@ __global__ void certify_angle_kernel(uint64_t begin, uint64_t n, unsigned *out) 
   atomicMax(out + 3, __float_as_uint(ws));
 }
 
+// [4] max over random (a, b, mu, sigma, ref) of |key~ - (theta - ref)| / E: the composed per-arm
+// bound of Argmin32 (|key - theta'| <= sigma32 kSigScale (e_z + kSig) + kth |key| + c_trial at
+// the widest key packing, 5 index bits) against the contract's theta = fma(sigma, z, mu) with
+// the contract's fp64 normal z (NC-3/NC-4); an empirical check of the analytic composition
+// over the regimes the replay meets: ref 1 .. 1e6, |mu - ref| / ref up to 1/2,
+// sigma / mu 1e-7 .. 0.3
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__global__ void certify_theta_kernel(const double2 *logtab, uint64_t begin, uint64_t n, unsigned *out) {
+  __shared__ double2 tab[kLogTab];
+  for (int i = threadIdx.x; i < kLogTab; i += blockDim.x) tab[i] = logtab[i];
+  __syncthreads();
+  const uint32_t keep = ~31u;
+  const float kth = kTheta + 0x1p-18f * 1.000001f;
+  float worst = 0.0f;
+  for (uint64_t i = begin + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < begin + n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t h0 = splitmix64(2 * i), h1 = splitmix64(2 * i + 1);
+    const uint32_t a = (uint32_t)h0, b = (uint32_t)(h0 >> 32);
+    const double u0 = (double)(h1 & 0xfffff) * 0x1p-20, u1 = (double)((h1 >> 20) & 0xfffff) * 0x1p-20;
+    const double u2 = (double)(h1 >> 40) * 0x1p-24;
+    const double ref = exp10(6.0 * u0);
+    const double mu = ref * (1.0 + (u1 - 0.5) * exp10(-6.0 * u2));
+    const double sig = mu * exp10(-7.0 + 6.5 * u2 * u1);
+    double z0, z1;
+    box_muller(a, b, z0, z1, tab);                                     // the contract's normals
+    const float c_trial = __double2float_ru(fabs(ref) * 0x1p-52 + 0x1p-120);
+    float zf0, zf1, rsq;
+    normal_pair32(a, b, zf0, zf1, rsq);
+    const float ez = __fmaf_ru(rsq, kZb, kZr * kRMax * 1.000001f);
+    const float muf = (float)(mu - ref), sgf = (float)sig;
+    const float S = __fmaf_ru(__fmul_ru(sgf, kSigScale), __fadd_ru(ez, kSig), c_trial);
+#pragma unroll
+    for (int arm = 0; arm < 2; ++arm) {
+      const double th = fma(sig, arm ? z1 : z0, mu);                   // contract theta (NC-4)
+      const float t32 = fmaf(sgf, arm ? zf1 : zf0, muf);
+      const float key = __int_as_float((__float_as_int(t32) & (int)keep) | 31);
+      const float E = __fmaf_ru(kth, fabsf(key), S);
+      const double hi = th - ref, bb = hi - th;                          // two-sum of th - ref
+      const double lo = (th - (hi - bb)) + (-ref - bb);
+      const double d = fabs(((double)key - hi) - lo);
+      // S = +inf (a pair with r2 = 0: rsq = +inf) is never certified: nothing to check
+      const float q = (S == __int_as_float(0x7f800000)) ? 0.0f : (float)(d / (double)E) * 1.000001f;
+      worst = fmaxf(worst, (q == q) ? q : __int_as_float(0x7f800000));
+    }
+  }
+  atomicMax(out + 4, __float_as_uint(worst));
+}
+
 }  // namespace cert
 }  // namespace zs

@@ -22,6 +22,9 @@ namespace zs {
 #ifndef ZS_PHILOX_PREFIX
 #define ZS_PHILOX_PREFIX 1
 #endif
+#ifndef ZS_QUAD2
+#define ZS_QUAD2 1
+#endif
 #ifndef ZS_PHILOX_WIDE
 #define ZS_PHILOX_WIDE 1
 #endif
@@ -143,6 +146,9 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   // fp32 (mu - ref, sigma) of arms 2k, 2k+1 of this thread: float4 [pair][thread]
   float4 *s_f = reinterpret_cast<float4 *>(smem + a.tab_bytes);
   float2 *s_f2 = reinterpret_cast<float2 *>(s_f);         // arm b: s_f2[2 ((b >> 1) TPB + tid) + (b & 1)]
+  // the replica words of the current block of four recurrences (NC-3), [thread][4]: one LDS per
+  // decision instead of four live registers
+  uint32_t *s_rw = reinterpret_cast<uint32_t *>(smem + a.tab_bytes + (size_t)((((B + 1) >> 1) + 1) & ~1) * 16 * TPB);
 
   const bool active = j0 + tid < cp.n;
   const int64_t jj = active ? a.perm[cp.out_off + j0 + tid] : 0;
@@ -163,7 +169,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   unsigned long long dig = 0;
   uint32_t ts_set = 0, ts_pairs = 0, quads = 0;
   int nstop = 0, last_b = -1;
-  uint32_t n_sampled = 0, n_forced = 0, n_recomp = 0, n_cert = 0, n_fall = 0;
+  uint32_t n_fall = 0;              // exact fallbacks (every phase-B decision samples and observes)
   double ref = 0.0;
   float c_trial = 0.0f;
   const int npairs = (B + 1) >> 1;
@@ -204,7 +210,6 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   }
 
   int s = 0;
-  U4 rw{0u, 0u, 0u, 0u};
   ArmStat qc{0.0, 0.0, 0.0, 0, 0};
   int qc_b = -1;
 #if ZS_PHILOX_PREFIX
@@ -217,7 +222,10 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
     if (S > 1)
       while ((long long)(s + 1) * R <= (long long)t * S) ++s;
     if (active) {
-      if ((t & 3) == 0 || t == a.t_split) rw = replica_words_c(trial, t);
+      if ((t & 3) == 0 || t == a.t_split) {
+        const U4 rw = replica_words_c(trial, t);
+        reinterpret_cast<uint4 *>(s_rw)[tid] = make_uint4(rw.x, rw.y, rw.z, rw.w);
+      }
       // ---------------- step 2: Alg. 1, b = argmin_a theta_a over the survivors
       const uint32_t unripe = 0u;   // every Thompson-phase arm has n >= 2 (run twice in pruning)
       (void)unripe;
@@ -227,15 +235,14 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
 #if ZS_PHILOX_PREFIX
         const PhiloxPrefix pre = philox_prefix((uint32_t)t, tlo, thi, k0f, k1f);
 #endif
-        uint32_t qm = quads;
-        while (qm) {                                        // the same trip count in a warp
-          const int qd = __ffs(qm) - 1;
-          qm &= qm - 1u;
+        auto quad_block = [&](int qd) -> U4 {
 #if ZS_PHILOX_PREFIX
-          const U4 x = philox_from_prefix(pre, (uint32_t)qd, k0f, k1f);
+          return philox_from_prefix(pre, (uint32_t)qd, k0f, k1f);
 #else
-          const U4 x = block_c(trial, t, qd);
+          return block_c(trial, t, qd);
 #endif
+        };
+        auto quad_argmin = [&](int qd, const U4 &x) {
           float z0, z1, rsq;
           const float4 m0 = s_f[(2 * qd) * TPB + tid];
           const float4 m1 = s_f[(2 * qd + 1) * TPB + tid];
@@ -243,11 +250,25 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
           am.pair(4 * qd, m0, z0, z1, rsq, keep);
           cert::normal_pair32(x.z, x.w, z0, z1, rsq);
           am.pair(4 * qd + 2, m1, z0, z1, rsq, keep);
+        };
+        uint32_t qm = quads;
+        while (qm) {                                        // the same trip count in a warp
+          const int qa = __ffs(qm) - 1;
+          qm &= qm - 1u;
+#if ZS_QUAD2
+          if (qm) {                                         // two quads: two independent Philox
+            const int qb = __ffs(qm) - 1;                   // chains in one basic block
+            qm &= qm - 1u;
+            const U4 xa = quad_block(qa), xb = quad_block(qb);
+            quad_argmin(qa, xa);
+            quad_argmin(qb, xb);
+            continue;
+          }
+#endif
+          quad_argmin(qa, quad_block(qa));
         }
         b = am.arg(keep);
-        if (am.certified(c_trial, kth) && !a.force_exact) {
-          n_cert += 1;
-        } else {
+        if (!am.certified(c_trial, kth) || a.force_exact) {
           // the contract's exact draw (NC-3/NC-4): fp64 posteriors from the Observe records
           // (the cached record is the newest of its arm), every survivor pair transformed,
           // strict < in ascending arm order
@@ -277,7 +298,6 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
             }
           }
         }
-        n_sampled += 1;
       }
       // Observe record of arm b (write-back cache)
       if (b != qc_b) {
@@ -289,7 +309,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
       const int p = ac.pstar;
       const double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;
       // ---------------- step 3: replay one recorded run
-      const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
+      const uint32_t r = __umulhi(s_rw[4 * tid + (t & 3)], (uint32_t)K);
       const int E = pool[((size_t)s * B + b) * K + r];
       const int Erun = E > 0 ? E : a.max_epochs;
       hkey = b * K + (int)r;                               // bin (b, replica) of the row
@@ -335,7 +355,9 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
     }
     {
       const bool special = active && (vPacked & 1);
+#ifndef ZS_DIAG_NOHIST
       if (active && !special) red_add_u32(hrow + hkey, 1u);
+#endif
       hrow += hstride;
       if (__any_sync(0xffffffffu, special))
         curve_accumulate(curves, t, tid & 31, special ? vC : 0.0, special ? vE : 0.0, special ? vT : 0.0,
@@ -351,7 +373,6 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
       const double dm = ms.x - ref;
       s_f2[2 * ((b >> 1) * TPB + tid) + (b & 1)] =
           (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y) : make_float2(0.0f, kInfF);
-      n_recomp += 1;
     }
   }
   if (active && qc_b >= 0) st[qc_b] = qc;
@@ -366,15 +387,17 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   // counters: the method's events (as replay_kernel), then the work: [9] fp64 transforms
   // (fallback draws), [10] Philox blocks, [11] fp32 pairs, [12] certified, [13] fallbacks
   // (phase A's Thompson draws, carried in n_sampled, are full fp64 draws: counted in [9], [10])
-  const unsigned long long fp32_pairs = (unsigned long long)n_sampled * 2 * __popc(quads);
-  uint32_t n_prune = 0, n_full = n_fall;
+  const uint32_t nB = active ? (uint32_t)(R - a.t_split) : 0u;   // phase-B decisions = draws
+  const uint32_t n_cert = nB - n_fall;
+  const unsigned long long fp32_pairs = (unsigned long long)nB * 2 * __popc(quads);
+  uint32_t n_sampled = nB, n_prune = 0, n_forced = 0, n_recomp = nB, n_full = n_fall;
   if (active) {
     const Carry c = a.carry[o];
     n_full += c.n_sampled;
-    n_sampled += c.n_sampled; n_prune = c.n_prune; n_forced += c.n_forced; n_recomp += c.n_recomp;
+    n_sampled += c.n_sampled; n_prune = c.n_prune; n_forced = c.n_forced; n_recomp += c.n_recomp;
   }
   const unsigned long long fall_pairs = (unsigned long long)n_full * __popc(ts_pairs);
-  const unsigned long long blocks_fp32 = (unsigned long long)(n_sampled - n_full + n_fall) * __popc(quads);
+  const unsigned long long blocks_fp32 = (unsigned long long)nB * __popc(quads);
   const unsigned long long blocks_fall = (unsigned long long)n_full * __popc(quads);
   const unsigned long long pairs_all = (unsigned long long)n_sampled * __popc(ts_pairs);
   const unsigned long long blocks_all = (unsigned long long)n_sampled * __popc(quads);

@@ -529,7 +529,10 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
     ZS_CUDA(s, s->d_pareto.alloc((size_t)S * B * P));
     // counted curves: [cells][R][nhslot][4][B][K] u32, up to 16 slot copies within 64 MB
     const size_t per_slot = (size_t)nc * s->R * 4 * B * K * 4;
-    s->nhslot = (int)std::max<size_t>(1, std::min<size_t>(16, (64ull << 20) / std::max<size_t>(1, per_slot)));
+#ifndef ZS_HSLOT_MAX
+#define ZS_HSLOT_MAX 16
+#endif
+    s->nhslot = (int)std::max<size_t>(1, std::min<size_t>(ZS_HSLOT_MAX, (ZS_HSLOT_MAX * 4ull << 20) / std::max<size_t>(1, per_slot)));
     ZS_CUDA(s, s->d_hist.alloc(per_slot * s->nhslot));
   }
   // Stage the caller's arrays in pinned memory (read before this call returns), then copy them
@@ -802,7 +805,7 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     a.force_exact = s->draw == 2 ? 1 : 0;
     auto thompson_launch = [&]() {
       const dim3 tgrid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
-      const size_t tsmem = (size_t)s->tab_bytes + (size_t)128 * (((((s->B + 1) / 2) + 1) & ~1) * 16);
+      const size_t tsmem = (size_t)s->tab_bytes + (size_t)128 * (((((s->B + 1) / 2) + 1) & ~1) * 16 + 16);
       if (rk) {
         if (s->log_mode) zs::thompson_kernel<true, true><<<tgrid, 128, tsmem, st>>>(a);
         else zs::thompson_kernel<false, true><<<tgrid, 128, tsmem, st>>>(a);
@@ -1042,8 +1045,8 @@ zeus_status zeus_sim_certify_bounds(int32_t cuda_device, double *out) {
   unsigned *d_out = nullptr;
   cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaMalloc(&tab, zs::kLogTab * sizeof(double2));
-  if (e == cudaSuccess) e = cudaMalloc(&d_out, 4 * sizeof(unsigned));
-  if (e == cudaSuccess) e = cudaMemsetAsync(d_out, 0, 4 * sizeof(unsigned), st);
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, 5 * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_out, 0, 5 * sizeof(unsigned), st);
   if (e == cudaSuccess) {
     zs::log_table_kernel<<<1, 128, 0, st>>>(tab);
     int sms = 148;
@@ -1053,9 +1056,10 @@ zeus_status zeus_sim_certify_bounds(int32_t cuda_device, double *out) {
       zs::cert::certify_radius_kernel<<<sms * 8, 256, 0, st>>>(tab, b, chunk, d_out);
       zs::cert::certify_angle_kernel<<<sms * 8, 256, 0, st>>>(b, chunk, d_out);
     }
+    zs::cert::certify_theta_kernel<<<sms * 8, 256, 0, st>>>(tab, 0, 1ull << 28, d_out);
     e = cudaGetLastError();
   }
-  unsigned h[4] = {0, 0, 0, 0};
+  unsigned h[5] = {0, 0, 0, 0, 0};
   if (e == cudaSuccess) e = cudaMemcpyAsync(h, d_out, sizeof(h), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (tab) cudaFree(tab);
@@ -1069,6 +1073,10 @@ zeus_status zeus_sim_certify_bounds(int32_t cuda_device, double *out) {
   }
   out[4] = zs::cert::kAng;
   out[5] = zs::cert::kRMax;
+  float f4;
+  std::memcpy(&f4, &h[4], 4);
+  out[6] = f4;
+  out[7] = (double)(1ull << 28);
   return ZEUS_OK;
 }
 

@@ -132,8 +132,8 @@ def zeus_sim_curves_from_fixed(h, curves_fixed, curves):
 
 
 def zeus_sim_certify_bounds(cuda_device: int = 0):
-    """Exhaustive check of the certified draw's error bounds (include/zeus_sim.h): 6 doubles."""
-    out = np.zeros(6)
+    """Exhaustive check of the certified draw's error bounds (include/zeus_sim.h): 8 doubles."""
+    out = np.zeros(8)
     _check(lib().zeus_sim_certify_bounds(int(cuda_device), _ptr(out)), None)
     return out
 

@@ -471,6 +471,8 @@ def test_certified_draw_bounds(zs):
     assert 6.66 < out[1] <= out[5]
     assert out[2] <= out[4] and out[3] <= out[4], out
     assert out[2] > 0.5 * out[4] and out[3] > 0.5 * out[4]      # the bound is measured, not loose
+    # the composed per-arm bound (argmin keys vs the contract's theta), 2^28 seeded samples
+    assert 0.0 < out[6] <= 1.0, f"theta bound exceeded: ratio {out[6]}"
 
 
 def test_certified_draw_multicell_and_drift(zs, oracle):

@@ -39,6 +39,13 @@ VARIANTS = {
     "th_nowide": (["ZS_PHILOX_WIDE=0"], []),
     "th_noprefix": (["ZS_PHILOX_PREFIX=0"], []),
     "th_mb6": (["ZS_TH_MIN_BLOCKS=6"], []),
+    "th_mb7": (["ZS_TH_MIN_BLOCKS=7"], []),
+    "th_q1": (["ZS_QUAD2=0"], []),
+    "hs4": (["ZS_HSLOT_MAX=4"], []),
+    "hs64": (["ZS_HSLOT_MAX=64"], []),
+    "diag_nohist": (["ZS_DIAG_NOHIST"], []),   # timing diagnostic only: curves wrong
+    "th_q2_mb5": (["ZS_TH_MIN_BLOCKS=5"], []),
+    "th_mb8": (["ZS_TH_MIN_BLOCKS=8"], []),
 }
 
 if __name__ == "__main__":

@@ -10,12 +10,14 @@ from paper_2208_06102_b200 import synth
 from paper_2208_06102_b200.zeus_sim import Simulation
 # one-cell (RK kernels, two phases), multi-cell, windowed one pass, lane groups, baselines,
 # ablations, variant readings, concurrent submissions
-runs = [("cfg5", 600, 0), ("cfg3", 300, 0), ("cfg4_38", 500, 0), ("cfg1", 100, 3), ("f1", 200, 0),
-        ("f2", 200, 0), ("f2v", 200, 0), ("f3", 200, 0)]
-for name, trials, layout in runs:
+# (draw 0: the certified Thompson kernel; 1: the exact-screen phase B; 2: certified, all fallbacks)
+runs = [("cfg5", 600, 0, 0), ("cfg5", 300, 2, 1), ("cfg5", 300, 2, 2), ("cfg3", 300, 0, 0),
+        ("cfg4_38", 500, 0, 0), ("cfg1", 100, 3, 0), ("f1", 200, 0, 0), ("f2", 200, 0, 0),
+        ("f2v", 200, 0, 0), ("f3", 200, 0, 0)]
+for name, trials, layout, draw in runs:
     for job in synth.config(name, trials=trials)[:2]:
         R = min(job.recurrences, 120)
-        sim = Simulation(job.workload, job.cells, job.trials, R, layout=layout).load_profile()
+        sim = Simulation(job.workload, job.cells, job.trials, R, layout=layout, draw=draw).load_profile()
         sim.run().results()
         sim.close()
     print("ok", name, flush=True)

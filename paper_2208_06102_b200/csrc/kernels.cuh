@@ -72,10 +72,14 @@ __global__ void step1_kernel(Step1Args a) {
     const double *Th = a.Th + (size_t)b * a.P;
     double bc = __longlong_as_double(0x7ff0000000000000ll);   // +inf
     int bp = 0x7fffffff;
+    // per-p terms of the JIT epoch (1/Th, A/Th), computed by the lanes; lane 0 adds them in
+    // ascending p below (NC-2: the same terms, the same left-to-right order)
+    double term_t = 0.0, term_e = 0.0;
     for (int p = lane; p < a.P; p += 32) {                      // Eq. 7, lanes over p
       const double num = (eta * A[p]) + ((1.0 - eta) * a.MP);
       const double c = num / Th[p];
       if (c < bc) { bc = c; bp = p; }
+      if (p < 32) { term_t = 1.0 / Th[p]; term_e = A[p] / Th[p]; }
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {                   // argmin, ties -> smaller p
@@ -83,17 +87,19 @@ __global__ void step1_kernel(Step1Args a) {
       const int op = __shfl_xor_sync(0xffffffffu, bp, off);
       if (oc < bc || (oc == bc && op < bp)) { bc = oc; bp = op; }
     }
+    double st = 0.0, se = 0.0;                                  // JIT epoch, left-to-right (NC-2)
+    for (int p = 0; p < a.P; ++p) {
+      const double tt = (p < 32) ? __shfl_sync(0xffffffffu, term_t, p) : 1.0 / Th[p];
+      const double te = (p < 32) ? __shfl_sync(0xffffffffu, term_e, p) : A[p] / Th[p];
+      st = st + tt;
+      se = se + te;
+    }
     if (lane == 0) {
       if (bp == 0x7fffffff) bp = 0;
       ArmConst ac;
       ac.c1 = bc;
       ac.t1 = 1.0 / Th[bp];
       ac.e1 = A[bp] / Th[bp];
-      double st = 0.0, se = 0.0;                                // JIT epoch, left-to-right (NC-2)
-      for (int p = 0; p < a.P; ++p) {
-        st = st + 1.0 / Th[p];
-        se = se + A[p] / Th[p];
-      }
       ac.tP = st / (double)a.P;
       ac.eP = se / (double)a.P;
       ac.cP = (eta * ac.eP) + (((1.0 - eta) * a.MP) * ac.tP);
@@ -105,6 +111,7 @@ __global__ void step1_kernel(Step1Args a) {
   }
   __syncthreads();
   for (int s = threadIdx.x; s < a.S; s += blockDim.x) {        // known optimum
+    // (pool reads are independent loads; the compiler keeps them in flight)
     double best = __longlong_as_double(0x7ff0000000000000ll);
     int barg = -1;
     for (int b = 0; b < a.B; ++b) {
@@ -1173,20 +1180,41 @@ __global__ void bucket_scan_kernel(int32_t *bucket, int ncells, int nwin) {
   }
 }
 
-// phase-B lane order: the trials of each window grouped by their survivor-pair count
-__global__ void bucket_scatter_kernel(const CellParam *cells, const Carry *carry, int32_t *bucket,
-                                      int32_t *perm, int ncells, int B, int nwin, int key_quads) {
+// phase-B lane order: the trials of each window grouped by their survivor-pair (or quad) count.
+// One 256-trial tile per block iteration (a tile never straddles a window): ranks within the tile
+// from shared-memory atomics, then one global atomic per non-empty bucket reserves the tile's
+// range -- at most kBuckets global atomics per tile instead of one per trial (the bucket counters
+// were the contended addresses).  The order within a bucket is free: trials are independent.
+constexpr int kScatterTile = 256;
+static_assert(kRegroupWindow % kScatterTile == 0, "a tile must not straddle a regroup window");
+__global__ void __launch_bounds__(kScatterTile) bucket_scatter_kernel(const CellParam *cells, const Carry *carry,
+                                                                      int32_t *bucket, int32_t *perm, int ncells,
+                                                                      int B, int nwin, int key_quads) {
+  __shared__ int s_cnt[kBuckets], s_base[kBuckets];
   const int cell = blockIdx.y;
   const CellParam cp = cells[cell];
   if (cp.policy != 0 || cp.conc) return;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < cp.n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t ts_set = carry[cp.out_off + j].ts_set;
-    uint32_t pairs = 0;
-    for (int k = 0; 2 * k < B; ++k)
-      if ((ts_set >> (2 * k)) & 3u) pairs |= 1u << k;
-    const int pos = atomicAdd(&bucket[((size_t)cell * nwin + j / kRegroupWindow) * kBuckets + regroup_key(pairs, key_quads)], 1);
-    perm[cp.out_off + pos] = (int32_t)j;
+  const int64_t ntiles = (cp.n + kScatterTile - 1) / kScatterTile;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (threadIdx.x < kBuckets) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t j = tile * kScatterTile + threadIdx.x;
+    int key = -1, rank = 0;
+    if (j < cp.n) {
+      const uint32_t ts_set = carry[cp.out_off + j].ts_set;
+      uint32_t pairs = 0;
+      for (int k = 0; 2 * k < B; ++k)
+        if ((ts_set >> (2 * k)) & 3u) pairs |= 1u << k;
+      key = regroup_key(pairs, key_quads);
+      rank = atomicAdd(&s_cnt[key], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < kBuckets && s_cnt[threadIdx.x] > 0)
+      s_base[threadIdx.x] = atomicAdd(&bucket[((size_t)cell * nwin + (tile * kScatterTile) / kRegroupWindow) * kBuckets +
+                                              threadIdx.x], s_cnt[threadIdx.x]);
+    __syncthreads();
+    if (key >= 0) perm[cp.out_off + s_base[key] + rank] = (int32_t)j;
+    __syncthreads();                                        // s_cnt is reset by the next tile
   }
 }
 
@@ -2019,10 +2047,12 @@ __global__ void curve_reduce_kernel(const long long *slots, long long *fixed, do
     const long long cell = i / ((long long)R * kQ);
     const long long rq = i % ((long long)R * kQ);
     long long l[kLimbs] = {0, 0, 0};
-    for (int k = 0; k < nslot; ++k)
+    const long long *src = slots + (size_t)cell * nslot * (size_t)R * kRow + rq * kLimbs;
+#pragma unroll 8
+    for (int k = 0; k < nslot; ++k)                         // independent loads, in flight together
 #pragma unroll
       for (int m = 0; m < kLimbs; ++m)
-        l[m] += slots[((size_t)cell * nslot + k) * (size_t)R * kRow + rq * kLimbs + m];
+        l[m] += src[(size_t)k * R * kRow + m];
 #pragma unroll
     for (int m = 0; m < kLimbs; ++m) fixed[i * kLimbs + m] = l[m];
     const bool count = rq % kQ >= 4;       // counts are plain integers in limb 0

@@ -836,8 +836,8 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
       ZS_CUDA(s, cudaGetLastError());
       zs::bucket_scan_kernel<<<(unsigned)((nc * (int64_t)s->nwin + 127) / 128), 128, 0, st>>>(a.bucket, nc, s->nwin);
       ZS_CUDA(s, cudaGetLastError());
-      const unsigned sx = (unsigned)std::min<int64_t>((s->max_shard + 255) / 256, 1184);
-      zs::bucket_scatter_kernel<<<dim3(std::max(1u, sx), (unsigned)nc), 256, 0, st>>>(
+      const unsigned sx = (unsigned)std::min<int64_t>((s->max_shard + zs::kScatterTile - 1) / zs::kScatterTile, 1184);
+      zs::bucket_scatter_kernel<<<dim3(std::max(1u, sx), (unsigned)nc), zs::kScatterTile, 0, st>>>(
           a.cells, a.carry, a.bucket, a.perm, nc, s->B, s->nwin, a.key_quads);
       ZS_CUDA(s, cudaGetLastError());
       if (certified) thompson_launch();

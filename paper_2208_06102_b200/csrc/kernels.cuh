@@ -14,6 +14,7 @@
 #include <cstdint>
 
 #include "contract.cuh"
+#include "certify.cuh"
 
 
 
@@ -189,6 +190,9 @@ struct ReplayArgs {
   // then groups the lanes by survivor-quad count; force_exact sends every draw to its exact
   // fp64 fallback (a test of that path)
   int key_quads, force_exact;
+  // replay_kernel's one-pass and exact phase-B schedules: the certified fp32 draw (draw = 0 or 2)
+  // instead of the bound screen; its fp32 table follows the residual slots in shared memory
+  int cert_draw;
 };
 
 constexpr int kBuckets = 34;      // 2 x popcount of the survivor-pair mask + parity of its lowest pair
@@ -470,6 +474,37 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   // this kernel past phase A is screened, so the screened draws are n_sampled here)
   uint32_t n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
   uint32_t n_resid = 0;                                     // bound screen: residual pairs
+  uint32_t n_cert = 0, n_fall = 0;                          // certified draw (a.cert_draw)
+  // certified draw: fp32 (mu - ref, sigma) per arm, [pair][thread] float4, after
+  // the residual slots; ref = the leader's posterior mean when Thompson sampling starts
+  const int cpairs2 = ((((B + 1) >> 1) + 1) & ~1);
+  float2 *s_f2 = reinterpret_cast<float2 *>(smem + a.tab_bytes + (size_t)((B + 1) & ~1) * 16 * TPB +
+                                            (size_t)kResSlots * 16 * TPB);
+  const int ckbits = 32 - __clz(2 * cpairs2 - 1);
+  const uint32_t ckeep = ~((1u << ckbits) - 1u);
+  const float ckth = cert::kTheta + __int_as_float((127 - 23 + ckbits) << 23) * 1.000001f;
+  double cref = 0.0;
+  float c_trial = 0.0f;
+  const bool cert_on = PHASE != 1 && a.cert_draw;
+  auto f32_slot = [&](int arm_i, double2 ms) {              // (mu - ref, sigma) in fp32
+    const double dm = ms.x - cref;
+    s_f2[2 * ((arm_i >> 1) * TPB + tid) + (arm_i & 1)] =
+        (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y)
+                                         : make_float2(0.0f, __int_as_float(0x7f800000));
+  };
+  // (re)build the fp32 table when Thompson sampling starts: survivors with n >= 2 from their fp64
+  // posteriors, the rest (and the padding pair) as non-survivor sentinels
+  auto cert_begin = [&]() {
+    const int lead = (last_b >= 0 && ((ts_set >> last_b) & 1u) && ((mature >> last_b) & 1u))
+                         ? last_b : __ffs(ts_set & mature) - 1;
+    cref = lead >= 0 ? s_ms[lead * TPB + tid].x : 0.0;
+    if (!(fabs(cref) < 1e30)) cref = 0.0;
+    c_trial = __double2float_ru(fabs(cref) * 0x1p-52 + 0x1p-120);
+    for (int arm_i = 0; arm_i < 2 * cpairs2; ++arm_i) {
+      if (((ts_set & mature) >> arm_i) & 1u) f32_slot(arm_i, s_ms[arm_i * TPB + tid]);
+      else s_f2[2 * ((arm_i >> 1) * TPB + tid) + (arm_i & 1)] = make_float2(3.0e38f, 0.0f);
+    }
+  };
   if (PHASE == 2 && active) {                               // resume from phase A
     const Carry c = a.carry[o];
     best = c.best; totC = c.totC; totE = c.totE; totT = c.totT; dig = c.dig;
@@ -483,6 +518,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       const int n = (WINDOWED && cp.window > 0) ? min(q.cnt, cp.window) : q.cnt;
       s_ms[b * TPB + tid] = posterior(q.sh, q.S1, q.S2, n, cp.prec0, cp.pm0);
     }
+    if (cert_on) cert_begin();
   }
 
   const int t_begin = PHASE == 2 ? a.t_split : 0;
@@ -543,7 +579,31 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
           // pairs 2q and 2q+1 share one Philox block: it is drawn when the walk enters a new
           // quad (warp-uniform in phase B, where lanes are grouped by count and parity)
 #if ZS_BOUND_SKIP
-          if (PHASE != 1) {
+          if (cert_on) {
+            // certified fp32 draw; not certified: the exact loop below
+            cert::Argmin32 am;
+            am.init();
+            uint32_t qm = quads_of(ts_pairs);
+            while (qm) {
+              const int qd = __ffs(qm) - 1;
+              qm &= qm - 1u;
+              const U4 x = pair_block_c(trial, t, qd);
+              const float4 f0 = reinterpret_cast<const float4 *>(s_f2)[(2 * qd) * TPB + tid];
+              const float4 f1 = reinterpret_cast<const float4 *>(s_f2)[(2 * qd + 1) * TPB + tid];
+              float z0, z1, rsq;
+              cert::normal_pair32(x.x, x.y, z0, z1, rsq);
+              am.pair(4 * qd, f0, z0, z1, rsq, ckeep);
+              cert::normal_pair32(x.z, x.w, z0, z1, rsq);
+              am.pair(4 * qd + 2, f1, z0, z1, rsq, ckeep);
+            }
+            if (am.certified(c_trial, ckth) && !a.force_exact) {
+              b = am.arg(ckeep);
+              pm = 0u;
+              n_cert += 1;
+            } else {
+              n_fall += 1;
+            }
+          } else if (PHASE != 1) {
             // bound screen (exact): draw the pair of the leader (the previous
             // decision's arm) first; then an arm a can only win if mu_a - sigma_a r_ub <= bt,
             // r_ub >= |z| bounded from the pair's radius word alone.  Pairs that fail the
@@ -748,6 +808,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
             ts_pairs = 0u;
             for (int k = 0; 2 * k < B; ++k)
               if ((ts_set >> (2 * k)) & 3u) ts_pairs |= 1u << k;
+            if (cert_on) cert_begin();
           }
         }
       }
@@ -815,7 +876,9 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
         qc_b = b;
         seen |= 1u << b;
         if ((PHASE == 2 && !ABL) || n >= 2) {               // every Thompson-phase arm was run in pruning
-          s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
+          const double2 ms = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
+          s_ms[b * TPB + tid] = ms;
+          if (cert_on && in_ts && ((ts_set >> b) & 1u)) f32_slot(b, ms);
           mature |= 1u << b;
           n_recomp += 1;
         }
@@ -852,13 +915,20 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   }
   const unsigned long long pairs_all = (unsigned long long)n_sampled * __popc(ts_pairs);
   const unsigned long long blocks_all = (unsigned long long)n_sampled * __popc(quads_of(ts_pairs));
-  const unsigned long long bm_done = pairs_all - screened + n_resid;
-  const unsigned long long blocks_done = blocks_all;
+  unsigned long long bm_done = pairs_all - screened + n_resid;
+  unsigned long long blocks_done = blocks_all, handled = screened;
+  if (cert_on) {                    // certified draw: fp64 transforms only in phase A and fallbacks
+    const unsigned long long nq = __popc(quads_of(ts_pairs));
+    bm_done = (unsigned long long)(n_sampled - n_cert) * __popc(ts_pairs);
+    blocks_done = (unsigned long long)(n_sampled + n_fall) * nq;
+    handled = (unsigned long long)(n_cert + n_fall) * 2 * nq;
+  }
   unsigned long long ctr[kCounters] = {
       active ? (unsigned long long)R : 0ull, n_sampled, pairs_all,
       (unsigned long long)n_sampled * __popc(ts_set),
       (unsigned long long)nstop, n_prune, n_forced, n_recomp, blocks_all,
-      active ? bm_done : 0ull, active ? blocks_done : 0ull, active ? screened : 0ull};
+      active ? bm_done : 0ull, active ? blocks_done : 0ull, active ? handled : 0ull,
+      active ? n_cert : 0ull, active ? n_fall : 0ull};
 #pragma unroll
   for (int q = 0; q < kCounters; ++q) {
     unsigned long long v = ctr[q];

@@ -795,8 +795,13 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
         k1 += 0xBB67AE85u;
       }
     }
+    // the one-pass and exact phase-B schedules run the certified draw too (draw != 1); its fp32
+    // table (float4 per pair, pairs padded to whole quads) follows the residual slots
+    a.cert_draw = s->draw != 1 ? 1 : 0;
+    const size_t cert_bytes = (size_t)s->tpb * (((((s->B + 1) / 2) + 1) & ~1) * 16);
     auto replay_launch = [&](int phase) {
-      replay_fn(windowed, s->log_mode, phase, s->any_ablation, rk)<<<grid, s->tpb, s->smem_bytes, st>>>(a);
+      const size_t rsmem = s->smem_bytes + (phase != 1 && a.cert_draw ? cert_bytes : 0);
+      replay_fn(windowed, s->log_mode, phase, s->any_ablation, rk)<<<grid, s->tpb, rsmem, st>>>(a);
     };
     // the Thompson phase with the certified fp32 draw unless the run asks for
     // the exact-screen kernel (draw = 1); cells with a window or an ablation keep replay_kernel

@@ -292,12 +292,12 @@ def test_schedules_bit_identical(zs, oracle, name):
             assert c[9] < 0.6 * c[2]
     # certified fp32 draw: every Thompson-phase draw is either certified or
     # sent to the exact fallback; draw = 2 sends all of them
+    # (windowed cells take it in replay_kernel's exact phase B, the others in thompson_kernel)
     ts_b = c4[12] + c4[13]
-    if job.cells[0]["window"] == 0:
-        assert ts_b > 0 and c5[12] == 0 and c5[13] == ts_b
-        assert c4[13] <= 0.01 * ts_b
-    else:                                    # a window keeps the exact-screen kernel
-        assert ts_b == 0 and c5[12] + c5[13] == 0
+    assert ts_b > 0 and c5[12] == 0 and c5[13] == ts_b
+    assert c4[13] <= 0.01 * ts_b
+    assert c1[12] + c1[13] > 0                  # the one-pass kernel certifies too (draw 0)
+    assert c2[12] + c2[13] == 0                 # draw 1: the exact screen only
     compare_cell(oracle, outs[1], job.workload, job.cells[0], 0, np.arange(job.trials),
                  job.recurrences, job.trials, logs=True)
 

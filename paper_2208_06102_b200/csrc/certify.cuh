@@ -105,6 +105,15 @@ struct Argmin32 {
     smax = fmaxf(smax, fmaxf(ms.y, ms.w));
     rsqmax = fmaxf(rsqmax, rsq);
   }
+  // the same with the pair's eligibility bits (arm a0: bit 0, a0 + 1: bit 1): an ineligible
+  // arm's theta becomes the non-survivor sentinel 3e38 (f3 / f2v kernels, whose fp32 tables hold
+  // every mature arm)
+  __device__ __forceinline__ void pair_masked(int a0, float4 ms, float z0, float z1, float rsq,
+                                              uint32_t keep, uint32_t two) {
+    if (!(two & 1u)) { ms.x = 3.0e38f; ms.y = 0.0f; }
+    if (!(two & 2u)) { ms.z = 3.0e38f; ms.w = 0.0f; }
+    pair(a0, ms, z0, z1, rsq, keep);
+  }
   __device__ __forceinline__ int arg(uint32_t keep) const { return __float_as_int(m1) & (int)~keep; }
   // Is arg() the contract's argmin?  For every other survivor x: key_x >= m2 (distinct arms have
   // distinct keys), and t - kth |t| is increasing in t, so theta_x - ref >= m2 - kth |m2| - S,

@@ -1322,6 +1322,7 @@ struct ConcArgs {
   double *best_ring;                   // [trial][best_n]
   int P, best_n;
   double MP;
+  int cert_draw, force_exact;          // certified fp32 draw, as ReplayArgs
 };
 
 template <bool LOG>
@@ -1374,6 +1375,30 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
   auto q_b = [&](int i) -> int & { return q_b_s[i * TPB + tid]; };
   auto q_flags = [&](int i) -> uint32_t & { return q_flags_s[i * TPB + tid]; };   // bit0 converged, bit1 walk
   int nq = 0;
+  // certified fp32 draw (a.cert_draw): fp32 (mu - ref, sigma) of every mature
+  // arm, [pair][thread] float4 after the queues; ref fixed when Thompson sampling starts
+  const int cpairs2 = ((((B + 1) >> 1) + 1) & ~1);
+  float2 *s_f2 = reinterpret_cast<float2 *>(q_flags_s + kMaxOutstanding * TPB);
+  const int ckbits = 32 - __clz(2 * cpairs2 - 1);
+  const uint32_t ckeep = ~((1u << ckbits) - 1u);
+  const float ckth = cert::kTheta + __int_as_float((127 - 23 + ckbits) << 23) * 1.000001f;
+  double cref = 0.0;
+  float c_trial = 0.0f;
+  uint32_t n_cert = 0, n_fall = 0;
+  auto f32_slot = [&](int arm_i, double2 ms) {
+    const double dm = ms.x - cref;
+    s_f2[2 * ((arm_i >> 1) * TPB + tid) + (arm_i & 1)] =
+        (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y)
+                                         : make_float2(0.0f, __int_as_float(0x7f800000));
+  };
+  auto cert_begin = [&]() {
+    const int lead = __ffs(ts_set & mature) - 1;
+    cref = lead >= 0 ? s_ms[lead * TPB + tid].x : 0.0;
+    if (!(fabs(cref) < 1e30)) cref = 0.0;
+    c_trial = __double2float_ru(fabs(cref) * 0x1p-52 + 0x1p-120);
+    for (int arm_i = 0; arm_i < 2 * cpairs2; ++arm_i)
+      if ((mature >> arm_i) & 1u) f32_slot(arm_i, s_ms[arm_i * TPB + tid]);
+  };
 
   ArmStat qc{0.0, 0.0, 0.0, 0, 0};                     // the last arm's record (read cache)
   int qc_b = -1;
@@ -1414,7 +1439,9 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
       qc_b = b;
       seen |= 1u << b;
       if (n >= 2) {
-        s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
+        const double2 ms = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
+        s_ms[b * TPB + tid] = ms;
+        if (a.cert_draw && in_ts) f32_slot(b, ms);
         mature |= 1u << b;
         n_recomp += 1;
       }
@@ -1446,6 +1473,7 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
         ts_pairs = 0u;
         for (int k = 0; 2 * k < B; ++k)
           if ((ts_set >> (2 * k)) & 3u) ts_pairs |= 1u << k;
+        if (a.cert_draw) cert_begin();
       }
     }
   };
@@ -1499,6 +1527,30 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
           double bt = kInf;
           b = -1;
           uint32_t pm = ts_pairs;
+          if (a.cert_draw) {                                 // certified fp32 draw (§7.9)
+            cert::Argmin32 am;
+            am.init();
+            uint32_t qm = quads_of(ts_pairs);
+            while (qm) {
+              const int qd = __ffs(qm) - 1;
+              qm &= qm - 1u;
+              const U4 x = pair_block(cp.key0, cp.key1, trial, t, qd);
+              const float4 f0 = reinterpret_cast<const float4 *>(s_f2)[(2 * qd) * TPB + tid];
+              const float4 f1 = reinterpret_cast<const float4 *>(s_f2)[(2 * qd + 1) * TPB + tid];
+              float z0, z1, rsq;
+              cert::normal_pair32(x.x, x.y, z0, z1, rsq);
+              am.pair_masked(4 * qd, f0, z0, z1, rsq, ckeep, (ts_set >> (4 * qd)) & 3u);
+              cert::normal_pair32(x.z, x.w, z0, z1, rsq);
+              am.pair_masked(4 * qd + 2, f1, z0, z1, rsq, ckeep, (ts_set >> (4 * qd + 2)) & 3u);
+            }
+            if (am.certified(c_trial, ckth) && !a.force_exact) {
+              b = am.arg(ckeep);
+              pm = 0u;
+              n_cert += 1;
+            } else {
+              n_fall += 1;
+            }
+          }
           int qcur = -1;
           U4 xq{0u, 0u, 0u, 0u};
           while (pm) {
@@ -1585,13 +1637,15 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
     a.n_stop[o] = nstop;
     a.final_arm[o] = last_b;
   }
+  const unsigned long long cq = __popc(quads_of(ts_pairs));
   unsigned long long ctr[kCounters] = {
       active ? (unsigned long long)R : 0ull, n_sampled,
       (unsigned long long)n_sampled * __popc(ts_pairs), (unsigned long long)n_sampled * __popc(ts_set),
       (unsigned long long)nstop, n_prune, n_forced, n_recomp,
-      (unsigned long long)n_sampled * __popc(quads_of(ts_pairs)),
-      (unsigned long long)n_sampled * __popc(ts_pairs),
-      (unsigned long long)n_sampled * __popc(quads_of(ts_pairs)), 0ull};
+      (unsigned long long)n_sampled * cq,
+      (unsigned long long)(n_sampled - n_cert) * __popc(ts_pairs),
+      (unsigned long long)(n_sampled + n_fall) * cq, (unsigned long long)(n_cert + n_fall) * 2 * cq,
+      n_cert, n_fall};
 #pragma unroll
   for (int qq = 0; qq < kCounters; ++qq) {
     unsigned long long v = ctr[qq];
@@ -1652,7 +1706,33 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
   unsigned long long dig = 0xcbf29ce484222325ull;
   int nstop = 0, last_b = -1;
   uint32_t n_dec = 0, n_sampled = 0, n_prune = 0, n_forced = 0, n_recomp = 0;
-  unsigned long long n_pairs = 0, n_normals = 0, n_blocks = 0;
+  unsigned long long n_pairs = 0, n_normals = 0, n_blocks = 0;   // the method's events
+  unsigned long long w_pairs = 0, w_blocks = 0, w_fp32 = 0;      // the work this build did
+  // certified fp32 draw (a.cert_draw): fp32 (mu - ref, sigma) of every mature
+  // arm after the (mu, sigma) table, ref fixed when Thompson sampling starts; the eligibility of
+  // an attempt (survivors not stopped in this recurrence) masks the keys
+  const int cpairs2 = ((((B + 1) >> 1) + 1) & ~1);
+  float2 *s_f2 = reinterpret_cast<float2 *>(smem + (size_t)((B + 1) & ~1) * 16 * TPB);
+  const int ckbits = 32 - __clz(2 * cpairs2 - 1);
+  const uint32_t ckeep = ~((1u << ckbits) - 1u);
+  const float ckth = cert::kTheta + __int_as_float((127 - 23 + ckbits) << 23) * 1.000001f;
+  double cref = 0.0;
+  float c_trial = 0.0f;
+  uint32_t n_cert = 0, n_fall = 0;
+  auto f32_slot = [&](int arm_i, double2 ms) {
+    const double dm = ms.x - cref;
+    s_f2[2 * ((arm_i >> 1) * TPB + tid) + (arm_i & 1)] =
+        (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y)
+                                         : make_float2(0.0f, __int_as_float(0x7f800000));
+  };
+  auto cert_begin = [&]() {
+    const int lead = __ffs(ts_set & mature) - 1;
+    cref = lead >= 0 ? s_ms[lead * TPB + tid].x : 0.0;
+    if (!(fabs(cref) < 1e30)) cref = 0.0;
+    c_trial = __double2float_ru(fabs(cref) * 0x1p-52 + 0x1p-120);
+    for (int arm_i = 0; arm_i < 2 * cpairs2; ++arm_i)
+      if ((mature >> arm_i) & 1u) f32_slot(arm_i, s_ms[arm_i * TPB + tid]);
+  };
 
   int s = 0;
   U4 rw{0u, 0u, 0u, 0u};
@@ -1692,20 +1772,52 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
           } else {
             double bt = kInf;
             b = -1;
+            bool exact = true;
+            uint32_t ep = 0u;                                // eligible pairs of this attempt
+            for (int k = 0; 2 * k < B; ++k)
+              if ((elig >> (2 * k)) & 3u) ep |= 1u << k;
+            n_pairs += __popc(ep);
+            n_normals += __popc(elig);
+            n_blocks += __popc(quads_of(ep));
+            if (a.cert_draw) {                               // certified fp32 draw (§7.9)
+              cert::Argmin32 am;
+              am.init();
+              uint32_t qm = quads_of(ep);
+              while (qm) {
+                const int qd = __ffs(qm) - 1;
+                qm &= qm - 1u;
+                const U4 x = pair_block(cp.key0, cp.key1, trial, t, qd | (j << 16));
+                w_blocks += 1;
+                w_fp32 += 2;
+                const float4 f0 = reinterpret_cast<const float4 *>(s_f2)[(2 * qd) * TPB + tid];
+                const float4 f1 = reinterpret_cast<const float4 *>(s_f2)[(2 * qd + 1) * TPB + tid];
+                float z0, z1, rsq;
+                cert::normal_pair32(x.x, x.y, z0, z1, rsq);
+                am.pair_masked(4 * qd, f0, z0, z1, rsq, ckeep, (elig >> (4 * qd)) & 3u);
+                cert::normal_pair32(x.z, x.w, z0, z1, rsq);
+                am.pair_masked(4 * qd + 2, f1, z0, z1, rsq, ckeep, (elig >> (4 * qd + 2)) & 3u);
+              }
+              if (am.certified(c_trial, ckth) && !a.force_exact) {
+                b = am.arg(ckeep);
+                exact = false;
+                n_cert += 1;
+              } else {
+                n_fall += 1;
+              }
+            }
             int qcur = -1;
             U4 xq{0u, 0u, 0u, 0u};
-            for (int k = 0; 2 * k < B; ++k) {
+            for (int k = 0; exact && 2 * k < B; ++k) {
               const uint32_t two = (elig >> (2 * k)) & 3u;
               if (!two) continue;
               if ((k >> 1) != qcur) {
                 qcur = k >> 1;
                 xq = pair_block(cp.key0, cp.key1, trial, t, qcur | (j << 16));
-                n_blocks += 1;
+                w_blocks += 1;
               }
               double z0, z1;
               box_muller((k & 1) ? xq.z : xq.x, (k & 1) ? xq.w : xq.y, z0, z1, a.logtab);
-              n_pairs += 1;
-              n_normals += __popc(two);
+              w_pairs += 1;
               const double2 m0 = s_ms[(2 * k) * TPB + tid];
               const double2 m1 = s_ms[(2 * k + 1) * TPB + tid];
               const double th0 = fma(m0.y, z0, m0.x);
@@ -1826,7 +1938,9 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
           qc_b = b;
           seen |= 1u << b;
           if (n >= 2) {
-            s_ms[b * TPB + tid] = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
+            const double2 ms = posterior(sh, S1, S2, n, cp.prec0, cp.pm0);
+            s_ms[b * TPB + tid] = ms;
+            if (a.cert_draw && in_ts) f32_slot(b, ms);
             mature |= 1u << b;
             n_recomp += 1;
           }
@@ -1855,6 +1969,7 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
             } else {
               in_ts = true;
               ts_set = no_prune ? all_arms : surv;
+              if (a.cert_draw) cert_begin();
             }
           }
         }
@@ -1906,7 +2021,7 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
   unsigned long long ctr[kCounters] = {
       active ? (unsigned long long)n_dec : 0ull, n_sampled, n_pairs, n_normals,
       (unsigned long long)nstop, n_prune, n_forced, n_recomp, n_blocks,
-      n_pairs, n_blocks, 0ull};
+      w_pairs, w_blocks, w_fp32, n_cert, n_fall};
 #pragma unroll
   for (int qq = 0; qq < kCounters; ++qq) {
     unsigned long long v = ctr[qq];

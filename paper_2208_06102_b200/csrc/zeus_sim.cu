@@ -727,16 +727,21 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     c.MP = s->MP;
     const size_t smem = (size_t)128 * (((s->B + 1) & ~1) * 16);
     const dim3 grid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
-    if (s->any_conc) {                      // + the outstanding-run queues (kernels.cuh)
-      const size_t csmem = smem + (size_t)128 * zs::kQueueBytes;
+    c.cert_draw = s->draw != 1 ? 1 : 0;
+    c.force_exact = s->draw == 2 ? 1 : 0;
+    if (s->any_conc) {                      // + the outstanding-run queues (kernels.cuh) + the
+                                            // certified draw's fp32 table (pairs padded to quads)
+      const size_t csmem = smem + (size_t)128 * zs::kQueueBytes +
+                           (size_t)128 * (((((s->B + 1) / 2) + 1) & ~1) * 16);
       if (s->log_mode) zs::concurrent_kernel<true><<<grid, 128, csmem, st>>>(c);
       else zs::concurrent_kernel<false><<<grid, 128, csmem, st>>>(c);
       ZS_CUDA(s, cudaGetLastError());
       s->launches += 1;
     }
     if (s->any_variant) {
-      if (s->log_mode) zs::variant_kernel<true><<<grid, 128, smem, st>>>(c);
-      else zs::variant_kernel<false><<<grid, 128, smem, st>>>(c);
+      const size_t vsmem = smem + (size_t)128 * (((((s->B + 1) / 2) + 1) & ~1) * 16);   // + fp32 table
+      if (s->log_mode) zs::variant_kernel<true><<<grid, 128, vsmem, st>>>(c);
+      else zs::variant_kernel<false><<<grid, 128, vsmem, st>>>(c);
       ZS_CUDA(s, cudaGetLastError());
       s->launches += 1;
     }

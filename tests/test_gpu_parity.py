@@ -343,39 +343,43 @@ def test_f4_pareto_front(zs, oracle):
                 assert np.array_equal(g["pareto"][s], oracle.pareto(job.workload, s)), (name, s)
 
 
-def test_f2_ablations(zs, oracle):
+@pytest.mark.parametrize("draw", [0, 2])
+def test_f2_ablations(zs, oracle, draw):
     """the ablations of P:L1076-1077 (no early stop = beta inf, no pruning,
-    no JIT profiling) in the same launch as full Zeus; every trial bit-exact vs the oracle."""
+    no JIT profiling) in the same launch as full Zeus; every trial bit-exact vs the oracle, with the
+    certified draw (0) and with every Thompson draw through its exact fallback (2)."""
     for job in synth.config("f2", trials=2000)[:3]:
-        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True)
+        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True, draw=draw)
         for ci, c in enumerate(job.cells):
             compare_cell(oracle, g, job.workload, c, ci, np.arange(job.trials), job.recurrences,
                          job.trials, logs=True)
 
 
-def test_f3_concurrent_submissions(zs, oracle):
+@pytest.mark.parametrize("draw", [0, 2])
+def test_f3_concurrent_submissions(zs, oracle, draw):
     """concurrent submissions under Poisson arrival schedules (§4.4
     P:L634-646) next to the sequential cell in one launch; every trial bit-exact."""
     for job in synth.config("f3", trials=2000)[:3]:
-        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True)
+        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True, draw=draw)
         for ci, c in enumerate(job.cells):
             compare_cell(oracle, g, job.workload, c, ci, np.arange(job.trials), job.recurrences,
                          job.trials, logs=True)
     # the drift config with a window, heavy overlap
     (job,) = synth.config("cfg4_38", trials=1500)
     c = dict(job.cells[0], arrivals=synth.arrival_schedule(job.workload, job.recurrences, 0.3, 5))
-    g = run_gpu(zs, job.workload, [c], job.trials, job.recurrences, log=True)
+    g = run_gpu(zs, job.workload, [c], job.trials, job.recurrences, log=True, draw=draw)
     compare_cell(oracle, g, job.workload, c, 0, np.arange(job.trials), job.recurrences, job.trials,
                  logs=True)
 
 
-def test_f2v_variant_readings(zs, oracle):
+@pytest.mark.parametrize("draw", [0, 2])
+def test_f2v_variant_readings(zs, oracle, draw):
     """SURVEY §8(f) f2, the variant readings of P:L559 (DESIGN.md R-Q4v retry, R-Q1v epoch-boundary
     stop, R-Q5v windowed best under drift), each in the same launch as the base cell: every
     trial and logged decision bit-exact vs the oracle, curves within 1e-9."""
     jobs = synth.config("f2v", trials=1500)
     for job in (jobs[0], jobs[3], jobs[6]):
-        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True)
+        g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True, draw=draw)
         decisions = 0
         for ci, c in enumerate(job.cells):
             o = compare_cell(oracle, g, job.workload, c, ci, np.arange(job.trials), job.recurrences,

@@ -724,7 +724,10 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       was_seen = (ZS_SLIM_B && PHASE == 2 && !ABL && !WINDOWED) ? true : ((seen >> b) & 1u);
       if (b != qc_b) {
         if (PHASE == 2 && qc_b >= 0) st[qc_b] = qc;
-        qc = st[b];
+        // an arm never observed in this trial has no record yet: nothing to load (its slot holds
+        // another run's bytes, a cold DRAM read on the decision's chain)
+        if (was_seen) qc = st[b];
+        else qc = ArmStat{0.0, 0.0, 0.0, 0, 0};
         qc_b = b;
       }
       // the windowed Observe's evicted cost, loaded as soon as the decision is known
@@ -1082,7 +1085,7 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
     double C = 0.0;
     if (active) {
       was_seen = (seen >> b) & 1u;
-      if (b == qc_b) q = qc; else q = st[b];
+      if (b == qc_b) q = qc; else if (was_seen) q = st[b]; else q = ArmStat{0.0, 0.0, 0.0, 0, 0};
       const ArmConst ac = arm[b];
       const uint32_t r = __umulhi(pick_word(rw, t), (uint32_t)K);
       const int E = pool[((size_t)s * B + b) * K + r];
@@ -1411,7 +1414,7 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
     {                                                        // Alg. 2 Observe (NC-6)
       const bool was_seen = (seen >> b) & 1u;
       ArmStat q;
-      if (b == qc_b) q = qc; else q = st[b];
+      if (b == qc_b) q = qc; else if (was_seen) q = st[b]; else q = ArmStat{0.0, 0.0, 0.0, 0, 0};
       const int cnt = was_seen ? q.cnt : 0;
       double sh, S1, S2;
       if (!was_seen) { sh = C; S1 = 0.0; S2 = 0.0; }
@@ -1835,7 +1838,7 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
         // the power limit; "no JIT" tries the limits in ascending order first
         const bool was_seen = (seen >> b) & 1u;
         ArmStat q;
-        if (b == qc_b) q = qc; else q = st[b];
+        if (b == qc_b) q = qc; else if (was_seen) q = st[b]; else q = ArmStat{0.0, 0.0, 0.0, 0, 0};
         const ArmConst ac = arm[b];
         int p = ac.pstar;
         double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;

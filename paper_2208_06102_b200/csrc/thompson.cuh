@@ -350,8 +350,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
       vC = C;
       vE = En;
       vT = Tm;
-      vReg = regret[s * B + b];
-      vPacked = (stopped ? 1 : 0) | ((b == optarm[s]) ? (1 << 8) : 0) | (1 << 16);
+      vPacked = stopped ? 1 : 0;            // the rest of a stopped run's curve values below
     }
     {
       const bool special = active && (vPacked & 1);
@@ -359,9 +358,16 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
       if (active && !special) red_add_u32(hrow + hkey, 1u);
 #endif
       hrow += hstride;
-      if (__any_sync(0xffffffffu, special))
+      if (__any_sync(0xffffffffu, special)) {
+        // a stopped run's pseudo-regret and counts (stop | optimal << 8 | Thompson << 16) are read
+        // only here (the counted runs take theirs from the histogram fold)
+        if (special) {
+          vReg = regret[s * B + b];
+          vPacked = 1 | ((b == optarm[s]) ? (1 << 8) : 0) | (1 << 16);
+        }
         curve_accumulate(curves, t, tid & 31, special ? vC : 0.0, special ? vE : 0.0, special ? vT : 0.0,
                          special ? vReg : 0.0, special ? vPacked : 0, a.curve_scale);
+      }
     }
     if (active) {
       // ---------------- Alg. 2 Observe(b, C) with shifted sums (NC-6)

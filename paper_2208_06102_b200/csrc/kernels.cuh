@@ -27,6 +27,9 @@
 #ifndef ZS_BOUND_SKIP
 #define ZS_BOUND_SKIP 1
 #endif
+#ifndef ZS_PHASEA_CERT
+#define ZS_PHASEA_CERT 1
+#endif
 
 namespace zs {
 
@@ -220,13 +223,14 @@ struct __align__(16) ArmStat {    // Observe state of one arm of one trial (NC-6
   int32_t cnt, pad;               // observations ever
 };
 
-// per-trial scalar state carried from phase A to phase B (80 B)
+// per-trial scalar state carried from phase A to phase B (88 B)
 struct Carry {
   double best, totC, totE, totT;
   unsigned long long dig;
   uint32_t profiled, seen, mature, ts_set;
   int32_t nstop, last_b;
   uint32_t n_sampled, n_prune, n_forced, n_recomp;
+  uint32_t n_cert, n_fall;        // phase A's certified draws and their exact fallbacks
 };
 
 // shared-memory table region of one block: [ArmConst B][regret S*B][opt_arm S][pool S*B*K]
@@ -485,7 +489,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const float ckth = cert::kTheta + __int_as_float((127 - 23 + ckbits) << 23) * 1.000001f;
   double cref = 0.0;
   float c_trial = 0.0f;
-  const bool cert_on = PHASE != 1 && a.cert_draw;
+  const bool cert_on = (PHASE != 1 || ZS_PHASEA_CERT) && a.cert_draw;
   auto f32_slot = [&](int arm_i, double2 ms) {              // (mu - ref, sigma) in fp32
     const double dm = ms.x - cref;
     s_f2[2 * ((arm_i >> 1) * TPB + tid) + (arm_i & 1)] =
@@ -895,6 +899,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       c.profiled = profiled; c.seen = seen; c.mature = mature; c.ts_set = ts_set;
       c.nstop = nstop; c.last_b = last_b;
       c.n_sampled = n_sampled; c.n_prune = n_prune; c.n_forced = n_forced; c.n_recomp = n_recomp;
+      c.n_cert = n_cert; c.n_fall = n_fall;
       a.carry[o] = c;
       atomicAdd(&a.bucket[((size_t)cell * a.nwin + jj / kRegroupWindow) * kBuckets + regroup_key(ts_pairs, a.key_quads)], 1);
     }
@@ -915,6 +920,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   if (PHASE == 2 && active) {
     const Carry c = a.carry[o];
     n_sampled += c.n_sampled; n_prune += c.n_prune; n_forced += c.n_forced; n_recomp += c.n_recomp;
+    n_cert += c.n_cert; n_fall += c.n_fall;
   }
   const unsigned long long pairs_all = (unsigned long long)n_sampled * __popc(ts_pairs);
   const unsigned long long blocks_all = (unsigned long long)n_sampled * __popc(quads_of(ts_pairs));

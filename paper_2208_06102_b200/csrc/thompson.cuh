@@ -394,16 +394,20 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   // (fallback draws), [10] Philox blocks, [11] fp32 pairs, [12] certified, [13] fallbacks
   // (phase A's Thompson draws, carried in n_sampled, are full fp64 draws: counted in [9], [10])
   const uint32_t nB = active ? (uint32_t)(R - a.t_split) : 0u;   // phase-B decisions = draws
-  const uint32_t n_cert = nB - n_fall;
-  const unsigned long long fp32_pairs = (unsigned long long)nB * 2 * __popc(quads);
-  uint32_t n_sampled = nB, n_prune = 0, n_forced = 0, n_recomp = nB, n_full = n_fall;
+  uint32_t n_cert = nB - n_fall;
+  // phase A's draws: certified (fp32 pairs, one block per quad) or full fp64 (its fallbacks and,
+  // without the certified draw, all of them)
+  uint32_t n_sampled = nB, n_prune = 0, n_forced = 0, n_recomp = nB, n_full = n_fall, n_tried = nB;
   if (active) {
     const Carry c = a.carry[o];
-    n_full += c.n_sampled;
+    n_full += c.n_sampled - c.n_cert;
+    n_tried += c.n_cert + c.n_fall;
+    n_cert += c.n_cert; n_fall += c.n_fall;
     n_sampled += c.n_sampled; n_prune = c.n_prune; n_forced = c.n_forced; n_recomp += c.n_recomp;
   }
+  const unsigned long long fp32_pairs = (unsigned long long)n_tried * 2 * __popc(quads);
   const unsigned long long fall_pairs = (unsigned long long)n_full * __popc(ts_pairs);
-  const unsigned long long blocks_fp32 = (unsigned long long)nB * __popc(quads);
+  const unsigned long long blocks_fp32 = (unsigned long long)n_tried * __popc(quads);
   const unsigned long long blocks_fall = (unsigned long long)n_full * __popc(quads);
   const unsigned long long pairs_all = (unsigned long long)n_sampled * __popc(ts_pairs);
   const unsigned long long blocks_all = (unsigned long long)n_sampled * __popc(quads);

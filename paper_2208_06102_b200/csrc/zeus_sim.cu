@@ -805,7 +805,7 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     a.cert_draw = s->draw != 1 ? 1 : 0;
     const size_t cert_bytes = (size_t)s->tpb * (((((s->B + 1) / 2) + 1) & ~1) * 16);
     auto replay_launch = [&](int phase) {
-      const size_t rsmem = s->smem_bytes + (phase != 1 && a.cert_draw ? cert_bytes : 0);
+      const size_t rsmem = s->smem_bytes + ((phase != 1 || ZS_PHASEA_CERT) && a.cert_draw ? cert_bytes : 0);
       replay_fn(windowed, s->log_mode, phase, s->any_ablation, rk)<<<grid, s->tpb, rsmem, st>>>(a);
     };
     // the Thompson phase with the certified fp32 draw unless the run asks for

@@ -42,6 +42,7 @@ VARIANTS = {
     "th_mb7": (["ZS_TH_MIN_BLOCKS=7"], []),
     "th_q1": (["ZS_QUAD2=0"], []),
     "hs4": (["ZS_HSLOT_MAX=4"], []),
+    "pa_cert": (["ZS_PHASEA_CERT=1"], []),
     "hs64": (["ZS_HSLOT_MAX=64"], []),
     "diag_nohist": (["ZS_DIAG_NOHIST"], []),   # timing diagnostic only: curves wrong
     "th_q2_mb5": (["ZS_TH_MIN_BLOCKS=5"], []),

@@ -1047,9 +1047,10 @@ zeus_status zeus_sim_shape(const zeus_sim *s, int32_t *recurrences, int64_t *sha
 
 zeus_status zeus_sim_certify_bounds(int32_t cuda_device, double *out) {
   if (!out) return ZEUS_E_INVALID;
-  int ndev = 0;
+  int ndev = 0, prev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) return ZEUS_E_CUDA;
-  if (cudaSetDevice(cuda_device) != cudaSuccess) return ZEUS_E_CUDA;
+  if (cudaGetDevice(&prev) != cudaSuccess || cudaSetDevice(cuda_device) != cudaSuccess) return ZEUS_E_CUDA;
+  struct Restore { int d; ~Restore() { cudaSetDevice(d); } } restore{prev};   // the caller's device
   cudaStream_t st = nullptr;
   double2 *tab = nullptr;
   unsigned *d_out = nullptr;

@@ -2235,22 +2235,29 @@ __global__ void curve_hist_fold_kernel(const uint32_t *hist, long long *slots, c
 
 __global__ void curve_reduce_kernel(const long long *slots, long long *fixed, double *curves,
                                     int ncells, int nslot, int R, double inv_scale) {
+  // one warp per output value: lanes sum the slot copies (integers: exact in any order), a
+  // shuffle tree adds the lanes, lane 0 carries the limbs and rounds once
   const long long total = (long long)ncells * R * kQ;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long i = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < total; i += nwarps) {
     const long long cell = i / ((long long)R * kQ);
     const long long rq = i % ((long long)R * kQ);
-    long long l[kLimbs] = {0, 0, 0};
     const long long *src = slots + (size_t)cell * nslot * (size_t)R * kRow + rq * kLimbs;
-#pragma unroll 8
-    for (int k = 0; k < nslot; ++k)                         // independent loads, in flight together
+    long long l[kLimbs] = {0, 0, 0};
+    for (int k = lane; k < nslot; k += 32)
 #pragma unroll
-      for (int m = 0; m < kLimbs; ++m)
-        l[m] += src[(size_t)k * R * kRow + m];
+      for (int m = 0; m < kLimbs; ++m) l[m] += src[(size_t)k * R * kRow + m];
 #pragma unroll
-    for (int m = 0; m < kLimbs; ++m) fixed[i * kLimbs + m] = l[m];
-    const bool count = rq % kQ >= 4;       // counts are plain integers in limb 0
-    curves[i] = count ? (double)l[0] : fixed_to_double(l[0], l[1], l[2], inv_scale);
+    for (int m = 0; m < kLimbs; ++m)
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) l[m] += __shfl_xor_sync(0xffffffffu, l[m], off);
+    if (lane == 0) {
+#pragma unroll
+      for (int m = 0; m < kLimbs; ++m) fixed[i * kLimbs + m] = l[m];
+      const bool count = rq % kQ >= 4;     // counts are plain integers in limb 0
+      curves[i] = count ? (double)l[0] : fixed_to_double(l[0], l[1], l[2], inv_scale);
+    }
   }
 }
 

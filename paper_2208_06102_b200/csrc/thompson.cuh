@@ -93,7 +93,11 @@ __device__ __forceinline__ U4 philox_from_prefix(const PhiloxPrefix &p, uint32_t
   return c;
 }
 
-template <bool LOG, bool RK>
+// SREC (launches of at most a couple of waves, where one warp per scheduler makes the decision's
+// latency the throughput): every survivor's Observe record lives in shared memory for the whole
+// phase ([arm][thread], after the replica words), loaded once at the start and written back at
+// the end, so a decision that moves to another arm waits on a shared-memory load, not on L2.
+template <bool LOG, bool RK, bool SREC>
 __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
@@ -154,7 +158,13 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   const int64_t jj = active ? a.perm[cp.out_off + j0 + tid] : 0;
   const int64_t trial = cp.begin + jj;
   const size_t o = (size_t)(cp.out_off + jj);
-  ArmStat *st = a.st + o * B;
+  ArmStat *st_g = a.st + o * B;
+  ArmStat *s_rec = reinterpret_cast<ArmStat *>(smem + a.tab_bytes +
+                                               (size_t)((((B + 1) >> 1) + 1) & ~1) * 16 * TPB + 16 * (size_t)TPB);
+  auto rec = [&](int arm_i) -> ArmStat & {
+    if constexpr (SREC) return s_rec[(size_t)arm_i * TPB + tid];
+    else return st_g[arm_i];
+  };
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
   long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
   const int HB = 4 * B * K;
@@ -188,9 +198,12 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
     quads = quads_of(ts_pairs);
     // ref: the posterior mean of the leader (the last arm run, or the first survivor), so the
     // fp32 (mu - ref) of the arms that compete with it are small
+    if constexpr (SREC)                                     // the survivors' records, once
+      for (int b = 0; b < B; ++b)
+        if ((ts_set >> b) & 1u) s_rec[(size_t)b * TPB + tid] = st_g[b];
     const int lead = (last_b >= 0 && ((ts_set >> last_b) & 1u)) ? last_b : __ffs(ts_set) - 1;
     {
-      const ArmStat q = st[lead];
+      const ArmStat q = rec(lead);
       ref = posterior(q.sh, q.S1, q.S2, q.cnt, cp.prec0, cp.pm0).x;
     }
     if (!(fabs(ref) < 1e30)) ref = 0.0;
@@ -200,7 +213,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
       // (|mu'| < 1e30, sigma < 1e30), so it never wins and never hides a survivor's key
       float2 v = make_float2(3.0e38f, 0.0f);                // (every survivor ran at least twice)
       if ((ts_set >> b) & 1u) {
-        const ArmStat q = st[b];
+        const ArmStat q = rec(b);
         const double2 ms = posterior(q.sh, q.S1, q.S2, q.cnt, cp.prec0, cp.pm0);
         const double dm = ms.x - ref;
         v = (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y) : make_float2(0.0f, kInfF);
@@ -291,7 +304,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
             for (int h = 0; h < 2; ++h) {
               const int arm_i = 2 * k + h;
               if (!((ts_set >> arm_i) & 1u)) continue;
-              const ArmStat q = (arm_i == qc_b) ? qc : st[arm_i];
+              const ArmStat q = (arm_i == qc_b) ? qc : rec(arm_i);
               const double2 ms = posterior(q.sh, q.S1, q.S2, q.cnt, cp.prec0, cp.pm0);
               const double th = fma(ms.y, h ? z1 : z0, ms.x);
               if (th < bt) { bt = th; b = arm_i; }
@@ -301,8 +314,8 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
       }
       // Observe record of arm b (write-back cache)
       if (b != qc_b) {
-        if (qc_b >= 0) st[qc_b] = qc;
-        qc = st[b];
+        if (qc_b >= 0) rec(qc_b) = qc;
+        qc = rec(b);
         qc_b = b;
       }
       const ArmConst ac = arm[b];
@@ -381,7 +394,11 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
           (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y) : make_float2(0.0f, kInfF);
     }
   }
-  if (active && qc_b >= 0) st[qc_b] = qc;
+  if (active && qc_b >= 0) rec(qc_b) = qc;
+  if constexpr (SREC)                                       // write the phase's records back
+    if (active)
+      for (int b = 0; b < B; ++b)
+        if ((ts_set >> b) & 1u) st_g[b] = s_rec[(size_t)b * TPB + tid];
   if (active) {
     a.tot_cost[o] = totC;
     a.tot_energy[o] = totE;

@@ -57,7 +57,7 @@ struct zeus_sim {
   // cells / run
   std::vector<zeus_cell> cells;
   std::vector<zs::CellParam> cpar;
-  int R = 0, log_mode = 0, layout = 0, device = 0, wmax = 0, draw = 0;
+  int R = 0, log_mode = 0, layout = 0, device = 0, wmax = 0, draw = 0, sms = 148;
   int64_t shard_total = 0, max_shard = 0;
   // trace
   int S = 0, K = 0, reg_stride = 0, opt_stride = 0;
@@ -346,6 +346,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
   s->layout = opts->layout;
   s->use_graph = opts->graph;
   s->draw = opts->draw;
+  cudaDeviceGetAttribute(&s->sms, cudaDevAttrMultiProcessorCount, cuda_device);
   {                                      // arrival schedules: finite, non-decreasing (R-Q31)
     Errors EA;
     for (int i = 0; i < num_cells; ++i) {
@@ -632,10 +633,14 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
       for (int ph = 0; ph < 3; ++ph)
         for (int ab = 0; ab < 3; ++ab)            // ab == 2: the RK kernels
           ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph, ab == 1, ab == 2), s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, false>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, false>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, true>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, true>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, false, false>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, false, false>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, true, false>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, true, false>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, false, true>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, false, true>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, true, true>, s->device));
+  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, true, true>, s->device));
   ZS_CUDA(s, grant_group<2>(s->device));
   ZS_CUDA(s, grant_group<4>(s->device));
   ZS_CUDA(s, grant_group<8>(s->device));
@@ -816,12 +821,25 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     auto thompson_launch = [&]() {
       const dim3 tgrid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
       const size_t tsmem = (size_t)s->tab_bytes + (size_t)128 * (((((s->B + 1) / 2) + 1) & ~1) * 16 + 16);
-      if (rk) {
-        if (s->log_mode) zs::thompson_kernel<true, true><<<tgrid, 128, tsmem, st>>>(a);
-        else zs::thompson_kernel<false, true><<<tgrid, 128, tsmem, st>>>(a);
+      // launches of at most two blocks per SM keep the survivors' records in shared memory
+      // (thompson.cuh, SREC): there the decision's latency is the throughput
+      const size_t rec_bytes = (size_t)128 * s->B * sizeof(zs::ArmStat);
+      const bool srec = (int64_t)tgrid.x * tgrid.y <= 2 * (int64_t)s->sms && tsmem + rec_bytes <= 100 * 1024;
+      const size_t m = tsmem + (srec ? rec_bytes : 0);
+      if (srec) {
+        if (rk) {
+          if (s->log_mode) zs::thompson_kernel<true, true, true><<<tgrid, 128, m, st>>>(a);
+          else zs::thompson_kernel<false, true, true><<<tgrid, 128, m, st>>>(a);
+        } else {
+          if (s->log_mode) zs::thompson_kernel<true, false, true><<<tgrid, 128, m, st>>>(a);
+          else zs::thompson_kernel<false, false, true><<<tgrid, 128, m, st>>>(a);
+        }
+      } else if (rk) {
+        if (s->log_mode) zs::thompson_kernel<true, true, false><<<tgrid, 128, m, st>>>(a);
+        else zs::thompson_kernel<false, true, false><<<tgrid, 128, m, st>>>(a);
       } else {
-        if (s->log_mode) zs::thompson_kernel<true, false><<<tgrid, 128, tsmem, st>>>(a);
-        else zs::thompson_kernel<false, false><<<tgrid, 128, tsmem, st>>>(a);
+        if (s->log_mode) zs::thompson_kernel<true, false, false><<<tgrid, 128, m, st>>>(a);
+        else zs::thompson_kernel<false, false, false><<<tgrid, 128, m, st>>>(a);
       }
     };
     // auto: two phases except for windowed launches, where the one-pass kernel measured
@@ -865,7 +883,7 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     }
   }
   ZS_CUDA(s, record(s->ev1));
-  zs::curve_reduce_kernel<<<std::max(1, std::min(1184, (int)((nc * (size_t)s->R * zs::kQ + 255) / 256))), 256, 0, st>>>(
+  zs::curve_reduce_kernel<<<std::max(1, std::min(4 * 1184, (int)((nc * (size_t)s->R * zs::kQ + 7) / 8))), 256, 0, st>>>(
       s->d_slots.as<long long>(), s->d_fixed.as<long long>(), s->d_curves.as<double>(), nc, s->nslot,
       s->R, std::ldexp(1.0, -s->curve_bits));
   ZS_CUDA(s, cudaGetLastError());

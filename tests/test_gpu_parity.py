@@ -197,14 +197,14 @@ def _random_trace(rng, B, P, S, K, fail=0.2):
     (17, 5, 2, 3, 0, 2.0, 150, 60),       # odd arm count, two phases, two slices
     (3, 4, 1, 2, 0, math.inf, 130, 30),   # two phases, two pairs, no early stop
 ])
-@pytest.mark.parametrize("layout", [0, 3])
-def test_random_traces_edge_cases(zs, oracle, B, P, S, K, window, beta, trials, R, layout):
+@pytest.mark.parametrize("layout,draw", [(0, 0), (0, 2), (3, 0)])
+def test_random_traces_edge_cases(zs, oracle, B, P, S, K, window, beta, trials, R, layout, draw):
     rng = np.random.default_rng(B * 1000 + P)
     w = _random_trace(rng, B, P, S, K)
     cells = [synth.cell(eta=e, beta=beta, window=window, seed=int(rng.integers(2**63)),
                         prior_mean=pm, prior_var=pv)
              for e, pm, pv in ((0.0, 0.0, math.inf), (1.0, 500.0, 1e6), (0.37, 0.0, math.inf))]
-    g = run_gpu(zs, w, cells, trials, R, log=True, layout=layout)
+    g = run_gpu(zs, w, cells, trials, R, log=True, layout=layout, draw=draw)
     Rr = g["R"]
     assert Rr == (R if R > 0 else 2 * B * P)
     compare_step1(oracle, g, w, cells)

@@ -41,6 +41,11 @@
  *    results do not depend on how [0, trials) is split across ranks.
  *  - No CPU fallback: when no CUDA device is usable every call that would
  *    launch work fails with ZEUS_E_CUDA.
+ *  - Exactness: every decision is the numerics contract's.  The
+ *    Thompson draw may be evaluated in fp32 with a proven error bound and its
+ *    argmin certified against the contract's fp64 values (zeus_run_opts.draw,
+ *    DESIGN.md §7.9); where the bound cannot separate the winner the contract's
+ *    fp64 draw decides.  Options change the work, never the results.
  */
 #ifndef ZEUS_SIM_H
 #define ZEUS_SIM_H
@@ -49,11 +54,11 @@
 extern "C" {
 #endif
 
-#define ZEUS_SIM_ABI_VERSION 1
+#define ZEUS_SIM_ABI_VERSION 2   /* 2: zeus_run_opts.draw, 14 counters, zeus_sim_certify_bounds */
 #define ZEUS_MAX_BATCH_SIZES 32
 #define ZEUS_MAX_POWER_LIMITS 64
 #define ZEUS_CURVE_QUANTITIES 7   /* cost, energy, time, pseudo-regret, n_stop, n_opt, n_ts */
-#define ZEUS_COUNTERS 12   /* 0..8 contract events (oracle-checked), 9..11 work evaluated */
+#define ZEUS_COUNTERS 14   /* 0..8 contract events (oracle-checked), 9..13 work evaluated */
 
 typedef enum {
   ZEUS_OK = 0,

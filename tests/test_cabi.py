@@ -141,3 +141,11 @@ def test_variant_validation(zs):
         with pytest.raises(zs.ZeusError) as e:
             zs.zeus_sim_create(job, [cell], opts)
         assert e.value.status == 1 and frag in str(e.value), str(e.value)
+
+
+def test_header_constants_match_binding(zs):
+    """The binding's sizes follow the header (counters array, curve quantities)."""
+    src = open(HEADER).read()
+    n = int(re.search(r"#define ZEUS_COUNTERS (\d+)", src).group(1))
+    q = int(re.search(r"#define ZEUS_CURVE_QUANTITIES (\d+)", src).group(1))
+    assert zs.COUNTERS == n and q == 7

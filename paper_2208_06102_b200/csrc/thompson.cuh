@@ -1,7 +1,7 @@
 // thompson.cuh -- the Thompson-sampling phase of the two-phase schedule
 // with the certified fp32 draw of certify.cuh.
 //
-// thompson_kernel<LOG, RK> runs recurrences t_split..R-1 of every trial of a launch whose
+// thompson_kernel<LOG, RK, SREC> runs recurrences t_split..R-1 of every trial of a launch whose
 // cells have no window and no ablation, after replay_kernel's phase A (Alg. 3 pruning) and the
 // regroup.  Per decision (Alg. 1, then steps 3-4 as in replay_kernel):
 //   * every survivor quad's Philox block (NC-3) is drawn; both of its Box-Muller pairs are

@@ -48,13 +48,22 @@ def test_radius_cap_covers_the_largest_radius(C):
     assert rmax + er < float(C["kRMax"])
 
 
-def test_normal_error_constants(C):
+def normal_constants_ok(C):
     """|z32 - z| <= e_r (1 + 2 kAng + 2u + 2ud) + r32 (kAng + u (1 + kAng) + ud), with e_r the
     checked radius bound evaluated with two upward roundings (x (1 + 2^-23)^2)."""
     a, b, ang = C["kAlpha"], C["kBeta"], C["kAng"]
     grow = (1 + 2 * U) ** 2 * (1 + 2 * ang + 2 * U + 2 * UD)
-    assert C["kZr"] >= a * grow + (ang + U * (1 + ang) + UD) * (1 + 4 * U)
-    assert C["kZb"] >= b * grow
+    return C["kZr"] >= a * grow + (ang + U * (1 + ang) + UD) * (1 + 4 * U) and C["kZb"] >= b * grow
+
+
+def test_normal_error_constants(C):
+    assert normal_constants_ok(C)
+
+
+def test_normal_error_constants_negative_control(C):
+    """The check has teeth: the angle term dropped from kZr, or kZb without its growth, fails."""
+    assert not normal_constants_ok(dict(C, kZr=C["kAlpha"] * F(1000002, 1000000)))
+    assert not normal_constants_ok(dict(C, kZb=C["kBeta"]))
 
 
 def test_theta_error_constants(C):

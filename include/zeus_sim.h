@@ -137,8 +137,9 @@ typedef struct {
   int32_t layout;                    /* schedule of the replay kernel; results
                                         are bit-identical for every value:
                                         0 auto: 3 when the grouped launch fills at most a
-                                          quarter wave, else 2 when R > 2|𝓑| and no cell has a
-                                          window, else 1 (chosen by measurement);
+                                          quarter wave, else 2 when R > 2|𝓑| and either no
+                                          cell has a window or R >= 16|𝓑|, else 1 (chosen by
+                                          measurement);
                                         1 one pass, one thread per trial;
                                         2 two phases: the pruning stage, then the Thompson
                                           stage with trials regrouped by survivor count;

@@ -590,7 +590,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   int best_warps = -1;
   // sized for the kernel that dominates: the Thompson phase when the schedule has two
   // phases (R > 2B), else the one-pass kernel; ties keep the larger block (fewer stagings)
-  const bool two_phase = (s->layout == 2 || (s->layout == 0 && s->wmax == 0)) && std::min(s->R, 2 * B) < s->R;
+  const bool two_phase = (s->layout == 2 || (s->layout == 0 && (s->wmax == 0 || s->R >= 16 * B))) &&
+                         std::min(s->R, 2 * B) < s->R;
   for (int tpb : {128, 64, 32}) {
     const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
     if (bytes > 227 * 1024) continue;
@@ -842,9 +843,12 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
         else zs::thompson_kernel<false, false, false><<<tgrid, 128, m, st>>>(a);
       }
     };
-    // auto: two phases except for windowed launches, where the one-pass kernel measured
-    // faster (CFG4 1.45e10 vs 1.30e10 decisions/s); explicit layouts are honoured
-    const bool two_phase = (s->layout == 2 || (s->layout == 0 && !windowed)) && a.t_split < s->R;
+    // auto: two phases, except for windowed launches with few Thompson recurrences per pruning
+    // recurrence (R < 8 x 2|B|), where the one-pass kernel measured faster (session r02al: CFG4 at
+    // R = 200 two phases 2.08 vs one pass 1.96e10, CFG4 at R = 38 one pass 1.26 vs 1.08e10);
+    // explicit layouts are honoured
+    const bool two_phase = (s->layout == 2 || (s->layout == 0 && (!windowed || s->R >= 16 * s->B))) &&
+                           a.t_split < s->R;
     if (s->group_w > 0) {                    // lane-group layout (latency-bound launches)
       const int tpg = 128 / s->group_w;
       const dim3 ggrid((unsigned)((s->max_shard + tpg - 1) / tpg), (unsigned)nc);

@@ -196,6 +196,8 @@ struct ReplayArgs {
   // replay_kernel's one-pass and exact phase-B schedules: the certified fp32 draw (draw = 0 or 2)
   // instead of the bound screen; its fp32 table follows the residual slots in shared memory
   int cert_draw;
+  // thompson_kernel<…, WIN>'s shared-memory table layout (ThTabLayout, computed on the host)
+  int th_logtab, th_pool, th_bytes, th_pool_smem;
 };
 
 constexpr int kBuckets = 34;      // 2 x popcount of the survivor-pair mask + parity of its lowest pair

@@ -1,8 +1,8 @@
 // thompson.cuh -- the Thompson-sampling phase of the two-phase schedule
 // with the certified fp32 draw of certify.cuh.
 //
-// thompson_kernel<LOG, RK, SREC> runs recurrences t_split..R-1 of every trial of a launch whose
-// cells have no window and no ablation, after replay_kernel's phase A (Alg. 3 pruning) and the
+// thompson_kernel<LOG, RK, SREC, WIN> runs recurrences t_split..R-1 of every trial of a launch whose
+// cells have no ablation, after replay_kernel's phase A (Alg. 3 pruning) and the
 // regroup.  Per decision (Alg. 1, then steps 3-4 as in replay_kernel):
 //   * every survivor quad's Philox block (NC-3) is drawn; both of its Box-Muller pairs are
 //     transformed in fp32 and every arm's theta in fp32 with its error bound (certify.cuh);
@@ -93,12 +93,35 @@ __device__ __forceinline__ U4 philox_from_prefix(const PhiloxPrefix &p, uint32_t
   return c;
 }
 
+// Shared-memory tables of the windowed variant (WIN): the arm constants and the sampler's log
+// table, and the trace pool when it is small; the pseudo-regret and optimum tables are read only
+// on a stopped run's path, from global memory, so many slices (CFG4: 200) cost no residency.
+// The offsets travel in the kernel parameters (ReplayArgs::th_*).
+constexpr int kThPoolSmemMax = 16384;
+struct ThTabLayout {
+  int arms, logtab, pool, bytes;
+  bool pool_smem;
+  __host__ __device__ ThTabLayout(int B, int S, int K) {
+    arms = 0;
+    logtab = TabLayout::align16(B * (int)sizeof(ArmConst));
+    pool = TabLayout::align16(logtab + kLogTab * 16);
+    pool_smem = S * B * K * 4 <= kThPoolSmemMax;
+    bytes = pool_smem ? TabLayout::align16(pool + S * B * K * 4) : pool;
+  }
+};
+#ifndef ZS_WIN_MIN_BLOCKS
+#define ZS_WIN_MIN_BLOCKS 6
+#endif
+
 // SREC (launches of at most a couple of waves, where one warp per scheduler makes the decision's
 // latency the throughput): every survivor's Observe record lives in shared memory for the whole
 // phase ([arm][thread], after the replica words), loaded once at the start and written back at
 // the end, so a decision that moves to another arm waits on a shared-memory load, not on L2.
-template <bool LOG, bool RK, bool SREC>
-__global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
+// WIN: some cell has a window N: each Observe evicts the cost that leaves the arm's
+// window from the HBM ring (loaded as soon as the decision is known) and the posterior uses
+// n = min(count, N), as replay_kernel's windowed path; six blocks per SM (one wave of 10^5 trials).
+template <bool LOG, bool RK, bool SREC, bool WIN>
+__device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
   const int cell = blockIdx.y;
@@ -125,42 +148,52 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
 
   // ---- stage the cell's tables with TMA bulk copies (one elected thread)
   const TabLayout L(a.B, a.S, a.K);
+  const int tab_end = WIN ? a.th_bytes : a.tab_bytes;         // where the per-thread state starts
   if (tid == 0) {
     mbar_init(&mbar, 1);
     const uint32_t p_arm = (a.B * (uint32_t)sizeof(ArmConst) + 15u) & ~15u;
     const uint32_t p_reg = (a.S * a.B * 8u + 15u) & ~15u;
     const uint32_t p_opt = (a.S * 4u + 15u) & ~15u;
     const uint32_t p_pool = (a.S * a.B * a.K * 4u + 15u) & ~15u;
-    mbar_expect_tx(&mbar, p_arm + p_reg + p_opt + p_pool + kLogTab * 16u);
-    tma_bulk_load(smem + L.logtab, a.logtab, kLogTab * 16u, &mbar);
-    tma_bulk_load(smem + L.arms, a.arms + (size_t)cell * a.B, p_arm, &mbar);
-    tma_bulk_load(smem + L.regret, a.regret + (size_t)cell * a.reg_stride, p_reg, &mbar);
-    tma_bulk_load(smem + L.optarm, a.opt_arm + (size_t)cell * a.opt_stride, p_opt, &mbar);
-    tma_bulk_load(smem + L.pool, a.pool, p_pool, &mbar);
+    if constexpr (WIN) {
+      mbar_expect_tx(&mbar, p_arm + (a.th_pool_smem ? p_pool : 0u) + kLogTab * 16u);
+      tma_bulk_load(smem + a.th_logtab, a.logtab, kLogTab * 16u, &mbar);
+      tma_bulk_load(smem, a.arms + (size_t)cell * a.B, p_arm, &mbar);
+      if (a.th_pool_smem) tma_bulk_load(smem + a.th_pool, a.pool, p_pool, &mbar);
+    } else {
+      mbar_expect_tx(&mbar, p_arm + p_reg + p_opt + p_pool + kLogTab * 16u);
+      tma_bulk_load(smem + L.logtab, a.logtab, kLogTab * 16u, &mbar);
+      tma_bulk_load(smem + L.arms, a.arms + (size_t)cell * a.B, p_arm, &mbar);
+      tma_bulk_load(smem + L.regret, a.regret + (size_t)cell * a.reg_stride, p_reg, &mbar);
+      tma_bulk_load(smem + L.optarm, a.opt_arm + (size_t)cell * a.opt_stride, p_opt, &mbar);
+      tma_bulk_load(smem + L.pool, a.pool, p_pool, &mbar);
+    }
   }
   __syncthreads();
   mbar_wait(&mbar, 0);
 
-  const ArmConst *arm = reinterpret_cast<const ArmConst *>(smem + L.arms);
-  const double *regret = reinterpret_cast<const double *>(smem + L.regret);
-  const int32_t *optarm = reinterpret_cast<const int32_t *>(smem + L.optarm);
-  const int32_t *pool = reinterpret_cast<const int32_t *>(smem + L.pool);
-  const double2 *logtab = reinterpret_cast<const double2 *>(smem + L.logtab);
+  const ArmConst *arm = reinterpret_cast<const ArmConst *>(smem + (WIN ? 0 : L.arms));
+  const double *regret = reinterpret_cast<const double *>(smem + L.regret);     // !WIN only
+  const int32_t *optarm = reinterpret_cast<const int32_t *>(smem + L.optarm);   // !WIN only
+  const int32_t *pool = reinterpret_cast<const int32_t *>(smem + (WIN ? a.th_pool : L.pool));
+  const double2 *logtab = reinterpret_cast<const double2 *>(smem + (WIN ? a.th_logtab : L.logtab));
   const int B = a.B, R = a.R, S = a.S, K = a.K;
   // fp32 (mu - ref, sigma) of arms 2k, 2k+1 of this thread: float4 [pair][thread]
-  float4 *s_f = reinterpret_cast<float4 *>(smem + a.tab_bytes);
+  float4 *s_f = reinterpret_cast<float4 *>(smem + tab_end);
   float2 *s_f2 = reinterpret_cast<float2 *>(s_f);         // arm b: s_f2[2 ((b >> 1) TPB + tid) + (b & 1)]
   // the replica words of the current block of four recurrences (NC-3), [thread][4]: one LDS per
   // decision instead of four live registers
-  uint32_t *s_rw = reinterpret_cast<uint32_t *>(smem + a.tab_bytes + (size_t)((((B + 1) >> 1) + 1) & ~1) * 16 * TPB);
+  uint32_t *s_rw = reinterpret_cast<uint32_t *>(smem + tab_end + (size_t)((((B + 1) >> 1) + 1) & ~1) * 16 * TPB);
 
   const bool active = j0 + tid < cp.n;
   const int64_t jj = active ? a.perm[cp.out_off + j0 + tid] : 0;
   const int64_t trial = cp.begin + jj;
   const size_t o = (size_t)(cp.out_off + jj);
   ArmStat *st_g = a.st + o * B;
-  ArmStat *s_rec = reinterpret_cast<ArmStat *>(smem + a.tab_bytes +
+  ArmStat *s_rec = reinterpret_cast<ArmStat *>(smem + tab_end +
                                                (size_t)((((B + 1) >> 1) + 1) & ~1) * 16 * TPB + 16 * (size_t)TPB);
+  const int Nw = WIN ? cp.window : 0;                       // window of this cell (0: none)
+  auto nwin = [&](int cnt) { return (WIN && Nw > 0) ? min(cnt, Nw) : cnt; };
   auto rec = [&](int arm_i) -> ArmStat & {
     if constexpr (SREC) return s_rec[(size_t)arm_i * TPB + tid];
     else return st_g[arm_i];
@@ -204,7 +237,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
     const int lead = (last_b >= 0 && ((ts_set >> last_b) & 1u)) ? last_b : __ffs(ts_set) - 1;
     {
       const ArmStat q = rec(lead);
-      ref = posterior(q.sh, q.S1, q.S2, q.cnt, cp.prec0, cp.pm0).x;
+      ref = posterior(q.sh, q.S1, q.S2, nwin(q.cnt), cp.prec0, cp.pm0).x;
     }
     if (!(fabs(ref) < 1e30)) ref = 0.0;
     c_trial = __double2float_ru(fabs(ref) * 0x1p-52 + 0x1p-120);
@@ -214,7 +247,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
       float2 v = make_float2(3.0e38f, 0.0f);                // (every survivor ran at least twice)
       if ((ts_set >> b) & 1u) {
         const ArmStat q = rec(b);
-        const double2 ms = posterior(q.sh, q.S1, q.S2, q.cnt, cp.prec0, cp.pm0);
+        const double2 ms = posterior(q.sh, q.S1, q.S2, nwin(q.cnt), cp.prec0, cp.pm0);
         const double dm = ms.x - ref;
         v = (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y) : make_float2(0.0f, kInfF);
       }
@@ -231,7 +264,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
   for (int t = a.t_split; t < R; ++t) {
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0, b = 0, hkey = -1;
-    double C = 0.0;
+    double C = 0.0, y_old = 0.0;
     if (S > 1)
       while ((long long)(s + 1) * R <= (long long)t * S) ++s;
     if (active) {
@@ -305,7 +338,7 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
               const int arm_i = 2 * k + h;
               if (!((ts_set >> arm_i) & 1u)) continue;
               const ArmStat q = (arm_i == qc_b) ? qc : rec(arm_i);
-              const double2 ms = posterior(q.sh, q.S1, q.S2, q.cnt, cp.prec0, cp.pm0);
+              const double2 ms = posterior(q.sh, q.S1, q.S2, nwin(q.cnt), cp.prec0, cp.pm0);
               const double th = fma(ms.y, h ? z1 : z0, ms.x);
               if (th < bt) { bt = th; b = arm_i; }
             }
@@ -318,12 +351,16 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
         qc = rec(b);
         qc_b = b;
       }
+      // the windowed Observe's evicted cost, loaded as soon as the decision is known
+      if (WIN && Nw > 0 && qc.cnt >= Nw)
+        y_old = a.st_ring[(o * B + b) * (size_t)a.ring_n + (qc.cnt % Nw)];
       const ArmConst ac = arm[b];
       const int p = ac.pstar;
       const double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;
       // ---------------- step 3: replay one recorded run
       const uint32_t r = __umulhi(s_rw[4 * tid + (t & 3)], (uint32_t)K);
-      const int E = pool[((size_t)s * B + b) * K + r];
+      const int pidx = (s * B + b) * K + (int)r;
+      const int E = (!WIN || a.th_pool_smem) ? pool[pidx] : __ldg(a.pool + pidx);
       const int Erun = E > 0 ? E : a.max_epochs;
       hkey = b * K + (int)r;                               // bin (b, replica) of the row
       const double em1 = (double)(Erun - 1);
@@ -375,20 +412,35 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
         // a stopped run's pseudo-regret and counts (stop | optimal << 8 | Thompson << 16) are read
         // only here (the counted runs take theirs from the histogram fold)
         if (special) {
-          vReg = regret[s * B + b];
-          vPacked = 1 | ((b == optarm[s]) ? (1 << 8) : 0) | (1 << 16);
+          if constexpr (WIN) {                // global: a stopped run's path only
+            vReg = __ldg(a.regret + (size_t)cell * a.reg_stride + s * B + b);
+            vPacked = 1 | ((b == __ldg(a.opt_arm + (size_t)cell * a.opt_stride + s)) ? (1 << 8) : 0) | (1 << 16);
+          } else {
+            vReg = regret[s * B + b];
+            vPacked = 1 | ((b == optarm[s]) ? (1 << 8) : 0) | (1 << 16);
+          }
         }
         curve_accumulate(curves, t, tid & 31, special ? vC : 0.0, special ? vE : 0.0, special ? vT : 0.0,
                          special ? vReg : 0.0, special ? vPacked : 0, a.curve_scale);
       }
     }
     if (active) {
-      // ---------------- Alg. 2 Observe(b, C) with shifted sums (NC-6)
+      // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N (NC-6)
+      int n = qc.cnt;
+      if (WIN && Nw > 0) {
+        if (qc.cnt >= Nw) {                                 // the oldest cost leaves the window
+          const double dy = y_old - qc.sh;
+          qc.S1 = qc.S1 - dy;
+          qc.S2 = qc.S2 - dy * dy;
+          n = Nw - 1;
+        }
+        a.st_ring[(o * B + b) * (size_t)a.ring_n + (qc.cnt % Nw)] = C;
+      }
       const double d = C - qc.sh;
       qc.S1 = qc.S1 + d;
       qc.S2 = qc.S2 + d * d;
       qc.cnt += 1;
-      const double2 ms = posterior(qc.sh, qc.S1, qc.S2, qc.cnt, cp.prec0, cp.pm0);
+      const double2 ms = posterior(qc.sh, qc.S1, qc.S2, n + 1, cp.prec0, cp.pm0);
       const double dm = ms.x - ref;
       s_f2[2 * ((b >> 1) * TPB + tid) + (b & 1)] =
           (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y) : make_float2(0.0f, kInfF);
@@ -441,6 +493,17 @@ __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     if ((tid & 31) == 0 && v) atomicAdd(a.counters + q, v);
   }
+}
+
+// the kernels: the windowed variant asks for six 128-thread blocks per SM (80 registers, no
+// spills: one wave of CFG4's 10^5 trials); the others keep the compiler's choice (96)
+template <bool LOG, bool RK, bool SREC, bool WIN>
+__global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
+  if constexpr (!WIN) thompson_body<LOG, RK, SREC, false>(a);
+}
+template <bool LOG, bool RK, bool SREC>
+__global__ void __launch_bounds__(128, ZS_WIN_MIN_BLOCKS) thompson_win_kernel(ReplayArgs a) {
+  thompson_body<LOG, RK, SREC, true>(a);
 }
 
 }  // namespace zs

@@ -226,6 +226,28 @@ ReplayFn replay_fn(bool windowed, bool log, int phase, bool abl = false, bool rk
   return log ? pick<false, true, false>(phase) : pick<false, false, false>(phase);
 }
 
+#ifndef ZS_WIN_THOMPSON
+#define ZS_WIN_THOMPSON 1
+#endif
+// thompson_kernel<LOG, RK, SREC, WIN> by runtime flags
+typedef void (*ThompsonFn)(zs::ReplayArgs);
+ThompsonFn thompson_fn(bool log, bool rk, bool srec, bool win) {
+  if (win) {
+    if (srec) {
+      if (rk) return log ? zs::thompson_win_kernel<true, true, true> : zs::thompson_win_kernel<false, true, true>;
+      return log ? zs::thompson_win_kernel<true, false, true> : zs::thompson_win_kernel<false, false, true>;
+    }
+    if (rk) return log ? zs::thompson_win_kernel<true, true, false> : zs::thompson_win_kernel<false, true, false>;
+    return log ? zs::thompson_win_kernel<true, false, false> : zs::thompson_win_kernel<false, false, false>;
+  }
+  if (srec) {
+    if (rk) return log ? zs::thompson_kernel<true, true, true, false> : zs::thompson_kernel<false, true, true, false>;
+    return log ? zs::thompson_kernel<true, false, true, false> : zs::thompson_kernel<false, false, true, false>;
+  }
+  if (rk) return log ? zs::thompson_kernel<true, true, false, false> : zs::thompson_kernel<false, true, false, false>;
+  return log ? zs::thompson_kernel<true, false, false, false> : zs::thompson_kernel<false, false, false, false>;
+}
+
 // Dynamic shared memory allowed per launch of fn: the device's opt-in maximum minus the
 // kernel's static shared memory.  Set once to the maximum (the attribute is process-wide),
 // so handles with different footprints can launch the same kernels concurrently.
@@ -634,14 +656,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
       for (int ph = 0; ph < 3; ++ph)
         for (int ab = 0; ab < 3; ++ab)            // ab == 2: the RK kernels
           ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph, ab == 1, ab == 2), s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, false, false>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, false, false>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, true, false>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, true, false>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, false, true>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, false, true>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<false, true, true>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::thompson_kernel<true, true, true>, s->device));
+  for (int f = 0; f < 16; ++f)
+    ZS_CUDA(s, grant_max_smem((const void *)thompson_fn(f & 1, f & 2, f & 4, f & 8), s->device));
   ZS_CUDA(s, grant_group<2>(s->device));
   ZS_CUDA(s, grant_group<4>(s->device));
   ZS_CUDA(s, grant_group<8>(s->device));
@@ -816,32 +832,24 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     };
     // the Thompson phase with the certified fp32 draw unless the run asks for
     // the exact-screen kernel (draw = 1); cells with a window or an ablation keep replay_kernel
-    const bool certified = !windowed && !s->any_ablation && s->draw != 1;
+    const bool certified = !s->any_ablation && s->draw != 1 && (!windowed || ZS_WIN_THOMPSON);
     a.key_quads = certified ? 1 : 0;
     a.force_exact = s->draw == 2 ? 1 : 0;
     auto thompson_launch = [&]() {
       const dim3 tgrid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
-      const size_t tsmem = (size_t)s->tab_bytes + (size_t)128 * (((((s->B + 1) / 2) + 1) & ~1) * 16 + 16);
+      size_t tab = (size_t)s->tab_bytes;
+      if (windowed) {                          // the compact table layout of the WIN variant
+        const zs::ThTabLayout TL(s->B, s->S, s->K);
+        a.th_logtab = TL.logtab; a.th_pool = TL.pool; a.th_bytes = TL.bytes; a.th_pool_smem = TL.pool_smem;
+        tab = (size_t)TL.bytes;
+      }
+      const size_t tsmem = tab + (size_t)128 * (((((s->B + 1) / 2) + 1) & ~1) * 16 + 16);
       // launches of at most two blocks per SM keep the survivors' records in shared memory
       // (thompson.cuh, SREC): there the decision's latency is the throughput
       const size_t rec_bytes = (size_t)128 * s->B * sizeof(zs::ArmStat);
       const bool srec = (int64_t)tgrid.x * tgrid.y <= 2 * (int64_t)s->sms && tsmem + rec_bytes <= 100 * 1024;
       const size_t m = tsmem + (srec ? rec_bytes : 0);
-      if (srec) {
-        if (rk) {
-          if (s->log_mode) zs::thompson_kernel<true, true, true><<<tgrid, 128, m, st>>>(a);
-          else zs::thompson_kernel<false, true, true><<<tgrid, 128, m, st>>>(a);
-        } else {
-          if (s->log_mode) zs::thompson_kernel<true, false, true><<<tgrid, 128, m, st>>>(a);
-          else zs::thompson_kernel<false, false, true><<<tgrid, 128, m, st>>>(a);
-        }
-      } else if (rk) {
-        if (s->log_mode) zs::thompson_kernel<true, true, false><<<tgrid, 128, m, st>>>(a);
-        else zs::thompson_kernel<false, true, false><<<tgrid, 128, m, st>>>(a);
-      } else {
-        if (s->log_mode) zs::thompson_kernel<true, false, false><<<tgrid, 128, m, st>>>(a);
-        else zs::thompson_kernel<false, false, false><<<tgrid, 128, m, st>>>(a);
-      }
+      thompson_fn(s->log_mode, rk, srec, windowed)<<<tgrid, 128, m, st>>>(a);
     };
     // auto: two phases, except for windowed launches with few Thompson recurrences per pruning
     // recurrence (R < 8 x 2|B|), where the one-pass kernel measured faster (session r02al: CFG4 at

@@ -12,7 +12,7 @@ from paper_2208_06102_b200.zeus_sim import Simulation
 # ablations, variant readings, concurrent submissions
 # (draw 0: the certified Thompson kernel; 1: the exact-screen phase B; 2: certified, all fallbacks)
 runs = [("cfg5", 600, 0, 0), ("cfg5", 300, 2, 1), ("cfg5", 300, 2, 2), ("cfg3", 300, 0, 0),
-        ("cfg4_38", 500, 0, 0), ("cfg1", 100, 3, 0), ("f1", 200, 0, 0), ("f2", 200, 0, 0),
+        ("cfg4", 400, 0, 0), ("cfg4", 300, 0, 2), ("cfg4_38", 500, 0, 0), ("cfg1", 100, 3, 0), ("f1", 200, 0, 0), ("f2", 200, 0, 0),
         ("f2v", 200, 0, 0), ("f3", 200, 0, 0)]
 for name, trials, layout, draw in runs:
     for job in synth.config(name, trials=trials)[:2]:

@@ -1,5 +1,5 @@
 """Per-region warp-stall samples of the Thompson-phase kernel from an ncu report with
-imported source (tools/session_ncu_src.sh).  usage: python tools/ncu_regions.py <report.ncu-rep>"""
+imported source (tools/sessions/session_ncu_src.sh).  usage: python tools/ncu_regions.py <report.ncu-rep>"""
 import collections
 import csv
 import io

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of variant libraries over several configs (short benches), plus the GPU suite on the first.
-# usage: tools/session_cfgab.sh <tag> "<configs>" <variants...>
+# usage: tools/sessions/session_cfgab.sh <tag> "<configs>" <variants...>
 TAG=$1; CFGS=$2; shift 2
 OUT=gpurun_out/$TAG; mkdir -p $OUT
 ZEUS_SIM_LIB=$PWD/build/libzs_$1.so timeout -s KILL 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_$1.log 2>&1; echo "pytest[$1] rc=$? $(tail -1 $OUT/pytest_$1.log)"

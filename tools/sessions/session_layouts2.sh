@@ -1,6 +1,6 @@
 #!/bin/bash
 # Layout check of the latency-bound configs on the current build: auto (0), one pass (1),
-# two phases (2), lane groups (3).   usage: tools/session_layouts2.sh <tag>
+# two phases (2), lane groups (3).   usage: tools/sessions/session_layouts2.sh <tag>
 set -u
 OUT=gpurun_out/$1; mkdir -p $OUT
 for c in cfg2 f1 f2 cfg4 cfg1; do

@@ -1,6 +1,6 @@
 #!/bin/bash
 # ncu --set full of the Thompson-phase kernel for each variant library in build/
-# usage: tools/session_ncu_ab.sh <tag> <variant...>
+# usage: tools/sessions/session_ncu_ab.sh <tag> <variant...>
 TAG=$1; shift
 OUT=gpurun_out/$TAG; mkdir -p $OUT
 for v in "$@"; do

@@ -1,6 +1,6 @@
 #!/bin/bash
 # ncu --set full of the Thompson-phase kernel with source-level stall sampling (2M trials of CFG5).
-# usage: tools/session_ncu_src.sh <tag> [lib variant]
+# usage: tools/sessions/session_ncu_src.sh <tag> [lib variant]
 set -u
 TAG=$1; V=${2:-}
 OUT=gpurun_out/$TAG; mkdir -p $OUT

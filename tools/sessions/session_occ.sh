@@ -1,6 +1,6 @@
 #!/bin/bash
 # Occupancy lever probe: the same kernel under register caps, on a config whose shared memory
-# does not limit residency (CFG3, B <= 9) and on CFG5.  usage: tools/session_occ.sh <tag> <config> <variant...>
+# does not limit residency (CFG3, B <= 9) and on CFG5.  usage: tools/sessions/session_occ.sh <tag> <config> <variant...>
 set -u
 TAG=$1; CFG=$2; shift 2
 OUT=gpurun_out/$TAG; mkdir -p $OUT

@@ -1,6 +1,6 @@
 #!/bin/bash
 # GPU parity suite against one variant library, then an A/B bench of variants.
-# usage: tools/session_var.sh <tag> <variant-under-test> <ab variants...>
+# usage: tools/sessions/session_var.sh <tag> <variant-under-test> <ab variants...>
 TAG=$1; V=$2; shift 2
 OUT=gpurun_out/$TAG; mkdir -p $OUT
 ZEUS_SIM_LIB=$PWD/build/libzs_$V.so timeout -s KILL 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_$V.log 2>&1; echo "pytest[$V] rc=$? $(tail -1 $OUT/pytest_$V.log)"

@@ -144,7 +144,12 @@ typedef struct {
                                         2 two phases: the pruning stage, then the Thompson
                                           stage with trials regrouped by survivor count;
                                         3 one pass, a lane group of W = 2/4/8 lanes per trial
-                                          (the draw split across lanes, shuffle argmin) */
+                                          (the draw split across lanes, shuffle argmin);
+                                        4 two phases with the early split: the pruning phase
+                                          stops each trial at its first pure Thompson decision
+                                          and the Thompson phase starts it there (auto takes it
+                                          for the certified draw when R < 40|𝓑| and the launch
+                                          exceeds two blocks per SM) */
   int32_t graph;                     /* 0: zeus_sim_run enqueues its kernels one by one;
                                         1: the first run captures them into a CUDA graph (on an
                                           internal stream) and every run launches that graph on

@@ -193,6 +193,10 @@ struct ReplayArgs {
   // then groups the lanes by survivor-quad count; force_exact sends every draw to its exact
   // fp64 fallback (a test of that path)
   int key_quads, force_exact;
+  // early split (thompson_kernel only): phase A stops each lane at its first pure Thompson
+  // decision (pruning over, every survivor observed twice) and the Thompson phase starts that
+  // lane there (Carry::t0), so phase A's warps never mix pruning and sampling lanes
+  int early_split;
   // replay_kernel's one-pass and exact phase-B schedules: the certified fp32 draw (draw = 0 or 2)
   // instead of the bound screen; its fp32 table follows the residual slots in shared memory
   int cert_draw;
@@ -200,7 +204,10 @@ struct ReplayArgs {
   int th_logtab, th_pool, th_bytes, th_pool_smem;
 };
 
-constexpr int kBuckets = 34;      // 2 x popcount of the survivor-pair mask + parity of its lowest pair
+// regroup keys: 2 x popcount of the survivor-pair mask + parity of its lowest pair (exact phase B),
+// or quads x kT0Keys + the recurrence the lane's Thompson phase starts at (thompson_kernel, t0 <= 2B)
+constexpr int kT0Keys = 65;
+constexpr int kBuckets = 9 * kT0Keys;
 #ifndef ZS_REGROUP_WINDOW
 #define ZS_REGROUP_WINDOW 8192
 #endif
@@ -215,8 +222,8 @@ __device__ __forceinline__ uint32_t quads_of(uint32_t pairs) {
 
 // phase-B grouping key: lanes with the same number of survivor pairs and the same parity of
 // the lowest one draw the same number of Philox blocks at the same loop steps
-__device__ __forceinline__ int regroup_key(uint32_t pairs, int key_quads) {
-  if (key_quads) return __popc(quads_of(pairs));          // thompson_kernel: quads per decision
+__device__ __forceinline__ int regroup_key(uint32_t pairs, int key_quads, int t0) {
+  if (key_quads) return __popc(quads_of(pairs)) * kT0Keys + t0;   // thompson_kernel: quads, start
   return pairs ? 2 * __popc(pairs) + ((__ffs(pairs) - 1) & 1) : 0;
 }
 
@@ -225,7 +232,7 @@ struct __align__(16) ArmStat {    // Observe state of one arm of one trial (NC-6
   int32_t cnt, pad;               // observations ever
 };
 
-// per-trial scalar state carried from phase A to phase B (88 B)
+// per-trial scalar state carried from phase A to phase B (96 B)
 struct Carry {
   double best, totC, totE, totT;
   unsigned long long dig;
@@ -233,7 +240,8 @@ struct Carry {
   int32_t nstop, last_b;
   uint32_t n_sampled, n_prune, n_forced, n_recomp;
   uint32_t n_cert, n_fall;        // phase A's certified draws and their exact fallbacks
-};
+  int32_t t0, pad;                // the lane's first Thompson-phase recurrence (t_split, or earlier
+};                                // under ReplayArgs::early_split)
 
 // shared-memory table region of one block: [ArmConst B][regret S*B][opt_arm S][pool S*B*K]
 struct TabLayout {
@@ -535,7 +543,15 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   // repeats its arm, and then the decision needs no load of the record (same values)
   ArmStat qc{0.0, 0.0, 0.0, 0, 0};
   int qc_b = -1;
+  bool live = active;                                       // phase A under early_split: until t0
+  int t0 = t_end;
   for (int t = t_begin; t < t_end; ++t) {
+    if (PHASE == 1 && a.early_split) {
+      // the first pure Thompson decision (pruning over, every survivor observed twice) is the
+      // Thompson phase's: this lane stops here and resumes there (thompson_kernel, Carry::t0)
+      if (live && in_ts && !(ts_set & ~mature)) { live = false; t0 = t; }
+      if (!__any_sync(0xffffffffu, live)) break;
+    }
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0;
     // carried from the decision to the Observe, which runs after the curve reduction so
@@ -547,7 +563,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     double C = 0.0;
     if (S > 1)                                              // no 64-bit division per decision
       while ((long long)(s + 1) * R <= (long long)t * S) ++s;
-    if (active) {
+    if (live) {
       // step 3's replica words: one Philox block per four recurrences (NC-3), refreshed when
       // t enters a new block of four; warp-uniform because all lanes share t
       if ((t & 3) == 0 || t == t_begin) rw = replica_words_c(trial, t);
@@ -844,15 +860,15 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     if constexpr (kHist) {
       // a run that is not stopped is counted in its (b, replica) bin (one predicated RED); the
       // rare stopped runs (charged the continuous threshold) take the fixed-point sums
-      const bool special = active && (vPacked & 1);
-      if (active && !special) red_add_u32(hist + (size_t)t * a.nhslot * HB + hkey, 1u);
+      const bool special = live && (vPacked & 1);
+      if (live && !special) red_add_u32(hist + (size_t)t * a.nhslot * HB + hkey, 1u);
       if (__any_sync(0xffffffffu, special))
         curve_accumulate(curves, t, tid & 31, special ? vC : 0.0, special ? vE : 0.0, special ? vT : 0.0,
                          special ? vReg : 0.0, special ? vPacked : 0, a.curve_scale);
     } else {
       curve_accumulate(curves, t, tid & 31, vC, vE, vT, vReg, vPacked, a.curve_scale);
     }
-    if (active) {
+    if (live) {
       // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N
       {
         const ArmStat &qr = qc;                             // the record (see the decision)
@@ -902,8 +918,10 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
       c.nstop = nstop; c.last_b = last_b;
       c.n_sampled = n_sampled; c.n_prune = n_prune; c.n_forced = n_forced; c.n_recomp = n_recomp;
       c.n_cert = n_cert; c.n_fall = n_fall;
+      c.t0 = t0; c.pad = 0;
       a.carry[o] = c;
-      atomicAdd(&a.bucket[((size_t)cell * a.nwin + jj / kRegroupWindow) * kBuckets + regroup_key(ts_pairs, a.key_quads)], 1);
+      atomicAdd(&a.bucket[((size_t)cell * a.nwin + jj / kRegroupWindow) * kBuckets +
+                          regroup_key(ts_pairs, a.key_quads, a.early_split ? t0 : 0)], 1);
     }
     return;
   }
@@ -1249,15 +1267,24 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
   }
 }
 
-// bucket offsets: exclusive scan of each (cell, window) histogram, offset by the window base
+// bucket offsets: exclusive scan of each (cell, window) histogram, offset by the window base; one
+// warp per (cell, window), 32 buckets per step
 __global__ void bucket_scan_kernel(int32_t *bucket, int ncells, int nwin) {
-  const int64_t cw = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (cw >= (int64_t)ncells * nwin) return;
+  const int64_t cw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (cw >= (int64_t)ncells * nwin) return;                 // warp-uniform
   int run = (int)(cw % nwin) * kRegroupWindow;
-  for (int k = 0; k < kBuckets; ++k) {
-    const int c = bucket[cw * kBuckets + k];
-    bucket[cw * kBuckets + k] = run;
-    run += c;
+  for (int k0 = 0; k0 < kBuckets; k0 += 32) {
+    const int k = k0 + lane;
+    const int c = k < kBuckets ? bucket[cw * kBuckets + k] : 0;
+    int x = c;                                              // inclusive scan over the lanes
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, off);
+      if (lane >= off) x += y;
+    }
+    if (k < kBuckets) bucket[cw * kBuckets + k] = run + x - c;
+    run += __shfl_sync(0xffffffffu, x, 31);
   }
 }
 
@@ -1270,29 +1297,32 @@ constexpr int kScatterTile = 256;
 static_assert(kRegroupWindow % kScatterTile == 0, "a tile must not straddle a regroup window");
 __global__ void __launch_bounds__(kScatterTile) bucket_scatter_kernel(const CellParam *cells, const Carry *carry,
                                                                       int32_t *bucket, int32_t *perm, int ncells,
-                                                                      int B, int nwin, int key_quads) {
+                                                                      int B, int nwin, int key_quads,
+                                                                      int early_split) {
   __shared__ int s_cnt[kBuckets], s_base[kBuckets];
   const int cell = blockIdx.y;
   const CellParam cp = cells[cell];
   if (cp.policy != 0 || cp.conc) return;
   const int64_t ntiles = (cp.n + kScatterTile - 1) / kScatterTile;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    if (threadIdx.x < kBuckets) s_cnt[threadIdx.x] = 0;
+    for (int k = threadIdx.x; k < kBuckets; k += kScatterTile) s_cnt[k] = 0;
     __syncthreads();
     const int64_t j = tile * kScatterTile + threadIdx.x;
     int key = -1, rank = 0;
     if (j < cp.n) {
-      const uint32_t ts_set = carry[cp.out_off + j].ts_set;
+      const Carry &cj = carry[cp.out_off + j];
+      const uint32_t ts_set = cj.ts_set;
       uint32_t pairs = 0;
       for (int k = 0; 2 * k < B; ++k)
         if ((ts_set >> (2 * k)) & 3u) pairs |= 1u << k;
-      key = regroup_key(pairs, key_quads);
+      key = regroup_key(pairs, key_quads, early_split ? cj.t0 : 0);
       rank = atomicAdd(&s_cnt[key], 1);
     }
     __syncthreads();
-    if (threadIdx.x < kBuckets && s_cnt[threadIdx.x] > 0)
-      s_base[threadIdx.x] = atomicAdd(&bucket[((size_t)cell * nwin + (tile * kScatterTile) / kRegroupWindow) * kBuckets +
-                                              threadIdx.x], s_cnt[threadIdx.x]);
+    for (int k = threadIdx.x; k < kBuckets; k += kScatterTile)
+      if (s_cnt[k] > 0)
+        s_base[k] = atomicAdd(&bucket[((size_t)cell * nwin + (tile * kScatterTile) / kRegroupWindow) * kBuckets + k],
+                              s_cnt[k]);
     __syncthreads();
     if (key >= 0) perm[cp.out_off + s_base[key] + rank] = (int32_t)j;
     __syncthreads();                                        // s_cnt is reset by the next tile

@@ -120,7 +120,9 @@ struct ThTabLayout {
 // WIN: some cell has a window N: each Observe evicts the cost that leaves the arm's
 // window from the HBM ring (loaded as soon as the decision is known) and the posterior uses
 // n = min(count, N), as replay_kernel's windowed path; six blocks per SM (one wave of 10^5 trials).
-template <bool LOG, bool RK, bool SREC, bool WIN>
+// EARLY (ReplayArgs::early_split): phase A stopped each lane at its first pure Thompson decision
+// (Carry::t0 <= t_split); the warp starts at its lanes' earliest t0 and a lane idles until its own.
+template <bool LOG, bool RK, bool SREC, bool WIN, bool EARLY>
 __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t mbar;
@@ -203,8 +205,12 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   const int HB = 4 * B * K;
   // counted runs of class (Thompson decision, no profiling), row t_split; one row per t
   const size_t hstride = (size_t)a.nhslot * HB;
+  // EARLY: this lane's first recurrence here (an inactive lane: never), the warp's first (lanes
+  // were grouped by t0 within their quad count, so a warp's lanes mostly share it)
+  const int t0 = EARLY ? (active ? a.carry[o].t0 : 0x7fffffff) : a.t_split;
+  const int tw = EARLY ? min(R, __reduce_min_sync(0xffffffffu, t0)) : a.t_split;
   uint32_t *hrow = a.hist + ((size_t)cell * R * a.nhslot + (warp_global % a.nhslot)) * (size_t)HB +
-                   (size_t)a.t_split * hstride + 2 * B * K;
+                   (size_t)tw * hstride + 2 * B * K;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const float kInfF = __int_as_float(0x7f800000);
 
@@ -255,20 +261,25 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
     }
   }
 
+  if (EARLY && active && (t0 & 3) != 0 && t0 < R) {         // the replica block holding t0
+    const U4 rw = replica_words_c(trial, t0);
+    reinterpret_cast<uint4 *>(s_rw)[tid] = make_uint4(rw.x, rw.y, rw.z, rw.w);
+  }
   int s = 0;
   ArmStat qc{0.0, 0.0, 0.0, 0, 0};
   int qc_b = -1;
 #if ZS_PHILOX_PREFIX
   const uint32_t tlo = (uint32_t)trial, thi = (uint32_t)((uint64_t)trial >> 32);
 #endif
-  for (int t = a.t_split; t < R; ++t) {
+  for (int t = tw; t < R; ++t) {
+    const bool live = EARLY ? t >= t0 : active;             // this lane's trial decides at t
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0, b = 0, hkey = -1;
     double C = 0.0, y_old = 0.0;
     if (S > 1)
       while ((long long)(s + 1) * R <= (long long)t * S) ++s;
-    if (active) {
-      if ((t & 3) == 0 || t == a.t_split) {
+    if (live) {
+      if ((t & 3) == 0 || (!EARLY && t == a.t_split)) {
         const U4 rw = replica_words_c(trial, t);
         reinterpret_cast<uint4 *>(s_rw)[tid] = make_uint4(rw.x, rw.y, rw.z, rw.w);
       }
@@ -403,9 +414,9 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
       vPacked = stopped ? 1 : 0;            // the rest of a stopped run's curve values below
     }
     {
-      const bool special = active && (vPacked & 1);
+      const bool special = live && (vPacked & 1);
 #ifndef ZS_DIAG_NOHIST
-      if (active && !special) red_add_u32(hrow + hkey, 1u);
+      if (live && !special) red_add_u32(hrow + hkey, 1u);
 #endif
       hrow += hstride;
       if (__any_sync(0xffffffffu, special)) {
@@ -424,7 +435,7 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
                          special ? vReg : 0.0, special ? vPacked : 0, a.curve_scale);
       }
     }
-    if (active) {
+    if (live) {
       // ---------------- Alg. 2 Observe(b, C) with shifted sums and window N (NC-6)
       int n = qc.cnt;
       if (WIN && Nw > 0) {
@@ -462,7 +473,7 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   // counters: the method's events (as replay_kernel), then the work: [9] fp64 transforms
   // (fallback draws), [10] Philox blocks, [11] fp32 pairs, [12] certified, [13] fallbacks
   // (phase A's Thompson draws, carried in n_sampled, are full fp64 draws: counted in [9], [10])
-  const uint32_t nB = active ? (uint32_t)(R - a.t_split) : 0u;   // phase-B decisions = draws
+  const uint32_t nB = active ? (uint32_t)(R - (EARLY ? a.carry[o].t0 : a.t_split)) : 0u;   // draws here
   uint32_t n_cert = nB - n_fall;
   // phase A's draws: certified (fp32 pairs, one block per quad) or full fp64 (its fallbacks and,
   // without the certified draw, all of them)
@@ -497,13 +508,13 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
 
 // the kernels: the windowed variant asks for six 128-thread blocks per SM (80 registers, no
 // spills: one wave of CFG4's 10^5 trials); the others keep the compiler's choice (96)
-template <bool LOG, bool RK, bool SREC, bool WIN>
+template <bool LOG, bool RK, bool SREC, bool WIN, bool EARLY = false>
 __global__ void ZS_TH_BOUNDS thompson_kernel(ReplayArgs a) {
-  if constexpr (!WIN) thompson_body<LOG, RK, SREC, false>(a);
+  if constexpr (!WIN) thompson_body<LOG, RK, SREC, false, EARLY>(a);
 }
-template <bool LOG, bool RK, bool SREC>
+template <bool LOG, bool RK, bool SREC, bool EARLY = false>
 __global__ void __launch_bounds__(128, ZS_WIN_MIN_BLOCKS) thompson_win_kernel(ReplayArgs a) {
-  thompson_body<LOG, RK, SREC, true>(a);
+  thompson_body<LOG, RK, SREC, true, EARLY>(a);
 }
 
 }  // namespace zs

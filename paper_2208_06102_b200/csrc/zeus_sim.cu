@@ -226,12 +226,23 @@ ReplayFn replay_fn(bool windowed, bool log, int phase, bool abl = false, bool rk
   return log ? pick<false, true, false>(phase) : pick<false, false, false>(phase);
 }
 
+#ifndef ZS_EARLY_SPLIT
+#define ZS_EARLY_SPLIT 1        // phase A stops each lane at its first pure Thompson decision
+#endif
 #ifndef ZS_WIN_THOMPSON
 #define ZS_WIN_THOMPSON 1
 #endif
 // thompson_kernel<LOG, RK, SREC, WIN> by runtime flags
 typedef void (*ThompsonFn)(zs::ReplayArgs);
-ThompsonFn thompson_fn(bool log, bool rk, bool srec, bool win) {
+ThompsonFn thompson_fn(bool log, bool rk, bool srec, bool win, bool early = false) {
+  if (early && !srec) {               // the early split (phase A stopped each lane at its t0)
+    if (win) {
+      if (rk) return log ? zs::thompson_win_kernel<true, true, false, true> : zs::thompson_win_kernel<false, true, false, true>;
+      return log ? zs::thompson_win_kernel<true, false, false, true> : zs::thompson_win_kernel<false, false, false, true>;
+    }
+    if (rk) return log ? zs::thompson_kernel<true, true, false, false, true> : zs::thompson_kernel<false, true, false, false, true>;
+    return log ? zs::thompson_kernel<true, false, false, false, true> : zs::thompson_kernel<false, false, false, false, true>;
+  }
   if (win) {
     if (srec) {
       if (rk) return log ? zs::thompson_win_kernel<true, true, true> : zs::thompson_win_kernel<false, true, true>;
@@ -337,7 +348,7 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     if (opts->shard_begin < 0) E.add(ZEUS_E_INVALID, "shard_begin < 0");
     if (opts->shard_end >= 0 && opts->shard_end < opts->shard_begin) E.add(ZEUS_E_INVALID, "shard_end < shard_begin");
     if (opts->log_mode != 0 && opts->log_mode != 1) E.add(ZEUS_E_INVALID, "log_mode must be 0 or 1");
-    if (opts->layout < 0 || opts->layout > 3) E.add(ZEUS_E_INVALID, "layout must be 0, 1, 2 or 3");
+    if (opts->layout < 0 || opts->layout > 4) E.add(ZEUS_E_INVALID, "layout must be 0, 1, 2, 3 or 4");
     if (opts->graph != 0 && opts->graph != 1) E.add(ZEUS_E_INVALID, "graph must be 0 or 1");
     if (opts->draw < 0 || opts->draw > 2) E.add(ZEUS_E_INVALID, "draw must be 0, 1 or 2");
   }
@@ -612,7 +623,7 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   int best_warps = -1;
   // sized for the kernel that dominates: the Thompson phase when the schedule has two
   // phases (R > 2B), else the one-pass kernel; ties keep the larger block (fewer stagings)
-  const bool two_phase = (s->layout == 2 || (s->layout == 0 && (s->wmax == 0 || s->R >= 16 * B))) &&
+  const bool two_phase = (s->layout == 2 || s->layout == 4 || (s->layout == 0 && (s->wmax == 0 || s->R >= 16 * B))) &&
                          std::min(s->R, 2 * B) < s->R;
   for (int tpb : {128, 64, 32}) {
     const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
@@ -656,8 +667,8 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
       for (int ph = 0; ph < 3; ++ph)
         for (int ab = 0; ab < 3; ++ab)            // ab == 2: the RK kernels
           ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph, ab == 1, ab == 2), s->device));
-  for (int f = 0; f < 16; ++f)
-    ZS_CUDA(s, grant_max_smem((const void *)thompson_fn(f & 1, f & 2, f & 4, f & 8), s->device));
+  for (int f = 0; f < 32; ++f)
+    ZS_CUDA(s, grant_max_smem((const void *)thompson_fn(f & 1, f & 2, f & 4, f & 8, f & 16), s->device));
   ZS_CUDA(s, grant_group<2>(s->device));
   ZS_CUDA(s, grant_group<4>(s->device));
   ZS_CUDA(s, grant_group<8>(s->device));
@@ -835,27 +846,34 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     const bool certified = !s->any_ablation && s->draw != 1 && (!windowed || ZS_WIN_THOMPSON);
     a.key_quads = certified ? 1 : 0;
     a.force_exact = s->draw == 2 ? 1 : 0;
+    const dim3 tgrid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
+    size_t tab = (size_t)s->tab_bytes;
+    if (windowed) {                            // the compact table layout of the WIN variant
+      const zs::ThTabLayout TL(s->B, s->S, s->K);
+      a.th_logtab = TL.logtab; a.th_pool = TL.pool; a.th_bytes = TL.bytes; a.th_pool_smem = TL.pool_smem;
+      tab = (size_t)TL.bytes;
+    }
+    const size_t tsmem = tab + (size_t)128 * (((((s->B + 1) / 2) + 1) & ~1) * 16 + 16);
+    // launches of at most two blocks per SM keep the survivors' records in shared memory
+    // (thompson.cuh, SREC): there the decision's latency is the throughput
+    const size_t rec_bytes = (size_t)128 * s->B * sizeof(zs::ArmStat);
+    const bool srec = s->layout != 4 && (int64_t)tgrid.x * tgrid.y <= 2 * (int64_t)s->sms &&
+                      tsmem + rec_bytes <= 100 * 1024;
+    // early split: phase A stops each lane at its first pure Thompson decision and
+    // the Thompson phase starts it there, when the pruning stage is a large share of the run
+    // (R < 40 |B|, i.e. fewer than 20 Thompson recurrences per pruning recurrence) and the launch
+    // is not a small SREC one.  Measured (session r02bc): CFG3 +2.8 %, CFG4 +2 %; CFG5 (R = 62 |B|)
+    // -0.8 %, CFG2 (SREC) -0.7 %, so those keep the full phase A.  Layout 4 forces it.
+    a.early_split = certified && ZS_EARLY_SPLIT && (s->layout == 4 || (s->layout == 0 && !srec && s->R < 40 * s->B)) ? 1 : 0;
     auto thompson_launch = [&]() {
-      const dim3 tgrid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
-      size_t tab = (size_t)s->tab_bytes;
-      if (windowed) {                          // the compact table layout of the WIN variant
-        const zs::ThTabLayout TL(s->B, s->S, s->K);
-        a.th_logtab = TL.logtab; a.th_pool = TL.pool; a.th_bytes = TL.bytes; a.th_pool_smem = TL.pool_smem;
-        tab = (size_t)TL.bytes;
-      }
-      const size_t tsmem = tab + (size_t)128 * (((((s->B + 1) / 2) + 1) & ~1) * 16 + 16);
-      // launches of at most two blocks per SM keep the survivors' records in shared memory
-      // (thompson.cuh, SREC): there the decision's latency is the throughput
-      const size_t rec_bytes = (size_t)128 * s->B * sizeof(zs::ArmStat);
-      const bool srec = (int64_t)tgrid.x * tgrid.y <= 2 * (int64_t)s->sms && tsmem + rec_bytes <= 100 * 1024;
       const size_t m = tsmem + (srec ? rec_bytes : 0);
-      thompson_fn(s->log_mode, rk, srec, windowed)<<<tgrid, 128, m, st>>>(a);
+      thompson_fn(s->log_mode, rk, srec, windowed, a.early_split != 0)<<<tgrid, 128, m, st>>>(a);
     };
     // auto: two phases, except for windowed launches with few Thompson recurrences per pruning
     // recurrence (R < 8 x 2|B|), where the one-pass kernel measured faster (session r02al: CFG4 at
     // R = 200 two phases 2.08 vs one pass 1.96e10, CFG4 at R = 38 one pass 1.26 vs 1.08e10);
     // explicit layouts are honoured
-    const bool two_phase = (s->layout == 2 || (s->layout == 0 && (!windowed || s->R >= 16 * s->B))) &&
+    const bool two_phase = (s->layout == 2 || s->layout == 4 || (s->layout == 0 && (!windowed || s->R >= 16 * s->B))) &&
                            a.t_split < s->R;
     if (s->group_w > 0) {                    // lane-group layout (latency-bound launches)
       const int tpg = 128 / s->group_w;
@@ -874,11 +892,11 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
 
       replay_launch(1);
       ZS_CUDA(s, cudaGetLastError());
-      zs::bucket_scan_kernel<<<(unsigned)((nc * (int64_t)s->nwin + 127) / 128), 128, 0, st>>>(a.bucket, nc, s->nwin);
+      zs::bucket_scan_kernel<<<(unsigned)((nc * (int64_t)s->nwin * 32 + 127) / 128), 128, 0, st>>>(a.bucket, nc, s->nwin);
       ZS_CUDA(s, cudaGetLastError());
       const unsigned sx = (unsigned)std::min<int64_t>((s->max_shard + zs::kScatterTile - 1) / zs::kScatterTile, 1184);
       zs::bucket_scatter_kernel<<<dim3(std::max(1u, sx), (unsigned)nc), zs::kScatterTile, 0, st>>>(
-          a.cells, a.carry, a.bucket, a.perm, nc, s->B, s->nwin, a.key_quads);
+          a.cells, a.carry, a.bucket, a.perm, nc, s->B, s->nwin, a.key_quads, a.early_split);
       ZS_CUDA(s, cudaGetLastError());
       if (certified) thompson_launch();
       else replay_launch(2);

@@ -197,7 +197,7 @@ def _random_trace(rng, B, P, S, K, fail=0.2):
     (17, 5, 2, 3, 0, 2.0, 150, 60),       # odd arm count, two phases, two slices
     (3, 4, 1, 2, 0, math.inf, 130, 30),   # two phases, two pairs, no early stop
 ])
-@pytest.mark.parametrize("layout,draw", [(0, 0), (0, 2), (3, 0)])
+@pytest.mark.parametrize("layout,draw", [(0, 0), (0, 2), (3, 0), (4, 0)])
 def test_random_traces_edge_cases(zs, oracle, B, P, S, K, window, beta, trials, R, layout, draw):
     rng = np.random.default_rng(B * 1000 + P)
     w = _random_trace(rng, B, P, S, K)
@@ -271,11 +271,11 @@ def test_errors_are_reported(zs):
 @pytest.mark.parametrize("name", ["cfg1", "cfg4_38", "cfg5"])
 def test_schedules_bit_identical(zs, oracle, name):
     """layout 1 (one pass, thread per trial), layout 2 (pruning phase, regroup, Thompson
-    phase) and layout 3 (lane group per trial) give the same bits for every trial and
-    decision."""
+    phase), layout 3 (lane group per trial) and layout 4 (layout 2 with the early split) give
+    the same bits for every trial and decision."""
     (job,) = synth.config(name, trials=2000 if name != "cfg5" else 700)
     outs = [run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True, layout=l, draw=d)
-            for l, d in ((1, 0), (2, 1), (3, 0), (2, 0), (2, 2))]
+            for l, d in ((1, 0), (2, 1), (3, 0), (2, 0), (2, 2), (4, 0), (4, 2))]
     for o in outs[1:]:
         for k in ("log", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop", "final_arm"):
             assert np.array_equal(outs[0][k], o[k]), k
@@ -284,7 +284,7 @@ def test_schedules_bit_identical(zs, oracle, name):
     # evaluated work: lane groups transform every survivor pair (each with its own Philox
     # block); the bound screen of the one-pass and Thompson-phase kernels
     # transforms at most as many, and far fewer once the posteriors separate
-    c1, c2, c3, c4, c5 = (o["counters"] for o in outs)
+    c1, c2, c3, c4, c5, c6, c7 = (o["counters"] for o in outs)
     assert c3[9] == c3[2] and c3[10] == c3[2]
     for c in (c1, c2):
         assert c[9] <= c[2] and c[10] >= c[8]
@@ -295,6 +295,7 @@ def test_schedules_bit_identical(zs, oracle, name):
     # (windowed cells take it in replay_kernel's exact phase B, the others in thompson_kernel)
     ts_b = c4[12] + c4[13]
     assert ts_b > 0 and c5[12] == 0 and c5[13] == ts_b
+    assert c6[12] + c6[13] == ts_b and c7[12] == 0 and c7[13] == ts_b   # early split: same draws
     assert c4[13] <= 0.01 * ts_b
     assert c1[12] + c1[13] > 0                  # the one-pass kernel certifies too (draw 0)
     assert c2[12] + c2[13] == 0                 # draw 1: the exact screen only
@@ -453,7 +454,7 @@ def test_round_key_kernels_match_multicell_launch(zs):
     (6, 7, 40, 4, 10, 2.0, 300, 40),      # drift-shaped: one slice per recurrence, window N = 10
     (3, 4, 1, 2, 0, math.inf, 130, 30),   # two pairs, no early stop
 ])
-@pytest.mark.parametrize("layout,draw", [(1, 0), (2, 0), (2, 1), (2, 2)])
+@pytest.mark.parametrize("layout,draw", [(1, 0), (2, 0), (2, 1), (2, 2), (4, 0), (4, 2)])
 def test_random_traces_one_cell(zs, oracle, B, P, S, K, window, beta, trials, R, layout, draw):
     """One-cell launches run the RK kernels (round keys in the parameters, the
     record cache with write-back in the Thompson phase); edge shapes in both schedules,

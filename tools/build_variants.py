@@ -47,6 +47,11 @@ VARIANTS = {
     "diag_nohist": (["ZS_DIAG_NOHIST"], []),   # timing diagnostic only: curves wrong
     "th_q2_mb5": (["ZS_TH_MIN_BLOCKS=5"], []),
     "th_mb8": (["ZS_TH_MIN_BLOCKS=8"], []),
+    "nosplit": (["ZS_EARLY_SPLIT=0"], []),       # phase A runs every lane to t_split (round-2 r02ao)
+    "split": (["ZS_EARLY_SPLIT=1"], []),
+    "split_mb5": (["ZS_EARLY_SPLIT=1", "ZS_TH_MIN_BLOCKS=5"], []),
+    "split_pack": (["ZS_EARLY_SPLIT=1", "ZS_T0_PACK=1"], []),
+    "nosplit_mb5": (["ZS_EARLY_SPLIT=0", "ZS_TH_MIN_BLOCKS=5"], []),
 }
 
 if __name__ == "__main__":

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -492,6 +493,36 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
   return ZEUS_OK;
 }
 
+// Every kernel's dynamic shared-memory limit set to the device maximum, once per device and
+// process (the attribute is per function and process-wide, so handles with different footprints
+// can launch concurrently; each launch passes its own size).  Done in every zeus_sim_load_profile
+// it cost ~75 us of host time per call (~80 functions x 3 driver calls).
+cudaError_t grant_all(int device) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (device >= 0 && device < 64 && done[device]) return cudaSuccess;
+#define ZS_TRY(x) do { const cudaError_t e_ = (x); if (e_ != cudaSuccess) return e_; } while (0)
+  for (int w = 0; w < 2; ++w)
+    for (int l = 0; l < 2; ++l)
+      for (int ph = 0; ph < 3; ++ph)
+        for (int ab = 0; ab < 3; ++ab)            // ab == 2: the RK kernels
+          ZS_TRY(grant_max_smem((const void *)replay_fn(w, l, ph, ab == 1, ab == 2), device));
+  for (int f = 0; f < 32; ++f)
+    ZS_TRY(grant_max_smem((const void *)thompson_fn(f & 1, f & 2, f & 4, f & 8, f & 16), device));
+  ZS_TRY(grant_group<2>(device));
+  ZS_TRY(grant_group<4>(device));
+  ZS_TRY(grant_group<8>(device));
+  ZS_TRY(grant_max_smem((const void *)zs::concurrent_kernel<false>, device));
+  ZS_TRY(grant_max_smem((const void *)zs::concurrent_kernel<true>, device));
+  ZS_TRY(grant_max_smem((const void *)zs::variant_kernel<false>, device));
+  ZS_TRY(grant_max_smem((const void *)zs::variant_kernel<true>, device));
+  // a captured run binds buffer addresses and launch shapes: keep it only if none changed
+#undef ZS_TRY
+  if (device >= 0 && device < 64) done[device] = true;
+  return cudaSuccess;
+}
+
 zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th, int32_t S,
                                   int32_t K, const int32_t *pool) {
   NvtxRange nvtx_("zeus_sim_load_profile");
@@ -613,70 +644,59 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
   }
   ZS_CUDA(s, cudaEventRecord(s->ev_loaded, st));
 
-  // launch shape of the replay: the block size (32/64/128 trials) that keeps the
-  // most warps resident given the shared-memory footprint per trial
-  const zs::TabLayout L(B, S, K);
-  s->tab_bytes = L.bytes;
-  const int wmax = s->wmax;
-  // (mu, sigma) per arm, and the bound screen's two residual slots
-  const size_t per_thread = (size_t)((B + 1) & ~1) * 16 + (ZS_BOUND_SKIP ? 16 * zs::kResSlots : 0);
-  int best_warps = -1;
-  // sized for the kernel that dominates: the Thompson phase when the schedule has two
-  // phases (R > 2B), else the one-pass kernel; ties keep the larger block (fewer stagings)
-  const bool two_phase = (s->layout == 2 || s->layout == 4 || (s->layout == 0 && (s->wmax == 0 || s->R >= 16 * B))) &&
-                         std::min(s->R, 2 * B) < s->R;
-  for (int tpb : {128, 64, 32}) {
-    const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
-    if (bytes > 227 * 1024) continue;
-    int blocks = 0;
-    const void *fn = (const void *)replay_fn(wmax > 0, false, two_phase ? 2 : 0, s->any_ablation, s->cells.size() == 1);
-    int granted = 0;
-    ZS_CUDA(s, grant_max_smem(fn, s->device, &granted));
-    if ((int)bytes > granted) continue;
-    ZS_CUDA(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, tpb, bytes));
-    const int warps = blocks * tpb / 32;
-    if (warps > best_warps) { best_warps = warps; s->tpb = tpb; s->smem_bytes = (int)bytes; }
-#ifdef ZS_EXPERIMENT_SMEM_PAD
-    s->smem_bytes += ZS_EXPERIMENT_SMEM_PAD;   // occupancy experiments only
-#endif
-  }
-  if (best_warps <= 0) return fail(s, ZEUS_E_UNSUPPORTED, "no launch shape fits shared memory");
-  // lane groups (layout 3, or auto when one thread per trial cannot fill the GPU): W lanes per
-  // trial, W = the power of two covering about two survivor pairs per lane
-  {
-    int64_t zeus_trials = 0;
-    for (const auto &p : s->cpar) if (p.policy == ZEUS_POLICY_ZEUS && !p.conc) zeus_trials += p.n;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
-    const int pairs = (B + 1) / 2;
-    const int w = pairs <= 2 ? 2 : pairs <= 8 ? 4 : 8;
-    // measured: lane groups win only when the grouped launch fills at most a quarter of one
-    // wave (CFG1 +18 %); beyond that the serial work each lane repeats costs more than the
-    // split draw saves (CFG2 -35 %, CFG4 -70 %)
-    const bool small = zeus_trials * w * 4 <= (int64_t)sms * best_warps * 32;
-    s->group_w = 0;
-    if (!s->any_ablation && (s->layout == 3 || (s->layout == 0 && small))) {
-      const size_t gbytes = (size_t)L.bytes + (size_t)(128 / w) * (((B + 1) & ~1) * 16);
-      if (gbytes <= 200 * 1024) s->group_w = w;
+  // launch shape of the replay (a reload with the same table shape keeps it: it depends on
+  // B, S, K and the handle's fixed options only)
+  if (!same_shape) {
+    // launch shape of the replay: the block size (32/64/128 trials) that keeps the
+    // most warps resident given the shared-memory footprint per trial
+    const zs::TabLayout L(B, S, K);
+    s->tab_bytes = L.bytes;
+    const int wmax = s->wmax;
+    // (mu, sigma) per arm, and the bound screen's two residual slots
+    const size_t per_thread = (size_t)((B + 1) & ~1) * 16 + (ZS_BOUND_SKIP ? 16 * zs::kResSlots : 0);
+    int best_warps = -1;
+    // sized for the kernel that dominates: the Thompson phase when the schedule has two
+    // phases (R > 2B), else the one-pass kernel; ties keep the larger block (fewer stagings)
+    const bool two_phase = (s->layout == 2 || s->layout == 4 || (s->layout == 0 && (s->wmax == 0 || s->R >= 16 * B))) &&
+                           std::min(s->R, 2 * B) < s->R;
+    for (int tpb : {128, 64, 32}) {
+      const size_t bytes = (size_t)L.bytes + (size_t)tpb * per_thread;
+      if (bytes > 227 * 1024) continue;
+      int blocks = 0;
+      const void *fn = (const void *)replay_fn(wmax > 0, false, two_phase ? 2 : 0, s->any_ablation, s->cells.size() == 1);
+      int granted = 0;
+      ZS_CUDA(s, grant_max_smem(fn, s->device, &granted));
+      if ((int)bytes > granted) continue;
+      ZS_CUDA(s, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, tpb, bytes));
+      const int warps = blocks * tpb / 32;
+      if (warps > best_warps) { best_warps = warps; s->tpb = tpb; s->smem_bytes = (int)bytes; }
+  #ifdef ZS_EXPERIMENT_SMEM_PAD
+      s->smem_bytes += ZS_EXPERIMENT_SMEM_PAD;   // occupancy experiments only
+  #endif
+    }
+    if (best_warps <= 0) return fail(s, ZEUS_E_UNSUPPORTED, "no launch shape fits shared memory");
+    // lane groups (layout 3, or auto when one thread per trial cannot fill the GPU): W lanes per
+    // trial, W = the power of two covering about two survivor pairs per lane
+    {
+      int64_t zeus_trials = 0;
+      for (const auto &p : s->cpar) if (p.policy == ZEUS_POLICY_ZEUS && !p.conc) zeus_trials += p.n;
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+      const int pairs = (B + 1) / 2;
+      const int w = pairs <= 2 ? 2 : pairs <= 8 ? 4 : 8;
+      // measured: lane groups win only when the grouped launch fills at most a quarter of one
+      // wave (CFG1 +18 %); beyond that the serial work each lane repeats costs more than the
+      // split draw saves (CFG2 -35 %, CFG4 -70 %)
+      const bool small = zeus_trials * w * 4 <= (int64_t)sms * best_warps * 32;
+      s->group_w = 0;
+      if (!s->any_ablation && (s->layout == 3 || (s->layout == 0 && small))) {
+        const size_t gbytes = (size_t)L.bytes + (size_t)(128 / w) * (((B + 1) & ~1) * 16);
+        if (gbytes <= 200 * 1024) s->group_w = w;
+      }
     }
   }
-  // the attribute is per function (process-wide): grant the device maximum once, so handles
-  // with different footprints can launch concurrently; each launch passes its own size
-  for (int w = 0; w < 2; ++w)
-    for (int l = 0; l < 2; ++l)
-      for (int ph = 0; ph < 3; ++ph)
-        for (int ab = 0; ab < 3; ++ab)            // ab == 2: the RK kernels
-          ZS_CUDA(s, grant_max_smem((const void *)replay_fn(w, l, ph, ab == 1, ab == 2), s->device));
-  for (int f = 0; f < 32; ++f)
-    ZS_CUDA(s, grant_max_smem((const void *)thompson_fn(f & 1, f & 2, f & 4, f & 8, f & 16), s->device));
-  ZS_CUDA(s, grant_group<2>(s->device));
-  ZS_CUDA(s, grant_group<4>(s->device));
-  ZS_CUDA(s, grant_group<8>(s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::concurrent_kernel<false>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::concurrent_kernel<true>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::variant_kernel<false>, s->device));
-  ZS_CUDA(s, grant_max_smem((const void *)zs::variant_kernel<true>, s->device));
-  // a captured run binds buffer addresses and launch shapes: keep it only if none changed
+  // the shared-memory grants are process-wide attributes: once per device (grant_all)
+  ZS_CUDA(s, grant_all(s->device));
   s->loaded = true;
   if (s->launch_signature() != sig0) s->drop_graph();
   return ZEUS_OK;

@@ -428,9 +428,13 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
   }
   s->shard_total = off;
   s->nwin = (int)std::max<int64_t>(1, (s->max_shard + zs::kRegroupWindow - 1) / zs::kRegroupWindow);
-  // curve slots: spread the per-warp atomics over up to 64 copies, bounded to 64 MB
+  // curve slots: spread the per-warp atomics over up to 8 copies, bounded to 64 MB (64 copies:
+  // CFG3 -1.5 %, the memsets and the reduction of 64 MB per job; session r02bi)
+#ifndef ZS_SLOT_MAX
+#define ZS_SLOT_MAX 8
+#endif
   const size_t curve_bytes = (size_t)num_cells * s->R * zs::kRow * sizeof(long long);
-  s->nslot = (int)std::max<size_t>(1, std::min<size_t>(64, (64ull << 20) / std::max<size_t>(1, curve_bytes)));
+  s->nslot = (int)std::max<size_t>(1, std::min<size_t>(ZS_SLOT_MAX, (64ull << 20) / std::max<size_t>(1, curve_bytes)));
 
   const size_t n = (size_t)s->shard_total;
   cudaError_t e = cudaSuccess;
@@ -592,10 +596,10 @@ zeus_status zeus_sim_load_profile(zeus_sim *s, const double *A, const double *Th
     ZS_CUDA(s, s->d_optarm.alloc((size_t)nc * s->opt_stride * 4));
     ZS_CUDA(s, s->d_ebar.alloc((size_t)S * B * 8));
     ZS_CUDA(s, s->d_pareto.alloc((size_t)S * B * P));
-    // counted curves: [cells][R][nhslot][4][B][K] u32, up to 16 slot copies within 64 MB
+    // counted curves: [cells][R][nhslot][4][B][K] u32, up to ZS_HSLOT_MAX slot copies within 64 MB
     const size_t per_slot = (size_t)nc * s->R * 4 * B * K * 4;
 #ifndef ZS_HSLOT_MAX
-#define ZS_HSLOT_MAX 16
+#define ZS_HSLOT_MAX 4                      // 16: CFG3 -1.5 % with 64 curve slots (session r02bi)
 #endif
     s->nhslot = (int)std::max<size_t>(1, std::min<size_t>(ZS_HSLOT_MAX, (ZS_HSLOT_MAX * 4ull << 20) / std::max<size_t>(1, per_slot)));
     ZS_CUDA(s, s->d_hist.alloc(per_slot * s->nhslot));

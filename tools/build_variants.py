@@ -51,6 +51,9 @@ VARIANTS = {
     "split": (["ZS_EARLY_SPLIT=1"], []),
     "split_mb5": (["ZS_EARLY_SPLIT=1", "ZS_TH_MIN_BLOCKS=5"], []),
     "split_pack": (["ZS_EARLY_SPLIT=1", "ZS_T0_PACK=1"], []),
+    "sl8": (["ZS_SLOT_MAX=8"], []),
+    "sl8_hs4": (["ZS_SLOT_MAX=8", "ZS_HSLOT_MAX=4"], []),
+    "sl16_hs8": (["ZS_SLOT_MAX=16", "ZS_HSLOT_MAX=8"], []),
     "nosplit_mb5": (["ZS_EARLY_SPLIT=0", "ZS_TH_MIN_BLOCKS=5"], []),
 }
 

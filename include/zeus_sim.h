@@ -54,7 +54,8 @@
 extern "C" {
 #endif
 
-#define ZEUS_SIM_ABI_VERSION 2   /* 2: zeus_run_opts.draw, 14 counters, zeus_sim_certify_bounds */
+#define ZEUS_SIM_ABI_VERSION 3   /* 2: zeus_run_opts.draw, 14 counters, zeus_sim_certify_bounds;
+                                    3: zeus_sim_results_async, layout 4 (early split) */
 #define ZEUS_MAX_BATCH_SIZES 32
 #define ZEUS_MAX_POWER_LIMITS 64
 #define ZEUS_CURVE_QUANTITIES 7   /* cost, energy, time, pseudo-regret, n_stop, n_opt, n_ts */
@@ -256,6 +257,13 @@ zeus_status zeus_sim_run(zeus_sim *sim, void *cuda_stream);
  * log without log_mode; nothing is copied then), enqueues the copies on the
  * handle's stream, synchronises that stream, and returns. */
 zeus_status zeus_sim_results(zeus_sim *sim, zeus_results *out);
+
+/* The replay outputs (curves, curves_fixed, the per-trial arrays, log, counters) into DEVICE
+ * buffers only, enqueued on the handle's stream (the stream of the last zeus_sim_run) without
+ * synchronising: consumers order on that stream.  ZEUS_E_INVALID (nothing queued) for a host
+ * destination or a step-1 table / Pareto request, ZEUS_E_STATE before any run.  Fills
+ * kernel_launches and curve_scale_bits; the event timings are zeus_sim_results'. */
+zeus_status zeus_sim_results_async(zeus_sim *sim, zeus_results *out);
 
 /* curves [cells][R][7] (device) from fixed-point sums curves_fixed [cells][R][7][3] (device),
  * e.g. after an all-reduce (SUM) of every rank's curves_fixed: carries the limbs and rounds

@@ -201,7 +201,9 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
     else return st_g[arm_i];
   };
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
+#if !ZS_CURVES_REMAT
   long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
+#endif
   const int HB = 4 * B * K;
   // counted runs of class (Thompson decision, no profiling), row t_split; one row per t
   const size_t hstride = (size_t)a.nhslot * HB;
@@ -431,6 +433,10 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
             vPacked = 1 | ((b == optarm[s]) ? (1 << 8) : 0) | (1 << 16);
           }
         }
+#if ZS_CURVES_REMAT
+        // the warp's slot row, recomputed on this rare path (no pointer held across the loop)
+        long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
+#endif
         curve_accumulate(curves, t, tid & 31, special ? vC : 0.0, special ? vE : 0.0, special ? vT : 0.0,
                          special ? vReg : 0.0, special ? vPacked : 0, a.curve_scale);
       }

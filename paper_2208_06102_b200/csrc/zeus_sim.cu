@@ -978,6 +978,52 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
   return ZEUS_OK;
 }
 
+// The replay outputs into DEVICE buffers, enqueued on the handle's stream without waiting (the
+// multi-job bench step: six handles' curves handed to their consumers in stream order, no host
+// round trip per handle).  Everything is validated before any copy is queued.
+zeus_status zeus_sim_results_async(zeus_sim *s, zeus_results *out) {
+  NvtxRange nvtx_("zeus_sim_results_async");
+  if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
+  s->err.clear();
+  if (!out) return fail(s, ZEUS_E_INVALID, "out is NULL");
+  if (out->struct_size != sizeof(zeus_results)) return fail(s, ZEUS_E_INVALID, "zeus_results.struct_size mismatch (ABI)");
+  if (!s->loaded) return fail(s, ZEUS_E_STATE, "zeus_sim_results_async before zeus_sim_load_profile");
+  if (!s->ran) return fail(s, ZEUS_E_STATE, "zeus_sim_results_async before zeus_sim_run");
+  if (out->log && !s->log_mode) return fail(s, ZEUS_E_STATE, "log requested but log_mode = 0");
+  if (out->pstar_index || out->c1 || out->t1 || out->e1 || out->c_prof || out->t_prof || out->e_prof ||
+      out->opt_cost || out->opt_arm || out->pareto)
+    return fail(s, ZEUS_E_INVALID, "zeus_sim_results_async copies replay outputs only (step-1 tables and "
+                                   "Pareto masks: zeus_sim_results)");
+  ZS_CUDA(s, cudaSetDevice(s->device));
+  const int nc = (int)s->cells.size();
+  const size_t n = (size_t)s->shard_total;
+  struct Req { void *dst; const DevBuf *src; size_t bytes; const char *name; };
+  const Req req[] = {{out->curves, &s->d_curves, (size_t)nc * s->R * zs::kQ * 8, "curves"},
+                     {out->curves_fixed, &s->d_fixed, (size_t)nc * s->R * zs::kRow * 8, "curves_fixed"},
+                     {out->tot_cost, &s->d_tot_cost, n * 8, "tot_cost"},
+                     {out->tot_energy, &s->d_tot_energy, n * 8, "tot_energy"},
+                     {out->tot_time, &s->d_tot_time, n * 8, "tot_time"},
+                     {out->digest, &s->d_digest, n * 8, "digest"},
+                     {out->n_stop, &s->d_nstop, n * 4, "n_stop"},
+                     {out->final_arm, &s->d_final, n * 4, "final_arm"},
+                     {out->log, &s->d_log, n * (size_t)s->R * 4, "log"},
+                     {out->counters, &s->d_counters, zs::kCounters * 8, "counters"}};
+  for (const Req &r : req) {
+    if (!r.dst) continue;
+    cudaPointerAttributes pa{};
+    const cudaError_t e = cudaPointerGetAttributes(&pa, r.dst);
+    if (e != cudaSuccess || (pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged)) {
+      cudaGetLastError();
+      return fail(s, ZEUS_E_INVALID, std::string("zeus_sim_results_async: ") + r.name + " is not device memory");
+    }
+  }
+  for (const Req &r : req)
+    if (r.dst && r.bytes) ZS_CUDA(s, cudaMemcpyAsync(r.dst, r.src->p, r.bytes, cudaMemcpyDeviceToDevice, s->stream));
+  out->kernel_launches = s->launches;
+  out->curve_scale_bits = s->curve_bits;
+  return ZEUS_OK;
+}
+
 zeus_status zeus_sim_results(zeus_sim *s, zeus_results *out) {
   NvtxRange nvtx_("zeus_sim_results");
   if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");

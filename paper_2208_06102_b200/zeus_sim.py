@@ -24,7 +24,7 @@ STATUS = {0: "ZEUS_OK", 1: "ZEUS_E_INVALID", 2: "ZEUS_E_STATE", 3: "ZEUS_E_NO_CO
 CURVE_Q = 7
 COUNTERS = 14
 EXPORTS = ("zeus_sim_create", "zeus_sim_load_profile", "zeus_sim_run", "zeus_sim_results",
-           "zeus_sim_destroy", "zeus_sim_last_error", "zeus_sim_shape", "zeus_sim_curves_from_fixed",
+           "zeus_sim_results_async", "zeus_sim_destroy", "zeus_sim_last_error", "zeus_sim_shape", "zeus_sim_curves_from_fixed",
            "zeus_sim_certify_bounds")
 CURVE_LIMBS = 3
 
@@ -85,6 +85,7 @@ def lib():
                                             C.c_int32, C.c_void_p]
         L.zeus_sim_run.argtypes = [C.c_void_p, C.c_void_p]
         L.zeus_sim_results.argtypes = [C.c_void_p, C.POINTER(zeus_results)]
+        L.zeus_sim_results_async.argtypes = [C.c_void_p, C.POINTER(zeus_results)]
         L.zeus_sim_destroy.argtypes = [C.c_void_p]
         L.zeus_sim_destroy.restype = None
         L.zeus_sim_last_error.argtypes = [C.c_void_p]
@@ -92,7 +93,7 @@ def lib():
         L.zeus_sim_shape.argtypes = [C.c_void_p] + [C.c_void_p] * 5
         L.zeus_sim_curves_from_fixed.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.zeus_sim_certify_bounds.argtypes = [C.c_int32, C.c_void_p]
-        for f in ("zeus_sim_create", "zeus_sim_load_profile", "zeus_sim_run", "zeus_sim_results",
+        for f in ("zeus_sim_create", "zeus_sim_load_profile", "zeus_sim_run", "zeus_sim_results", "zeus_sim_results_async",
                   "zeus_sim_shape", "zeus_sim_curves_from_fixed", "zeus_sim_certify_bounds"):
             getattr(L, f).restype = C.c_int
         _lib = L
@@ -124,6 +125,11 @@ def zeus_sim_run(h, cuda_stream=None):
 
 def zeus_sim_results(h, res: zeus_results):
     _check(lib().zeus_sim_results(h, C.byref(res)), h)
+    return res
+
+
+def zeus_sim_results_async(h, res: zeus_results):
+    _check(lib().zeus_sim_results_async(h, C.byref(res)), h)
     return res
 
 
@@ -215,9 +221,11 @@ class Simulation:
         return self
 
     def results(self, want=("curves", "tot_cost", "tot_energy", "tot_time", "digest", "n_stop",
-                            "final_arm", "counters"), out=None):
+                            "final_arm", "counters"), out=None, enqueue_only=False):
         """Copies outputs into host numpy arrays (default) or into caller buffers given in
-        ``out`` (numpy arrays or torch tensors, host or device)."""
+        ``out`` (numpy arrays or torch tensors, host or device).  enqueue_only: the replay
+        outputs into the device buffers of ``out`` on the run's stream, without waiting
+        (zeus_sim_results_async; no timings)."""
         nc, R, n, B, S = self.ncells, self.R, self.shard_n, self.B, self.S
         shapes = {"curves": ((nc, R, CURVE_Q), np.float64),
                   "curves_fixed": ((nc, R, CURVE_Q, CURVE_LIMBS), np.int64), "tot_cost": ((n,), np.float64),
@@ -239,6 +247,11 @@ class Simulation:
         res.struct_size = C.sizeof(zeus_results)
         for k, v in bufs.items():
             setattr(res, k, _ptr(v).value if v is not None else None)
+        if enqueue_only:
+            zeus_sim_results_async(self.h, res)
+            bufs["kernel_launches"] = res.kernel_launches
+            bufs["curve_scale_bits"] = res.curve_scale_bits
+            return bufs
         zeus_sim_results(self.h, res)
         bufs["step1_ms"] = res.step1_ms
         bufs["replay_ms"] = res.replay_ms

@@ -250,6 +250,37 @@ def test_results_into_device_buffers(zs):
     sim.close()
 
 
+def test_results_async_device_buffers(zs):
+    """zeus_sim_results_async: the replay outputs enqueued into device buffers on the run's
+    stream (no synchronisation) equal zeus_sim_results'; host destinations and step-1 tables
+    are refused before anything is queued."""
+    import torch
+
+    (job,) = synth.config("cfg4", trials=3000)
+    sim = zs.Simulation(job.workload, job.cells, job.trials, job.recurrences).load_profile()
+    stream = torch.cuda.Stream()
+    sim.run(stream)
+    ref = sim.results(want=["curves", "curves_fixed", "tot_cost", "digest", "counters"])
+    sim.run(stream)                                  # a second run: the same bits
+    n = sim.shard_n
+    dev = {"curves": torch.zeros((1, sim.R, 7), dtype=torch.float64, device="cuda"),
+           "curves_fixed": torch.zeros((1, sim.R, 7, 3), dtype=torch.int64, device="cuda"),
+           "tot_cost": torch.zeros(n, dtype=torch.float64, device="cuda"),
+           "digest": torch.zeros(n, dtype=torch.int64, device="cuda"),
+           "counters": torch.zeros(14, dtype=torch.int64, device="cuda")}
+    r = sim.results(want=[], out=dev, enqueue_only=True)
+    assert r["kernel_launches"] > 0
+    stream.synchronize()
+    for k, v in dev.items():
+        assert np.array_equal(v.cpu().numpy().view(np.asarray(ref[k]).dtype).reshape(np.shape(ref[k])),
+                              np.asarray(ref[k])), k
+    with pytest.raises(zs.ZeusError, match="not device memory"):
+        sim.results(want=["tot_cost"], enqueue_only=True)
+    with pytest.raises(zs.ZeusError, match="replay outputs only"):
+        sim.results(want=["c1"], enqueue_only=True)
+    sim.close()
+
+
 def test_errors_are_reported(zs):
     (job,) = synth.config("cfg1")
     w = dict(job.workload)

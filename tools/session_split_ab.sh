@@ -13,7 +13,7 @@ done
 for rep in 1 2; do
 for c in ${AB_CONFIGS:-cfg5 cfg3}; do
   for v in "$@"; do
-    ZEUS_SIM_LIB=$PWD/build/libzs_$v.so timeout -s KILL 300 python bench.py --config $c --steps ${AB_STEPS:-5} --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/bench_${c}_${v}_$rep.json 2> $OUT/bench_${c}_${v}_$rep.err
+    ZEUS_SIM_LIB=$PWD/build/libzs_$v.so timeout -s KILL 300 python bench.py --config $c ${AB_ARGS:-} --steps ${AB_STEPS:-5} --warmup 3 --no-cpu-baseline --e2e-steps 1 > $OUT/bench_${c}_${v}_$rep.json 2> $OUT/bench_${c}_${v}_$rep.err
     python - "$c $v $rep" "$OUT/bench_${c}_${v}_$rep.json" <<'PY'
 import json, sys
 try:

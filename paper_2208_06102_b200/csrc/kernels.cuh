@@ -1268,22 +1268,27 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
 }
 
 // bucket offsets: exclusive scan of each (cell, window) histogram, offset by the window base; one
-// warp per (cell, window), 32 buckets per step
+// warp per (cell, window): every lane loads its kBuckets/32 counts at once (the loads in flight
+// together, not one round trip per 32 buckets), then a shuffle scan per 32-bucket chunk
+constexpr int kScanPerLane = (kBuckets + 31) / 32;
 __global__ void bucket_scan_kernel(int32_t *bucket, int ncells, int nwin) {
   const int64_t cw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (cw >= (int64_t)ncells * nwin) return;                 // warp-uniform
+  int32_t *row = bucket + cw * kBuckets;
+  int c[kScanPerLane];
+#pragma unroll
+  for (int j = 0; j < kScanPerLane; ++j) c[j] = (32 * j + lane < kBuckets) ? row[32 * j + lane] : 0;
   int run = (int)(cw % nwin) * kRegroupWindow;
-  for (int k0 = 0; k0 < kBuckets; k0 += 32) {
-    const int k = k0 + lane;
-    const int c = k < kBuckets ? bucket[cw * kBuckets + k] : 0;
-    int x = c;                                              // inclusive scan over the lanes
+#pragma unroll
+  for (int j = 0; j < kScanPerLane; ++j) {
+    int x = c[j];                                           // inclusive scan over the lanes
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, x, off);
       if (lane >= off) x += y;
     }
-    if (k < kBuckets) bucket[cw * kBuckets + k] = run + x - c;
+    if (32 * j + lane < kBuckets) row[32 * j + lane] = run + x - c[j];
     run += __shfl_sync(0xffffffffu, x, 31);
   }
 }

@@ -25,6 +25,18 @@ namespace zs {
 #ifndef ZS_QUAD2
 #define ZS_QUAD2 1
 #endif
+#ifndef ZS_WIN_MIN_BLOCKS
+#define ZS_WIN_MIN_BLOCKS 6
+#endif
+#ifndef ZS_WIN_POOL_FIT
+#define ZS_WIN_POOL_FIT 1
+#endif
+#ifndef ZS_WIN_PREFETCH
+#define ZS_WIN_PREFETCH 1
+#endif
+#ifndef ZS_CURVES_REMAT
+#define ZS_CURVES_REMAT 0     // the curve-slot pointer recomputed on the stopped-run path: -1.3 % (r02bj)
+#endif
 #ifndef ZS_PHILOX_WIDE
 #define ZS_PHILOX_WIDE 1
 #endif
@@ -97,21 +109,24 @@ __device__ __forceinline__ U4 philox_from_prefix(const PhiloxPrefix &p, uint32_t
 // table, and the trace pool when it is small; the pseudo-regret and optimum tables are read only
 // on a stopped run's path, from global memory, so many slices (CFG4: 200) cost no residency.
 // The offsets travel in the kernel parameters (ReplayArgs::th_*).
+// The pool goes to shared memory when it is small, or when it still leaves the kernel its six
+// blocks per SM (per_block = the block's per-thread state): a pool read through L1 sits on the
+// decision's chain, and the carveout leaves L1 little room (CFG4: 19.2 KB, session r02br).
 constexpr int kThPoolSmemMax = 16384;
+constexpr int kThSmemPerSm = 227 * 1024;
 struct ThTabLayout {
   int arms, logtab, pool, bytes;
   bool pool_smem;
-  __host__ __device__ ThTabLayout(int B, int S, int K) {
+  __host__ __device__ ThTabLayout(int B, int S, int K, int per_block = 0) {
     arms = 0;
     logtab = TabLayout::align16(B * (int)sizeof(ArmConst));
     pool = TabLayout::align16(logtab + kLogTab * 16);
-    pool_smem = S * B * K * 4 <= kThPoolSmemMax;
-    bytes = pool_smem ? TabLayout::align16(pool + S * B * K * 4) : pool;
+    const int pb = S * B * K * 4;
+    pool_smem = pb <= kThPoolSmemMax ||
+                (ZS_WIN_POOL_FIT && (TabLayout::align16(pool + pb) + per_block + 1024) * ZS_WIN_MIN_BLOCKS <= kThSmemPerSm);
+    bytes = pool_smem ? TabLayout::align16(pool + pb) : pool;
   }
 };
-#ifndef ZS_WIN_MIN_BLOCKS
-#define ZS_WIN_MIN_BLOCKS 6
-#endif
 
 // SREC (launches of at most a couple of waves, where one warp per scheduler makes the decision's
 // latency the throughput): every survivor's Observe record lives in shared memory for the whole
@@ -285,6 +300,14 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
         const U4 rw = replica_words_c(trial, t);
         reinterpret_cast<uint4 *>(s_rw)[tid] = make_uint4(rw.x, rw.y, rw.z, rw.w);
       }
+#if ZS_WIN_PREFETCH
+      // WIN: the evicted cost of the cached arm's window, loaded before the draw -- Thompson
+      // sampling mostly repeats its arm, and then the ring load is off the decision's chain
+      // (qc.pad = the arm's ring position cnt % N while the record is cached)
+      const int pb = qc_b;
+      double y_pre = 0.0;
+      if (WIN && Nw > 0 && pb >= 0 && qc.cnt >= Nw) y_pre = a.st_ring[(o * B + pb) * (size_t)a.ring_n + qc.pad];
+#endif
       // ---------------- step 2: Alg. 1, b = argmin_a theta_a over the survivors
       const uint32_t unripe = 0u;   // every Thompson-phase arm has n >= 2 (run twice in pruning)
       (void)unripe;
@@ -363,10 +386,20 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
         if (qc_b >= 0) rec(qc_b) = qc;
         qc = rec(b);
         qc_b = b;
+#if ZS_WIN_PREFETCH
+        if (WIN && Nw > 0) qc.pad = qc.cnt % Nw;
+#endif
       }
       // the windowed Observe's evicted cost, loaded as soon as the decision is known
+#if ZS_WIN_PREFETCH
+      if (WIN && Nw > 0 && qc.cnt >= Nw) {
+        if (b == pb) y_old = y_pre;
+        else y_old = a.st_ring[(o * B + b) * (size_t)a.ring_n + qc.pad];
+      }
+#else
       if (WIN && Nw > 0 && qc.cnt >= Nw)
         y_old = a.st_ring[(o * B + b) * (size_t)a.ring_n + (qc.cnt % Nw)];
+#endif
       const ArmConst ac = arm[b];
       const int p = ac.pstar;
       const double c1b = ac.c1, t1b = ac.t1, e1b = ac.e1;
@@ -451,7 +484,12 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
           qc.S2 = qc.S2 - dy * dy;
           n = Nw - 1;
         }
+#if ZS_WIN_PREFETCH
+        a.st_ring[(o * B + b) * (size_t)a.ring_n + qc.pad] = C;
+        qc.pad = (qc.pad + 1 == Nw) ? 0 : qc.pad + 1;
+#else
         a.st_ring[(o * B + b) * (size_t)a.ring_n + (qc.cnt % Nw)] = C;
+#endif
       }
       const double d = C - qc.sh;
       qc.S1 = qc.S1 + d;

@@ -873,7 +873,7 @@ static zeus_status enqueue_run(zeus_sim *s, cudaStream_t st, bool capturing) {
     const dim3 tgrid((unsigned)((s->max_shard + 127) / 128), (unsigned)nc);
     size_t tab = (size_t)s->tab_bytes;
     if (windowed) {                            // the compact table layout of the WIN variant
-      const zs::ThTabLayout TL(s->B, s->S, s->K);
+      const zs::ThTabLayout TL(s->B, s->S, s->K, 128 * (((((s->B + 1) / 2) + 1) & ~1) * 16 + 16));
       a.th_logtab = TL.logtab; a.th_pool = TL.pool; a.th_bytes = TL.bytes; a.th_pool_smem = TL.pool_smem;
       tab = (size_t)TL.bytes;
     }

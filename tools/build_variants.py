@@ -55,6 +55,9 @@ VARIANTS = {
     "sl8_hs4": (["ZS_SLOT_MAX=8", "ZS_HSLOT_MAX=4"], []),
     "sl16_hs8": (["ZS_SLOT_MAX=16", "ZS_HSLOT_MAX=8"], []),
     "remat": (["ZS_CURVES_REMAT=1"], []),
+    "winpf": (["ZS_WIN_PREFETCH=1"], []),
+    "winfit": (["ZS_WIN_POOL_FIT=1"], []),
+    "winpf_fit": (["ZS_WIN_PREFETCH=1", "ZS_WIN_POOL_FIT=1"], []),
     "nosplit_mb5": (["ZS_EARLY_SPLIT=0", "ZS_TH_MIN_BLOCKS=5"], []),
 }
 

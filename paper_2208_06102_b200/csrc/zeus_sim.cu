@@ -74,7 +74,10 @@ struct zeus_sim {
     return {(uintptr_t)d_A.p, (uintptr_t)d_Th.p, (uintptr_t)d_pool.p, (uintptr_t)d_arms.p,
             (uintptr_t)d_regret.p, (uintptr_t)d_opt.p, (uintptr_t)d_optarm.p, (uintptr_t)d_ebar.p,
             (uintptr_t)S, (uintptr_t)K, (uintptr_t)reg_stride, (uintptr_t)opt_stride, (uintptr_t)tpb,
-            (uintptr_t)smem_bytes, (uintptr_t)tab_bytes, (uintptr_t)group_w, (uintptr_t)loaded};
+            (uintptr_t)smem_bytes, (uintptr_t)tab_bytes, (uintptr_t)group_w, (uintptr_t)loaded,
+            // the curves' fixed-point scale follows the traces (load_profile) and is a kernel
+            // argument of the captured launches
+            (uintptr_t)(intptr_t)curve_bits};
   }
   void drop_graph() {
     if (graph_exec) cudaGraphExecDestroy(graph_exec);

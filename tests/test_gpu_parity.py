@@ -442,6 +442,27 @@ def test_cuda_graph_runs_identical(zs):
         g.close()
 
 
+def test_cuda_graph_reload_new_values_same_shape(zs):
+    """A same-shaped reload with different values keeps the captured graph only where nothing
+    captured changed: a trace 64x slower changes the curves' fixed-point scale F (a kernel
+    argument), so the graph is recaptured, and the run equals a fresh handle's."""
+    want = ["digest", "tot_cost", "curves", "curves_fixed"]
+    (job,) = synth.config("cfg4_38", trials=500)
+    w2 = dict(job.workload)
+    w2["throughput"] = np.asarray(job.workload["throughput"]) / 64.0      # every cost 64x: F - 6
+    direct = zs.Simulation(w2, job.cells, job.trials, job.recurrences).load_profile()
+    ref = direct.run().results(want=want)
+    direct.close()
+    g = zs.Simulation(job.workload, job.cells, job.trials, job.recurrences, graph=True).load_profile()
+    f0 = g.run().results(want=want)["curve_scale_bits"]
+    g.w = w2
+    out = g.load_profile().run().results(want=want)
+    g.close()
+    assert out["curve_scale_bits"] == ref["curve_scale_bits"] != f0
+    for k in want:
+        assert np.array_equal(out[k], ref[k]), k
+
+
 def test_bound_screen_every_path(zs, oracle):
     """a trace whose posteriors stay wide (32 arms, few recurrences, large beta)
     drives the bound screen through all of its paths -- screened-out pairs, parked residuals

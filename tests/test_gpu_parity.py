@@ -145,6 +145,12 @@ def test_cfg5_full_size_sampled(zs, oracle):
     np.testing.assert_allclose(c[:, 1].sum(), g["tot_energy"].sum(), rtol=1e-9)
     assert c[:, 4].sum() == g["n_stop"].sum() == g["counters"][4]
     assert g["counters"][0] == n * job.recurrences
+    # Thompson-sampling picks: every sampled or forced decision, and every decision once the
+    # pruning stage (at most 2|B| recurrences, Alg. 3) is over -- exact integer sums
+    B = len(job.workload["batch_sizes"])
+    assert c[:, 6].sum() == g["counters"][1] + g["counters"][6]
+    assert np.all(c[2 * B:, 6] == n)
+    assert c[:, 5].sum() <= n * job.recurrences
     # the 1-in-1000 sample's curves estimate the full curves (statistical, loose)
     np.testing.assert_allclose(o["curves"][-100:, 0].sum() * 1000, c[-100:, 0].sum(), rtol=0.05)
 

@@ -258,11 +258,12 @@ zeus_status zeus_sim_run(zeus_sim *sim, void *cuda_stream);
  * handle's stream, synchronises that stream, and returns. */
 zeus_status zeus_sim_results(zeus_sim *sim, zeus_results *out);
 
-/* The replay outputs (curves, curves_fixed, the per-trial arrays, log, counters) into DEVICE
- * buffers only, enqueued on the handle's stream (the stream of the last zeus_sim_run) without
- * synchronising: consumers order on that stream.  ZEUS_E_INVALID (nothing queued) for a host
- * destination or a step-1 table / Pareto request, ZEUS_E_STATE before any run.  Fills
- * kernel_launches and curve_scale_bits; the event timings are zeus_sim_results'. */
+/* The replay outputs (curves, curves_fixed, the per-trial arrays, log, counters) into device or
+ * PINNED host buffers (cudaHostAlloc / cudaHostRegister), enqueued on the handle's stream (the
+ * stream of the last zeus_sim_run) without synchronising: consumers order on that stream, a host
+ * reader synchronises it first.  ZEUS_E_INVALID (nothing queued) for a pageable destination or a
+ * step-1 table / Pareto request, ZEUS_E_STATE before any run.  Fills kernel_launches and
+ * curve_scale_bits; the event timings are zeus_sim_results'. */
 zeus_status zeus_sim_results_async(zeus_sim *sim, zeus_results *out);
 
 /* curves [cells][R][7] (device) from fixed-point sums curves_fixed [cells][R][7][3] (device),

@@ -981,9 +981,10 @@ zeus_status zeus_sim_run(zeus_sim *s, void *stream) {
   return ZEUS_OK;
 }
 
-// The replay outputs into DEVICE buffers, enqueued on the handle's stream without waiting (the
-// multi-job bench step: six handles' curves handed to their consumers in stream order, no host
-// round trip per handle).  Everything is validated before any copy is queued.
+// The replay outputs into device or pinned host buffers, enqueued on the handle's stream without
+// waiting (the multi-job bench step: six handles' curves handed to their consumers in stream
+// order, no host round trip per handle; the e2e loop: every job's copies queued before one
+// wait).  Everything is validated before any copy is queued.
 zeus_status zeus_sim_results_async(zeus_sim *s, zeus_results *out) {
   NvtxRange nvtx_("zeus_sim_results_async");
   if (!s) return fail(nullptr, ZEUS_E_INVALID, "sim is NULL");
@@ -1015,13 +1016,15 @@ zeus_status zeus_sim_results_async(zeus_sim *s, zeus_results *out) {
     if (!r.dst) continue;
     cudaPointerAttributes pa{};
     const cudaError_t e = cudaPointerGetAttributes(&pa, r.dst);
-    if (e != cudaSuccess || (pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged)) {
+    if (e != cudaSuccess || (pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged &&
+                             pa.type != cudaMemoryTypeHost)) {
       cudaGetLastError();
-      return fail(s, ZEUS_E_INVALID, std::string("zeus_sim_results_async: ") + r.name + " is not device memory");
+      return fail(s, ZEUS_E_INVALID, std::string("zeus_sim_results_async: ") + r.name +
+                                         " is neither device nor pinned host memory");
     }
   }
   for (const Req &r : req)
-    if (r.dst && r.bytes) ZS_CUDA(s, cudaMemcpyAsync(r.dst, r.src->p, r.bytes, cudaMemcpyDeviceToDevice, s->stream));
+    if (r.dst && r.bytes) ZS_CUDA(s, cudaMemcpyAsync(r.dst, r.src->p, r.bytes, cudaMemcpyDefault, s->stream));
   out->kernel_launches = s->launches;
   out->curve_scale_bits = s->curve_bits;
   return ZEUS_OK;

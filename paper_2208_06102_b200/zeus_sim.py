@@ -224,8 +224,8 @@ class Simulation:
                             "final_arm", "counters"), out=None, enqueue_only=False):
         """Copies outputs into host numpy arrays (default) or into caller buffers given in
         ``out`` (numpy arrays or torch tensors, host or device).  enqueue_only: the replay
-        outputs into the device buffers of ``out`` on the run's stream, without waiting
-        (zeus_sim_results_async; no timings)."""
+        outputs into the device or pinned host buffers of ``out`` on the run's stream, without
+        waiting (zeus_sim_results_async; no timings)."""
         nc, R, n, B, S = self.ncells, self.R, self.shard_n, self.B, self.S
         shapes = {"curves": ((nc, R, CURVE_Q), np.float64),
                   "curves_fixed": ((nc, R, CURVE_Q, CURVE_LIMBS), np.int64), "tot_cost": ((n,), np.float64),

@@ -280,8 +280,12 @@ def test_results_async_device_buffers(zs):
     for k, v in dev.items():
         assert np.array_equal(v.cpu().numpy().view(np.asarray(ref[k]).dtype).reshape(np.shape(ref[k])),
                               np.asarray(ref[k])), k
-    with pytest.raises(zs.ZeusError, match="not device memory"):
-        sim.results(want=["tot_cost"], enqueue_only=True)
+    with pytest.raises(zs.ZeusError, match="neither device nor pinned"):
+        sim.results(want=["tot_cost"], enqueue_only=True)          # pageable numpy
+    pinned = torch.zeros(n, dtype=torch.float64).pin_memory()
+    sim.results(want=[], out={"tot_cost": pinned}, enqueue_only=True)
+    stream.synchronize()
+    assert np.array_equal(pinned.numpy(), np.asarray(ref["tot_cost"]))
     with pytest.raises(zs.ZeusError, match="replay outputs only"):
         sim.results(want=["c1"], enqueue_only=True)
     sim.close()

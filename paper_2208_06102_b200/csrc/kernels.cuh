@@ -499,7 +499,9 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   const float ckth = cert::kTheta + __int_as_float((127 - 23 + ckbits) << 23) * 1.000001f;
   double cref = 0.0;
   float c_trial = 0.0f;
-  const bool cert_on = (PHASE != 1 || ZS_PHASEA_CERT) && a.cert_draw;
+  // (under the early split phase A never draws: a lane stops at its first pure Thompson decision,
+  // so its fp32 table is not built here -- the Thompson phase builds its own)
+  const bool cert_on = (PHASE != 1 || ZS_PHASEA_CERT) && a.cert_draw && !(PHASE == 1 && a.early_split);
   auto f32_slot = [&](int arm_i, double2 ms) {              // (mu - ref, sigma) in fp32
     const double dm = ms.x - cref;
     s_f2[2 * ((arm_i >> 1) * TPB + tid) + (arm_i & 1)] =

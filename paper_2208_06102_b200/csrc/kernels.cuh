@@ -516,9 +516,13 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
     cref = lead >= 0 ? s_ms[lead * TPB + tid].x : 0.0;
     if (!(fabs(cref) < 1e30)) cref = 0.0;
     c_trial = __double2float_ru(fabs(cref) * 0x1p-52 + 0x1p-120);
-    for (int arm_i = 0; arm_i < 2 * cpairs2; ++arm_i) {
-      if (((ts_set & mature) >> arm_i) & 1u) f32_slot(arm_i, s_ms[arm_i * TPB + tid]);
-      else s_f2[2 * ((arm_i >> 1) * TPB + tid) + (arm_i & 1)] = make_float2(3.0e38f, 0.0f);
+    // every slot a sentinel (one 16-byte store per pair), then the survivors' values: this runs
+    // where a lane's pruning ends, divergently, so its length is paid per distinct ending
+    for (int k = 0; k < cpairs2; ++k)
+      reinterpret_cast<float4 *>(s_f2)[k * TPB + tid] = make_float4(3.0e38f, 0.0f, 3.0e38f, 0.0f);
+    for (uint32_t m = ts_set & mature; m; m &= m - 1u) {
+      const int arm_i = __ffs(m) - 1;
+      f32_slot(arm_i, s_ms[arm_i * TPB + tid]);
     }
   };
   if (PHASE == 2 && active) {                               // resume from phase A

@@ -407,6 +407,8 @@ __device__ __forceinline__ uint32_t above_mask(int c) { return c >= 31 ? 0u : ~(
 #define ZS_REPLAY_BOUNDS __maxnreg__(ZS_MAXNREG)
 #elif defined(ZS_P2_MIN_BLOCKS)
 #define ZS_REPLAY_BOUNDS __launch_bounds__(128, (PHASE == 2 ? ZS_P2_MIN_BLOCKS : 1))
+#elif defined(ZS_P1_MIN_BLOCKS)
+#define ZS_REPLAY_BOUNDS __launch_bounds__(128, (PHASE == 1 ? ZS_P1_MIN_BLOCKS : 1))
 #else
 #define ZS_REPLAY_BOUNDS __launch_bounds__(128)
 #endif

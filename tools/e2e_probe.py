@@ -41,6 +41,29 @@ def one(mode):
     return (t1 - t0) * 1e3, (t2 - t1) * 1e3, (t2 - t0) * 1e3
 
 
+def per_call():
+    """host time of each call type per job (median over steps), after a device sync"""
+    tl, tr, ts = [], [], []
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        for sm, st, (A, Th, pool, out) in zip(sims, streams, staged):
+            t0 = time.perf_counter()
+            Z.zeus_sim_load_profile(sm.h, A, Th, pool.shape[0], pool.shape[2], pool)
+            t1 = time.perf_counter()
+            sm.run(st)
+            t2 = time.perf_counter()
+            tl.append(t1 - t0)
+            tr.append(t2 - t1)
+        torch.cuda.synchronize()
+        for sm, (A, Th, pool, out) in zip(sims, staged):
+            t0 = time.perf_counter()
+            sm.results(want=[], out=out)
+            ts.append(time.perf_counter() - t0)
+    print(f"{cfg} per call (host, us): load_profile {np.median(tl) * 1e6:.1f}, run {np.median(tr) * 1e6:.1f}, "
+          f"results after sync {np.median(ts) * 1e6:.1f}")
+
+
+per_call()
 for mode in ("full", "noload"):
     for _ in range(3):
         one(mode)

@@ -207,6 +207,9 @@ struct ReplayArgs {
 // regroup keys: 2 x popcount of the survivor-pair mask + parity of its lowest pair (exact phase B),
 // or quads x kT0Keys + the recurrence the lane's Thompson phase starts at (thompson_kernel, t0 <= 2B)
 constexpr int kT0Keys = 65;
+#ifndef ZS_QUADS_DESC
+#define ZS_QUADS_DESC 0
+#endif
 constexpr int kBuckets = 9 * kT0Keys;
 #ifndef ZS_REGROUP_WINDOW
 #define ZS_REGROUP_WINDOW 8192
@@ -223,7 +226,13 @@ __device__ __forceinline__ uint32_t quads_of(uint32_t pairs) {
 // phase-B grouping key: lanes with the same number of survivor pairs and the same parity of
 // the lowest one draw the same number of Philox blocks at the same loop steps
 __device__ __forceinline__ int regroup_key(uint32_t pairs, int key_quads, int t0) {
+#if ZS_QUADS_DESC
+  // thompson_kernel: quads (descending: a window's slow warps are dispatched first, so the launch
+  // ends on short ones), then the start recurrence
+  if (key_quads) return (8 - __popc(quads_of(pairs))) * kT0Keys + t0;
+#else
   if (key_quads) return __popc(quads_of(pairs)) * kT0Keys + t0;   // thompson_kernel: quads, start
+#endif
   return pairs ? 2 * __popc(pairs) + ((__ffs(pairs) - 1) & 1) : 0;
 }
 

@@ -394,6 +394,18 @@ def test_f2_ablations(zs, oracle, draw):
                          job.trials, logs=True)
 
 
+def test_layout4_with_ablation_and_policy_cells(zs, oracle):
+    """Layout 4 (the early split) asked for on launches it does not apply to -- ablation cells
+    (the exact phase B), the Default / Grid Search policies next to Zeus (f1) -- gives every
+    trial the oracle's bits."""
+    for name in ("f2", "f1"):
+        for job in synth.config(name, trials=1500)[:2]:
+            g = run_gpu(zs, job.workload, job.cells, job.trials, job.recurrences, log=True, layout=4)
+            for ci, c in enumerate(job.cells):
+                compare_cell(oracle, g, job.workload, c, ci, np.arange(job.trials), job.recurrences,
+                             job.trials, logs=True)
+
+
 @pytest.mark.parametrize("draw", [0, 2])
 def test_f3_concurrent_submissions(zs, oracle, draw):
     """concurrent submissions under Poisson arrival schedules (§4.4

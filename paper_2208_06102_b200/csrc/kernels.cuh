@@ -207,6 +207,9 @@ struct ReplayArgs {
 // regroup keys: 2 x popcount of the survivor-pair mask + parity of its lowest pair (exact phase B),
 // or quads x kT0Keys + the recurrence the lane's Thompson phase starts at (thompson_kernel, t0 <= 2B)
 constexpr int kT0Keys = 65;
+#ifndef ZS_CONC_MIN
+#define ZS_CONC_MIN 1
+#endif
 #ifndef ZS_QUADS_DESC
 #define ZS_QUADS_DESC 0
 #endif
@@ -1540,6 +1543,26 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
       }
     }
   };
+#if ZS_CONC_MIN
+  // the queue's earliest entry by (completion, submission), kept up to date: a scan only after a
+  // completion, none per submission check
+  int m_i = -1;
+  double m_done = kInf;
+  auto rescan = [&]() {
+    m_i = -1;
+    for (int i = 0; i < nq; ++i)
+      if (m_i < 0 || q_done(i) < q_done(m_i) || (q_done(i) == q_done(m_i) && q_seq(i) < q_seq(m_i))) m_i = i;
+    m_done = m_i >= 0 ? q_done(m_i) : kInf;
+  };
+  auto complete_earliest = [&]() {                          // by (completion, submission)
+    const int e = m_i;
+    complete(e);
+    --nq;                                                    // move the last entry into slot e
+    q_done(e) = q_done(nq); q_C(e) = q_C(nq); q_seq(e) = q_seq(nq); q_b(e) = q_b(nq);
+    q_flags(e) = q_flags(nq);
+    rescan();
+  };
+#else
   auto complete_earliest = [&]() {                          // by (completion, submission)
     int e = 0;
     for (int i = 1; i < nq; ++i)
@@ -1549,6 +1572,7 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
     q_done(e) = q_done(nq); q_C(e) = q_C(nq); q_seq(e) = q_seq(nq); q_b(e) = q_b(nq);
     q_flags(e) = q_flags(nq);
   };
+#endif
 
   int s = 0;
   U4 rw{0u, 0u, 0u, 0u};
@@ -1559,12 +1583,16 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
       while ((long long)(s + 1) * R <= (long long)t * S) ++s;
     if (active) {
       const double tau = __ldg(arr + t);
+#if ZS_CONC_MIN
+      while (m_i >= 0 && m_done <= tau) complete_earliest();   // runs finished by this submission
+#else
       for (;;) {                                             // runs finished by this submission
         bool any = false;
         for (int i = 0; i < nq; ++i) any |= q_done(i) <= tau;
         if (!any) break;
         complete_earliest();
       }
+#endif
       while (nq >= kMaxOutstanding) complete_earliest();
       if ((t & 3) == 0) rw = replica_words(cp.key0, cp.key1, trial, t);
       const bool ts_dec = in_ts;
@@ -1672,6 +1700,11 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
       const bool conv = (E > 0) && !stopped;
       q_done(nq) = tau + Tm; q_C(nq) = C; q_seq(nq) = t; q_b(nq) = b;
       q_flags(nq) = (conv ? 1u : 0u) | (walk_issue ? 2u : 0u);
+#if ZS_CONC_MIN
+      // the new entry has the largest submission index: it is the earliest only if it completes
+      // strictly first
+      if (m_i < 0 || tau + Tm < m_done) { m_i = nq; m_done = tau + Tm; }
+#endif
       ++nq;
       const uint32_t flags = (stopped ? 1u : 0u) | (conv ? 2u : 0u) | (prof_now ? 4u : 0u) |
                              (ts_dec ? 8u : 0u);

@@ -298,6 +298,11 @@ __device__ __forceinline__ void red_add_u64(long long *p, unsigned long long v, 
 __device__ __forceinline__ void red_add_u32(uint32_t *p, uint32_t v) {
   asm volatile("red.global.add.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
+// the same, predicated in PTX (no branch around it): the increment is 1 when pred holds
+__device__ __forceinline__ void red_inc_u32_if(uint32_t *p, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.global.add.u32 [%0], 1;\n\t}"
+               :: "l"(p), "r"((uint32_t)pred) : "memory");
+}
 __device__ __forceinline__ void curve_accumulate(long long *curves, int t, int lane, double vC,
                                                  double vE, double vT, double vReg, int vPacked,
                                                  double scale) {

@@ -37,6 +37,9 @@ namespace zs {
 #ifndef ZS_CURVES_REMAT
 #define ZS_CURVES_REMAT 0     // the curve-slot pointer recomputed on the stopped-run path: -1.3 % (r02bj)
 #endif
+#ifndef ZS_RED_PRED
+#define ZS_RED_PRED 0
+#endif
 #ifndef ZS_PHILOX_WIDE
 #define ZS_PHILOX_WIDE 1
 #endif
@@ -291,7 +294,7 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   for (int t = tw; t < R; ++t) {
     const bool live = EARLY ? t >= t0 : active;             // this lane's trial decides at t
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
-    int vPacked = 0, b = 0, hkey = -1;
+    int vPacked = 0, b = 0, hkey = 0;                      // hkey: counted only when live
     double C = 0.0, y_old = 0.0;
     if (S > 1)
       while ((long long)(s + 1) * R <= (long long)t * S) ++s;
@@ -451,7 +454,11 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
     {
       const bool special = live && (vPacked & 1);
 #ifndef ZS_DIAG_NOHIST
+#if ZS_RED_PRED
+      red_inc_u32_if(hrow + (uint32_t)hkey, live && !special);
+#else
       if (live && !special) red_add_u32(hrow + hkey, 1u);
+#endif
 #endif
       hrow += hstride;
       if (__any_sync(0xffffffffu, special)) {

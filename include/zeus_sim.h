@@ -224,7 +224,9 @@ typedef struct {
 } zeus_results;
 
 /* Validates job, cells and opts (every violated invariant is reported),
- * selects cuda_device, allocates device memory.  *out is NULL on failure. */
+ * selects cuda_device, allocates device memory.  *out is NULL on failure.
+ * ZEUS_E_UNSUPPORTED when the shard holds 2^32 or more Observe records (the
+ * trials of every cell x |B|): split it into smaller shards. */
 zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t num_cells,
                             const zeus_run_opts *opts, int32_t cuda_device, zeus_sim **out);
 

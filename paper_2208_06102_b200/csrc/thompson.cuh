@@ -37,8 +37,11 @@ namespace zs {
 #ifndef ZS_CURVES_REMAT
 #define ZS_CURVES_REMAT 0     // the curve-slot pointer recomputed on the stopped-run path: -1.3 % (r02bj)
 #endif
+#ifndef ZS_REC32
+#define ZS_REC32 1         // 32-bit Observe-record index (CFG5 +1.5 %, session r02cq)
+#endif
 #ifndef ZS_RED_PRED
-#define ZS_RED_PRED 0
+#define ZS_RED_PRED 1      // the histogram RED predicated, no branch (+0.2 % with REC32, r02cq)
 #endif
 #ifndef ZS_PHILOX_WIDE
 #define ZS_PHILOX_WIDE 1
@@ -210,13 +213,20 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   const int64_t trial = cp.begin + jj;
   const size_t o = (size_t)(cp.out_off + jj);
   ArmStat *st_g = a.st + o * B;
+  const uint32_t ob = (uint32_t)(o * B);                    // ZS_REC32: the trial's first record
   ArmStat *s_rec = reinterpret_cast<ArmStat *>(smem + tab_end +
                                                (size_t)((((B + 1) >> 1) + 1) & ~1) * 16 * TPB + 16 * (size_t)TPB);
   const int Nw = WIN ? cp.window : 0;                       // window of this cell (0: none)
   auto nwin = [&](int cnt) { return (WIN && Nw > 0) ? min(cnt, Nw) : cnt; };
   auto rec = [&](int arm_i) -> ArmStat & {
     if constexpr (SREC) return s_rec[(size_t)arm_i * TPB + tid];
+#if ZS_REC32
+    // 32-bit record index (the host guarantees shard * B < 2^32): one add and one wide multiply
+    // from the uniform base, instead of 64-bit pointer arithmetic on every record switch
+    else return *reinterpret_cast<ArmStat *>(reinterpret_cast<char *>(a.st) + (uint64_t)(ob + (uint32_t)arm_i) * 32u);
+#else
     else return st_g[arm_i];
+#endif
   };
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
 #if !ZS_CURVES_REMAT

@@ -356,6 +356,17 @@ zeus_status zeus_sim_create(const zeus_job *job, const zeus_cell *cells, int32_t
     if (opts->graph != 0 && opts->graph != 1) E.add(ZEUS_E_INVALID, "graph must be 0 or 1");
     if (opts->draw < 0 || opts->draw > 2) E.add(ZEUS_E_INVALID, "draw must be 0, 1 or 2");
   }
+  if (E.code == ZEUS_OK) {              // the Observe records are indexed in 32 bits (thompson.cuh)
+    uint64_t recs = 0;
+    for (int i = 0; i < num_cells; ++i) {
+      const int64_t b = std::min(opts->shard_begin, cells[i].trials);
+      const int64_t e = opts->shard_end < 0 ? cells[i].trials : std::min(opts->shard_end, cells[i].trials);
+      recs += (uint64_t)std::max<int64_t>(0, e - b) * (uint64_t)job->num_batch_sizes;
+    }
+    if (recs >= (1ull << 32))
+      E.add(ZEUS_E_UNSUPPORTED, "this shard holds >= 2^32 Observe records (trials x batch sizes over all "
+                                "cells); split it into smaller shards");
+  }
   if (E.code != ZEUS_OK) return fail(nullptr, E.code, E.s);
 
   int ndev = 0;

@@ -97,6 +97,17 @@ def test_unsupported_sizes(zs):
     assert e.value.status == 6 and "32 batch sizes" in str(e.value)
 
 
+def test_record_index_limit(zs):
+    """The Thompson phase indexes the Observe records in 32 bits: a shard with >= 2^32 records
+    (trials x |B| over every cell) is refused before anything is allocated."""
+    job, keep = _job(zs, bs=[8, 16, 32, 64], b0=1)
+    cells = [zs.zeus_cell(0.5, 2.0, 0, 0.0, math.inf, 1, 2 ** 30, 0, 0, None)]   # 2^30 x 4 = 2^32
+    opts = zs.zeus_run_opts(C.sizeof(zs.zeus_run_opts), 10, 0, -1, 0, 0)
+    with pytest.raises(zs.ZeusError) as e:
+        zs.zeus_sim_create(job, cells, opts)
+    assert e.value.status == 6 and "2^32 Observe records" in str(e.value)
+
+
 def test_abi_guard(zs):
     job, keep = _job(zs)
     job.struct_size = 3

@@ -59,6 +59,8 @@ VARIANTS = {
     "winfit": (["ZS_WIN_POOL_FIT=1"], []),
     "qdesc": (["ZS_QUADS_DESC=1"], []),
     "redpred": (["ZS_RED_PRED=1"], []),
+    "rec32": (["ZS_REC32=1"], []),
+    "rec32_rp": (["ZS_REC32=1", "ZS_RED_PRED=1"], []),
     "p1b5": (["ZS_P1_MIN_BLOCKS=5"], []),
     "p1b6": (["ZS_P1_MIN_BLOCKS=6"], []),
     "winpf_fit": (["ZS_WIN_PREFETCH=1", "ZS_WIN_POOL_FIT=1"], []),

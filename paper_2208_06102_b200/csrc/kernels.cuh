@@ -244,6 +244,17 @@ struct __align__(16) ArmStat {    // Observe state of one arm of one trial (NC-6
   int32_t cnt, pad;               // observations ever
 };
 
+// The Observe records of one trial, [trial][arm] 32 B each, addressed by a 32-bit index from the
+// uniform base (zeus_sim_create keeps shard x |B| < 2^32): one add and one wide multiply per
+// access instead of 64-bit pointer arithmetic (thompson.cuh ZS_REC32)
+struct RecRef {
+  ArmStat *base;
+  uint32_t ob;
+  __device__ __forceinline__ ArmStat &operator[](int arm) const {
+    return *reinterpret_cast<ArmStat *>(reinterpret_cast<char *>(base) + (uint64_t)(ob + (uint32_t)arm) * 32u);
+  }
+};
+
 // per-trial scalar state carried from phase A to phase B (96 B)
 struct Carry {
   double best, totC, totE, totT;
@@ -482,7 +493,7 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   if (PHASE == 2) jj = active ? a.perm[cp.out_off + j0 + tid] : 0;
   const int64_t trial = cp.begin + jj;
   const size_t o = (size_t)(cp.out_off + jj);              // this trial's row in the outputs/state
-  ArmStat *st = a.st + o * B;
+  const RecRef st{a.st, (uint32_t)(o * B)};               // the trial's Observe records (32-bit index)
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
   long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
   constexpr bool kHist = !ABL;                              // counted curves (see ReplayArgs::hist)
@@ -1045,7 +1056,7 @@ __global__ void __launch_bounds__(128) replay_group_kernel(ReplayArgs a) {
   const bool leader = l == 0;
   const int64_t trial = cp.begin + jj;
   const size_t o = (size_t)(cp.out_off + (active ? jj : 0));
-  ArmStat *st = a.st + o * B;
+  const RecRef st{a.st, (uint32_t)(o * B)};               // the trial's Observe records (32-bit index)
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
   long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
   const int HB = 4 * B * K;                                 // counted curves (ReplayArgs::hist)
@@ -1414,7 +1425,7 @@ __global__ void __launch_bounds__(128) concurrent_kernel(ConcArgs a) {
   const bool active = jj < cp.n;
   const int64_t trial = cp.begin + jj;
   const size_t o = (size_t)(cp.out_off + jj);
-  ArmStat *st = a.st + o * B;
+  const RecRef st{a.st, (uint32_t)(o * B)};               // the trial's Observe records (32-bit index)
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
   long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
@@ -1784,7 +1795,7 @@ __global__ void __launch_bounds__(128) variant_kernel(ConcArgs a) {
   const bool active = jj < cp.n;
   const int64_t trial = cp.begin + jj;
   const size_t o = (size_t)(cp.out_off + jj);
-  ArmStat *st = a.st + o * B;
+  const RecRef st{a.st, (uint32_t)(o * B)};               // the trial's Observe records (32-bit index)
   const int warp_global = blockIdx.x * (TPB >> 5) + (tid >> 5);
   long long *curves = a.curve_slots + ((size_t)cell * a.nslot + (warp_global % a.nslot)) * (size_t)R * kRow;
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);

@@ -37,6 +37,9 @@ namespace zs {
 #ifndef ZS_CURVES_REMAT
 #define ZS_CURVES_REMAT 0     // the curve-slot pointer recomputed on the stopped-run path: -1.3 % (r02bj)
 #endif
+#ifndef ZS_HIST32
+#define ZS_HIST32 0
+#endif
 #ifndef ZS_REC32
 #define ZS_REC32 1         // 32-bit Observe-record index (CFG5 +1.5 %, session r02cq)
 #endif
@@ -239,8 +242,14 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   // were grouped by t0 within their quad count, so a warp's lanes mostly share it)
   const int t0 = EARLY ? (active ? a.carry[o].t0 : 0x7fffffff) : a.t_split;
   const int tw = EARLY ? min(R, __reduce_min_sync(0xffffffffu, t0)) : a.t_split;
+#if ZS_HIST32
+  // the row as a 32-bit element index from the uniform base (the histogram has < 2^32 bins)
+  uint32_t hrow = (uint32_t)(((size_t)cell * R * a.nhslot + (warp_global % a.nhslot)) * (size_t)HB +
+                             (size_t)tw * hstride + 2 * B * K);
+#else
   uint32_t *hrow = a.hist + ((size_t)cell * R * a.nhslot + (warp_global % a.nhslot)) * (size_t)HB +
                    (size_t)tw * hstride + 2 * B * K;
+#endif
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);
   const float kInfF = __int_as_float(0x7f800000);
 
@@ -465,12 +474,16 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
       const bool special = live && (vPacked & 1);
 #ifndef ZS_DIAG_NOHIST
 #if ZS_RED_PRED
+#if ZS_HIST32
+      red_inc_u32_if(a.hist + (hrow + (uint32_t)hkey), live && !special);
+#else
       red_inc_u32_if(hrow + (uint32_t)hkey, live && !special);
+#endif
 #else
       if (live && !special) red_add_u32(hrow + hkey, 1u);
 #endif
 #endif
-      hrow += hstride;
+      hrow += (uint32_t)hstride;
       if (__any_sync(0xffffffffu, special)) {
         // a stopped run's pseudo-regret and counts (stop | optimal << 8 | Thompson << 16) are read
         // only here (the counted runs take theirs from the histogram fold)

@@ -37,6 +37,9 @@ namespace zs {
 #ifndef ZS_CURVES_REMAT
 #define ZS_CURVES_REMAT 0     // the curve-slot pointer recomputed on the stopped-run path: -1.3 % (r02bj)
 #endif
+#ifndef ZS_ACT_REG
+#define ZS_ACT_REG 1        // CFG5 +0.4 % (session r02cv)
+#endif
 #ifndef ZS_HIST32
 #define ZS_HIST32 0
 #endif
@@ -212,6 +215,12 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   uint32_t *s_rw = reinterpret_cast<uint32_t *>(smem + tab_end + (size_t)((((B + 1) >> 1) + 1) & ~1) * 16 * TPB);
 
   const bool active = j0 + tid < cp.n;
+#if ZS_ACT_REG
+  // `active` as an opaque 32-bit register: otherwise ptxas recomputes the 64-bit compare
+  // j0 + tid < n (three ISETP) at every use in the loop
+  uint32_t act_r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(act_r) : "r"(active ? 1u : 0u));
+#endif
   const int64_t jj = active ? a.perm[cp.out_off + j0 + tid] : 0;
   const int64_t trial = cp.begin + jj;
   const size_t o = (size_t)(cp.out_off + jj);
@@ -311,7 +320,11 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   const uint32_t tlo = (uint32_t)trial, thi = (uint32_t)((uint64_t)trial >> 32);
 #endif
   for (int t = tw; t < R; ++t) {
+#if ZS_ACT_REG
+    const bool live = EARLY ? t >= t0 : act_r != 0u;        // this lane's trial decides at t
+#else
     const bool live = EARLY ? t >= t0 : active;             // this lane's trial decides at t
+#endif
     double vC = 0.0, vE = 0.0, vT = 0.0, vReg = 0.0;
     int vPacked = 0, b = 0, hkey = 0;                      // hkey: counted only when live
     double C = 0.0, y_old = 0.0;

@@ -37,11 +37,23 @@ constexpr int kQ = 7;             // curve quantities
 constexpr int kCounters = 14;   // 9 contract events + transforms, Philox blocks, pairs screened / in fp32,
                                 // draws certified in fp32, exact fallbacks (thompson_kernel)
 
+#ifndef ZS_ARMC_PACK
+#define ZS_ARMC_PACK 0
+#endif
+#if ZS_ARMC_PACK
+// the fields every decision reads (c1, t1, e1, p*) in the first 32 bytes: two 16-byte loads
+struct __align__(16) ArmConst {   // per (cell, arm), 64 B
+  double c1, t1, e1;
+  int32_t pstar, pad0;
+  double cP, tP, eP, pad1;
+};
+#else
 struct ArmConst {                 // per (cell, arm), 64 B
   double c1, t1, e1, cP, tP, eP;
   int32_t pstar, pad0;
   double pad1;
 };
+#endif
 
 struct CellParam {                // per cell
   double eta, beta, prec0, pm0;

@@ -63,6 +63,7 @@ VARIANTS = {
     "hist32": (["ZS_HIST32=1"], []),
     "actreg": (["ZS_ACT_REG=1"], []),
     "noinit": (["ZS_NOINIT=1"], []),
+    "armpack": (["ZS_ARMC_PACK=1"], []),
     "rec32_rp": (["ZS_REC32=1", "ZS_RED_PRED=1"], []),
     "p1b5": (["ZS_P1_MIN_BLOCKS=5"], []),
     "p1b6": (["ZS_P1_MIN_BLOCKS=6"], []),

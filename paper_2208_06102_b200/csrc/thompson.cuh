@@ -37,6 +37,9 @@ namespace zs {
 #ifndef ZS_CURVES_REMAT
 #define ZS_CURVES_REMAT 0     // the curve-slot pointer recomputed on the stopped-run path: -1.3 % (r02bj)
 #endif
+#ifndef ZS_TPB_CONST
+#define ZS_TPB_CONST 0
+#endif
 #ifndef ZS_NOINIT
 #define ZS_NOINIT 1         // CFG5 +0.2 %, CFG3 +0.5 % (session r02cw)
 #endif
@@ -158,7 +161,14 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   __shared__ __align__(8) uint64_t mbar;
   const int cell = blockIdx.y;
   const CellParam cp = a.cells[cell];
+#if ZS_TPB_CONST
+  // every Thompson launch has 128-thread blocks (zeus_sim.cu thompson_launch): the shared-memory
+  // indexing folds to shifts and immediate offsets
+  constexpr int TPB = 128;
+  const int tid = threadIdx.x;
+#else
   const int tid = threadIdx.x, TPB = blockDim.x;
+#endif
   const int64_t j0 = (int64_t)blockIdx.x * TPB;
   if (j0 >= cp.n || cp.policy != 0 || cp.conc) return;
   auto k0f = [&](int r) -> uint32_t {

@@ -105,6 +105,17 @@ struct Argmin32 {
     smax = fmaxf(smax, fmaxf(ms.y, ms.w));
     rsqmax = fmaxf(rsqmax, rsq);
   }
+  // the same without the sigma maximum (the caller keeps an upper bound of it, certified_ub)
+  __device__ __forceinline__ void pair_nos(int a0, float4 ms, float z0, float z1, float rsq, uint32_t keep) {
+    const float t0 = fmaf(ms.y, z0, ms.x);
+    const float t1 = fmaf(ms.w, z1, ms.z);
+    const float k0 = __int_as_float((__float_as_int(t0) & (int)keep) | a0);
+    const float k1 = __int_as_float((__float_as_int(t1) & (int)keep) | (a0 + 1));
+    const float lo = fminf(k0, k1), hi = fmaxf(k0, k1);
+    m2 = fminf(fminf(m2, hi), fmaxf(m1, lo));
+    m1 = fminf(m1, lo);
+    rsqmax = fmaxf(rsqmax, rsq);
+  }
   // the same with the pair's eligibility bits (arm a0: bit 0, a0 + 1: bit 1): an ineligible
   // arm's theta becomes the non-survivor sentinel 3e38 (f3 / f2v kernels, whose fp32 tables hold
   // every mature arm)
@@ -121,8 +132,12 @@ struct Argmin32 {
   // kth = kTheta + 2^(bits-23) (1 + 2^-20).  NaN anywhere fails the test; m2 = +inf (one
   // survivor) passes whenever S is finite.
   __device__ __forceinline__ bool certified(float c_trial, float kth) const {
+    return certified_ub(smax, c_trial, kth);
+  }
+  // with any upper bound sub >= every survivor's sigma32 (a larger bound only widens S)
+  __device__ __forceinline__ bool certified_ub(float sub, float c_trial, float kth) const {
     const float ez = __fmaf_ru(rsqmax, kZb, kZr * kRMax * 1.000001f);
-    const float S = __fmaf_ru(__fmul_ru(smax, kSigScale), __fadd_ru(ez, kSig), c_trial);
+    const float S = __fmaf_ru(__fmul_ru(sub, kSigScale), __fadd_ru(ez, kSig), c_trial);
     const float lo2 = (m2 == __int_as_float(0x7f800000)) ? m2 : __fmaf_rd(-kth, fabsf(m2), m2);
     const float hi1 = __fmaf_ru(kth, fabsf(m1), m1);
     return __fsub_rd(lo2, hi1) > __fmul_ru(2.0f, S);

@@ -40,6 +40,9 @@ namespace zs {
 #ifndef ZS_TPB_CONST
 #define ZS_TPB_CONST 0
 #endif
+#ifndef ZS_SMAX_UB
+#define ZS_SMAX_UB 1        // CFG2 +2.5 %, CFG3 +0.4 %, CFG5 +0.2 %, CFG4 -0.5 % (session r02da)
+#endif
 #ifndef ZS_NOINIT
 #define ZS_NOINIT 1         // CFG5 +0.2 %, CFG3 +0.5 % (session r02cw)
 #endif
@@ -282,6 +285,11 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
   uint32_t n_fall = 0;              // exact fallbacks (every phase-B decision samples and observes)
   double ref = 0.0;
   float c_trial = 0.0f;
+#if ZS_SMAX_UB
+  // an upper bound of every survivor's fp32 sigma (the certificate's smax): raised at each
+  // Observe, recomputed exactly every 64 recurrences, so the quad loop does not track it
+  float smax_ub = 0.0f;
+#endif
   const int npairs = (B + 1) >> 1;
   const int npairs2 = (npairs + 1) & ~1;                    // whole quads (padding: non-survivors)
   // key packing (certify.cuh Argmin32): the arm index in the low `bits` mantissa bits
@@ -319,6 +327,9 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
         v = (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y) : make_float2(0.0f, kInfF);
       }
       s_f2[2 * ((b >> 1) * TPB + tid) + (b & 1)] = v;
+#if ZS_SMAX_UB
+      smax_ub = fmaxf(smax_ub, v.y);
+#endif
     }
   }
 
@@ -383,9 +394,15 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
           const float4 m0 = s_f[(2 * qd) * TPB + tid];
           const float4 m1 = s_f[(2 * qd + 1) * TPB + tid];
           cert::normal_pair32(x.x, x.y, z0, z1, rsq);
+#if ZS_SMAX_UB
+          am.pair_nos(4 * qd, m0, z0, z1, rsq, keep);
+          cert::normal_pair32(x.z, x.w, z0, z1, rsq);
+          am.pair_nos(4 * qd + 2, m1, z0, z1, rsq, keep);
+#else
           am.pair(4 * qd, m0, z0, z1, rsq, keep);
           cert::normal_pair32(x.z, x.w, z0, z1, rsq);
           am.pair(4 * qd + 2, m1, z0, z1, rsq, keep);
+#endif
         };
         uint32_t qm = quads;
         while (qm) {                                        // the same trip count in a warp
@@ -404,7 +421,11 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
           quad_argmin(qa, quad_block(qa));
         }
         b = am.arg(keep);
+#if ZS_SMAX_UB
+        if (!am.certified_ub(smax_ub, c_trial, kth) || a.force_exact) {
+#else
         if (!am.certified(c_trial, kth) || a.force_exact) {
+#endif
           // the contract's exact draw (NC-3/NC-4): fp64 posteriors from the Observe records
           // (the cached record is the newest of its arm), every survivor pair transformed,
           // strict < in ascending arm order
@@ -559,8 +580,16 @@ __device__ __forceinline__ void thompson_body(const ReplayArgs &a) {
       qc.cnt += 1;
       const double2 ms = posterior(qc.sh, qc.S1, qc.S2, n + 1, cp.prec0, cp.pm0);
       const double dm = ms.x - ref;
-      s_f2[2 * ((b >> 1) * TPB + tid) + (b & 1)] =
-          (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y) : make_float2(0.0f, kInfF);
+      const float2 vn = (fabs(dm) < 1e30 && ms.y < 1e30) ? make_float2((float)dm, (float)ms.y) : make_float2(0.0f, kInfF);
+      s_f2[2 * ((b >> 1) * TPB + tid) + (b & 1)] = vn;
+#if ZS_SMAX_UB
+      smax_ub = fmaxf(smax_ub, vn.y);
+      if ((t & 63) == 63) {                                 // tighten: the exact maximum again
+        float m = 0.0f;
+        for (int k = 0; k < 2 * npairs2; ++k) m = fmaxf(m, s_f2[2 * ((k >> 1) * TPB + tid) + (k & 1)].y);
+        smax_ub = m;
+      }
+#endif
     }
   }
   if (active && qc_b >= 0) rec(qc_b) = qc;

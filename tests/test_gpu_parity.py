@@ -461,6 +461,33 @@ def test_cuda_graph_runs_identical(zs):
         g.close()
 
 
+def test_cuda_graph_with_early_split_and_async_results(zs):
+    """A captured run of the early-split schedule (layout 4: pruning-only phase A, (quads, t0)
+    regroup, thompson_kernel<..., EARLY>) replays with the direct launches' bits, and its outputs
+    handed over by zeus_sim_results_async match."""
+    import torch
+
+    want = ["digest", "tot_cost", "curves"]
+    job = synth.config("cfg3", trials=1500)[0]
+    cells = job.cells[:3]
+    direct = zs.Simulation(job.workload, cells, job.trials, job.recurrences, layout=4).load_profile()
+    ref = direct.run().results(want=want)
+    direct.close()
+    g = zs.Simulation(job.workload, cells, job.trials, job.recurrences, layout=4, graph=True).load_profile()
+    stream = torch.cuda.Stream()
+    for _ in range(2):
+        g.run(stream)
+        dev = {"digest": torch.zeros(g.shard_n, dtype=torch.int64, device="cuda"),
+               "tot_cost": torch.zeros(g.shard_n, dtype=torch.float64, device="cuda"),
+               "curves": torch.zeros((len(cells), g.R, 7), dtype=torch.float64, device="cuda")}
+        g.results(want=[], out=dev, enqueue_only=True)
+        stream.synchronize()
+        assert np.array_equal(dev["digest"].cpu().numpy().view(np.uint64), ref["digest"])
+        assert np.array_equal(dev["tot_cost"].cpu().numpy(), ref["tot_cost"])
+        assert np.array_equal(dev["curves"].cpu().numpy(), ref["curves"])
+    g.close()
+
+
 def test_cuda_graph_reload_new_values_same_shape(zs):
     """A same-shaped reload with different values keeps the captured graph only where nothing
     captured changed: a trace 64x slower changes the curves' fixed-point scale F (a kernel

@@ -219,6 +219,9 @@ struct ReplayArgs {
 // regroup keys: 2 x popcount of the survivor-pair mask + parity of its lowest pair (exact phase B),
 // or quads x kT0Keys + the recurrence the lane's Thompson phase starts at (thompson_kernel, t0 <= 2B)
 constexpr int kT0Keys = 65;
+#ifndef ZS_ACT_REG_A
+#define ZS_ACT_REG_A 1      // CFG5 +0.25 % (session r02dc)
+#endif
 #ifndef ZS_CONC_MIN
 #define ZS_CONC_MIN 1
 #endif
@@ -591,7 +594,14 @@ __global__ void ZS_REPLAY_BOUNDS replay_kernel(ReplayArgs a) {
   // repeats its arm, and then the decision needs no load of the record (same values)
   ArmStat qc{0.0, 0.0, 0.0, 0, 0};
   int qc_b = -1;
+#if ZS_ACT_REG_A
+  // `active` through an opaque register (ptxas otherwise re-evaluates the 64-bit bound check)
+  uint32_t act_r;
+  asm volatile("mov.u32 %0, %1;" : "=r"(act_r) : "r"(active ? 1u : 0u));
+  bool live = act_r != 0u;                                  // phase A under early_split: until t0
+#else
   bool live = active;                                       // phase A under early_split: until t0
+#endif
   int t0 = t_end;
   for (int t = t_begin; t < t_end; ++t) {
     if (PHASE == 1 && a.early_split) {

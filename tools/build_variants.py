@@ -66,6 +66,7 @@ VARIANTS = {
     "armpack": (["ZS_ARMC_PACK=1"], []),
     "tpb128": (["ZS_TPB_CONST=1"], []),
     "smaxub": (["ZS_SMAX_UB=1"], []),
+    "actregA": (["ZS_ACT_REG_A=1"], []),
     "rec32_rp": (["ZS_REC32=1", "ZS_RED_PRED=1"], []),
     "p1b5": (["ZS_P1_MIN_BLOCKS=5"], []),
     "p1b6": (["ZS_P1_MIN_BLOCKS=6"], []),
